@@ -1,0 +1,435 @@
+"""bench.py — verified log entries/sec of the B200 batch verifier.
+
+Contract (see the task's bench contract and SURVEY.md §8d):
+  python bench.py --gpus N --steps K --warmup W [--impl reference]
+One process per GPU (torchrun for N > 1). A "step" is one full coarse-mode
+PAVer pass (BASELINE.json config 2: 2^26 x 32-byte entries per GPU,
+n2 = 256 -> 2^18 epochs, suite 1 / SHA-256) over a synthetic log already
+resident in HBM: K0 seed derivation -> K1+K2 fused hash + segmented modular
+sum -> e-hat fold -> K3 ristretto255 group check -> verdict to host. For
+N > 1 each rank verifies its own contiguous epoch shard (weak scaling) and
+the per-shard partial e-hat (32 B) is combined with an NCCL all-gather and a
+rank-ordered device fold before the single group check on rank 0.
+
+Extra keys: e2e (same metric through the C-ABI with the log in pinned HOST
+memory, H2D inside the timed region), roofline (integer pipe, measured
+peak), cpu_baseline (the reference's own paver, compiled from
+/root/reference into oracle/_ref, on this host's cores), clocks, gpu_launches.
+"""
+import argparse
+import ctypes
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "verified log entries/sec (device-timed) at 1/2/4/8 B200 vs CPU ref"
+L_ORDER = 2**252 + 27742317777372353535851937790883648493
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--log2n", type=int, default=26, help="entries per GPU = 2^log2n")
+    ap.add_argument("--n2", type=int, default=256)
+    ap.add_argument("--suite", type=int, default=1)
+    ap.add_argument("--entry-len", type=int, default=32)
+    ap.add_argument("--seed", type=int, default=0x5EED)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-log2n", type=int, default=21)
+    return ap.parse_args()
+
+
+def config_dict(a, n_gpus):
+    return {
+        "workload": f"BASELINE config 2: 2^{a.log2n} x {a.entry_len}-byte entries per GPU, coarse single-aggregate "
+                    f"PAVer (suite {a.suite}, n2={a.n2}), inputs resident in HBM",
+        "entries_per_gpu": 1 << a.log2n,
+        "entry_len": a.entry_len,
+        "n2": a.n2,
+        "suite": a.suite,
+        "mode": "coarse",
+        "parallelism": f"epoch-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
+        "l2": "inputs larger than L2 (2 GiB log per GPU vs 126 MB L2)",
+    }
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(s[0]) for s in self.samples if s[0].isdigit()]
+        mx = [int(s[1]) for s in self.samples if s[1].isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU reference
+def run_ref_tool(log2n, n2, entry_len, suite, seed, reps, mode="coarse"):
+    if not os.path.exists(REF_TOOL):
+        return None
+    cmd = [REF_TOOL, "bench", str(suite), str(log2n), str(n2), str(entry_len), "0", str(seed), str(reps), mode]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    if out.returncode != 0:
+        raise RuntimeError(f"ref_tool failed: {out.stderr.strip()}")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(a):
+    r = run_ref_tool(a.cpu_log2n, a.n2, a.entry_len, a.suite, a.seed, 1)
+    if r is None:
+        return None
+    return {"value": round(r["eps_best"], 1), "unit": "entries/s", "cores": r["workers"],
+            "kind": "reference",
+            "sample": f"reference poslo::paver (proj/src/batch_verify.cpp:64-87, OpenSSL 3 + libsodium 1.0.20) "
+                      f"on an epoch-aligned 2^{a.cpu_log2n}-entry prefix of the same synthetic log "
+                      f"(n2={a.n2}, suite {a.suite}), workers={r['workers']} = all host threads, "
+                      f"{cpu_model()}; {r['best_s']:.2f} s wall"}
+
+
+def reference_arm(a, rank, world):
+    if rank != 0:
+        return 0
+    log2n = min(a.cpu_log2n, 20)
+    reps = a.warmup + a.steps
+    r = run_ref_tool(log2n, a.n2, a.entry_len, a.suite, a.seed, reps)
+    line = {"impl": "reference", "metric": METRIC, "unit": "entries/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config_dict(a, world)}
+    if r is None:
+        line.update({"unavailable": "oracle/_ref/ref_tool not built (needs /root/reference at build time)"})
+        print(json.dumps(line), flush=True)
+        return 0
+    times = r["times"][a.warmup:]
+    t = sum(times) / len(times)
+    value = (1 << log2n) / t
+    line.update({
+        "value": round(value, 1), "ms_per_step": round(t * 1e3, 3),
+        "cpu_baseline": {"value": round(value, 1), "unit": "entries/s", "cores": r["workers"], "kind": "reference",
+                         "sample": f"each step = reference paver over a 2^{log2n}-entry epoch-aligned sample of the "
+                                   f"workload ({cpu_model()}, {r['workers']} threads)"},
+        "e2e": {"value": round(value, 1), "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "verdict": bool(r["verdict"]),
+    })
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- roofline helpers
+def sass_ops_per_entry(lib_path, kernel_substr, entries_per_thread):
+    """Integer-pipe instructions per entry of the hashing kernel, counted once
+    from the shipped SASS (ALU + FMA pipe ops; memory/control excluded)."""
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True, timeout=300).stdout
+    except Exception:
+        return None
+    blocks = out.split("Function : ")
+    for blk in blocks:
+        if kernel_substr in blk.split("\n", 1)[0]:
+            n = 0
+            for line in blk.splitlines():
+                line = line.strip()
+                if not line.startswith("/*") or "*/" not in line:
+                    continue
+                ins = line.split("*/", 1)[1].strip().split(" ")[0].strip("{").strip()
+                if ins.startswith("@"):
+                    ins = line.split("*/", 1)[1].strip().split(" ")[1]
+                op = ins.split(".")[0]
+                if op in ("LOP3", "SHF", "IADD3", "IMAD", "PRMT", "IADD", "LEA", "VIADD", "IABS", "SEL",
+                          "ISETP", "SHL", "SHR", "IMNMX", "BMSK", "FLO", "POPC"):
+                    n += 1
+            return n / entries_per_thread
+    return None
+
+
+def int_peak(device):
+    lib_path = os.path.join(ROOT, "paper_2506_08781_b200", "libposlo_microbench.so")
+    if not os.path.exists(lib_path):
+        return None
+    lib = ctypes.CDLL(lib_path)
+    lib.poslo_microbench_int_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(ctypes.c_double)]
+    res = {}
+    for mode, name in ((0, "alu"), (1, "fma"), (2, "dual")):
+        v, ms = ctypes.c_double(), ctypes.c_double()
+        if lib.poslo_microbench_int_peak(device, mode, ctypes.byref(v), ctypes.byref(ms)) == 0:
+            res[name] = v.value
+    return res
+
+
+# ----------------------------------------------------------------- B200 arm
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return reference_arm(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2506_08781_b200 import api
+    from paper_2506_08781_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    v = api.Verifier(local)
+    stream = torch.cuda.current_stream()
+    v.set_stream(stream.cuda_stream)
+    lib = v._lib
+
+    n = 1 << a.log2n
+    L = a.entry_len
+    n1_local = n // a.n2
+    n1_total = n1_local * world
+    D = max(1, (n1_total - 1).bit_length())
+    rng = random.Random(a.seed)
+    root = bytes(rng.getrandbits(8) for _ in range(16))
+    ds = api.SeedStack(D, [api.SeedNode(D, 0, root)])  # fully disclosed tree: D PRFs per epoch
+
+    # synthetic log of this rank's epochs, generated on the device
+    log = torch.empty(n * L, dtype=torch.uint8, device="cuda")
+    err = N.PosloError()
+    rc = lib.poslo_gpu_synth_log(v._ctx, a.seed, rank * n, n, L, ctypes.c_void_p(log.data_ptr()),
+                                 ctypes.byref(err))
+    assert rc == 0, err.message
+    import numpy as np
+    epochs = np.arange(rank * n1_local, (rank + 1) * n1_local, dtype=np.uint32)
+    ds_bytes = ds.serialize()
+    ds_buf = ctypes.create_string_buffer(ds_bytes, len(ds_bytes))
+
+    def batch(payload_ptr, device_resident):
+        b = N.PosloBatch()
+        b.suite, b.n2, b.payload, b.payload_bytes = a.suite, a.n2, payload_ptr, n * L
+        b.offsets, b.entry_len, b.n_entries = None, L, n
+        b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, n1_local
+        b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(ds_buf), len(ds_bytes), D, device_resident
+        return b
+
+    bdev = batch(log.data_ptr(), 1)
+
+    def call(fn, *args):
+        e = N.PosloError()
+        rc = fn(v._ctx, *args, ctypes.byref(e))
+        if rc:
+            raise RuntimeError(f"{fn.__name__}: {rc} {e.message.decode()}")
+
+    # ---- fixture (untimed): a valid coarse aggregate signature for the whole job
+    e_part = ctypes.create_string_buffer(32)
+    call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), None, e_part)
+    parts = [e_part.raw]
+    if world > 1:
+        t = torch.frombuffer(bytearray(e_part.raw), dtype=torch.uint8).cuda()
+        g = torch.empty(world * 32, dtype=torch.uint8, device="cuda")
+        dist.all_gather_into_tensor(g, t)
+        gb = g.cpu().numpy().tobytes()
+        parts = [gb[32 * r:32 * r + 32] for r in range(world)]
+    e_hat = sum(int.from_bytes(p, "little") for p in parts) % L_ORDER
+    y = rng.randrange(1, L_ORDER)
+    r_nonce = rng.randrange(1, L_ORDER)
+    s_hat = (r_nonce - e_hat * y) % L_ORDER
+    Y = v.exp_base(y.to_bytes(32, "little"))
+    R = v.exp_base(r_nonce.to_bytes(32, "little"))
+    s_le = s_hat.to_bytes(32, "little")
+    Yb, Sb, Rb = (ctypes.create_string_buffer(x, 32) for x in (Y, s_le, R))
+    verdict = ctypes.c_uint8(0)
+
+    def step_single(b):
+        call(lib.poslo_gpu_paver, ctypes.byref(b), Yb, Sb, Rb, None, ctypes.byref(verdict))
+        return verdict.value
+
+    gbuf = torch.empty(world * 32, dtype=torch.uint8, device="cuda")
+
+    def step_multi(b):
+        call(lib.poslo_gpu_agg_ekeys, ctypes.byref(b), None, e_part)
+        t = torch.frombuffer(bytearray(e_part.raw), dtype=torch.uint8).to("cuda", non_blocking=True)
+        dist.all_gather_into_tensor(gbuf, t)
+        ok = 1
+        if rank == 0:
+            gathered = gbuf.cpu().numpy().tobytes()
+            eh = ctypes.create_string_buffer(32)
+            call(lib.poslo_gpu_scalar_sum, world, gathered, eh)  # rank-ordered device fold mod l
+            call(lib.poslo_gpu_group_check, 1, Yb, eh, Sb, Rb, ctypes.byref(verdict))
+            ok = verdict.value
+        return ok
+
+    step = step_single if world == 1 else step_multi
+
+    # ---- warm-up + correctness of the fixture
+    for _ in range(a.warmup):
+        ok = step(bdev)
+    if rank == 0:
+        assert ok == 1, "verifier rejected a valid aggregate"
+    # tamper check (untimed): one flipped bit must be rejected
+    if world == 1:
+        saved = log[0].item()
+        log[0] = saved ^ 1
+        torch.cuda.synchronize()
+        assert step_single(bdev) == 0, "tampered log accepted"
+        log[0] = saved
+        torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    v.enable_timing(True)
+    hash_ms = []
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            ok = step(bdev)
+            hash_ms.append(v.last_timings()["hash"])
+            launches += v.last_launches()
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+    ms_per_step = ms / a.steps
+    value = world * n / (ms_per_step * 1e-3)
+
+    # ---- e2e: same metric through the C-ABI with the log in pinned HOST memory
+    v.enable_timing(False)
+    host = torch.empty(n * L, dtype=torch.uint8, pin_memory=True)
+    host.copy_(log)
+    bhost = batch(host.data_ptr(), 0)
+    step(bhost)  # warm the staging buffers
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(a.e2e_steps):
+        step(bhost)
+    ev1.record(stream)
+    ev1.synchronize()
+    e2e_ms = max(ev0.elapsed_time(ev1), (time.perf_counter() - t0) * 1e3) / a.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e_value = world * n / (e2e_ms * 1e-3)
+    del host
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (integer pipe)
+    lib_path = os.path.join(ROOT, "paper_2506_08781_b200", "libposlo_gpu.so")
+    kname, ept = ("k_hash_s1_l32ILi128ELi2E", 2) if a.n2 <= 256 else ("k_hash_s1_l32ILi256ELi4E", 4)
+    if a.suite == 2:
+        kname = kname.replace("s1", "s2")
+    ops = sass_ops_per_entry(lib_path, kname, ept)
+    peaks = int_peak(local) or {}
+    hash_avg_ms = statistics.mean(hash_ms) if hash_ms else None
+    peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak = 6534.5
+    if os.path.exists(peaks_file):
+        hbm_peak = json.load(open(peaks_file)).get("hbm_gbs", hbm_peak)
+    roof = None
+    if ops and hash_avg_ms and peaks.get("dual"):
+        achieved = ops * n / (hash_avg_ms * 1e-3) / 1e12
+        peak = peaks["dual"] / 1e12
+        hbm_gbs = n * L / (hash_avg_ms * 1e-3) / 1e9
+        roof = {"bound": "int", "kernel": kname, "achieved": round(achieved, 2), "peak": round(peak, 2),
+                "unit": "Tops/s (int32 lane-ops)", "frac": round(achieved / peak, 4), "traffic": None,
+                "ops_per_entry": round(ops, 1), "ms_per_launch": round(hash_avg_ms, 4),
+                "peak_source": "measured live: LOP3+IMAD dual-pipe microbench (paper_2506_08781_b200/csrc/microbench.cu)",
+                "alu_only_peak": round(peaks.get("alu", 0) / 1e12, 2),
+                "hbm": {"achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": round(hbm_gbs / hbm_peak, 4), "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                "share_of_step": round(hash_avg_ms / ms_per_step, 4)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "entries/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (counter-based log, include/poslo_synth.h)",
+        "config": config_dict(a, world),
+        "e2e": {"value": round(e2e_value, 1), "unit": "entries/s", "h2d_bytes_per_step": n * L + 4 * n1_local + len(ds_bytes) + 8,
+                "d2h_bytes_per_step": 1 + 8, "ms_per_step": round(e2e_ms, 3),
+                "path": "poslo_gpu_paver(device_resident=0) on pinned host log"},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "verdict": bool(ok),
+        "clocks": clk.summary(),
+        "log2_value": round(__import__("math").log2(value), 3),
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(a)
+        except Exception as e:  # reported, never silently replaced
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

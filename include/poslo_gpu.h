@@ -1,0 +1,174 @@
+/* poslo_gpu.h — C-ABI of the B200 batch verifier for POSLO (arXiv 2506.08781).
+ *
+ * Drop-in boundary for the reference's batch-verification path
+ * (/root/reference/proj/include/poslo/batch_verify.hpp:11-30). Plain pointers
+ * and sizes only; no C++ or torch types. The C++ drop-in
+ * (paper_2506_08781_b200/host/batch_verify_gpu.cpp) implements the reference
+ * signatures `poslo::agg_ekeys` / `poslo::paver` on top of these calls, and
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *   - Scalars are 32-byte LITTLE-endian canonical values (< l), the reference's
+ *     in-memory Scalar form (group.hpp:38,43); the big-endian wire form is the
+ *     host's business.
+ *   - Group elements are 32-byte canonical ristretto255 encodings; identity is
+ *     32 zero bytes (group.hpp:47-59).
+ *   - `ds` is the SeedStack wire format exactly as SeedStack::serialize
+ *     writes it (seed_manager.cpp:32-39), with capacity D = log2(n1).
+ *   - Entry layout: the queried epochs' entries are packed back to back in
+ *     epoch order; epoch k (k-th entry of `epochs`) owns entries
+ *     [epoch_starts[k], epoch_starts[k+1]) — or [k*n2, (k+1)*n2) when
+ *     epoch_starts is NULL. Entry t's bytes are payload[offsets[t] ..
+ *     offsets[t+1]) — or payload[t*entry_len .. (t+1)*entry_len) when offsets
+ *     is NULL.
+ *   - `device_resident`: payload/offsets are device pointers (already in HBM);
+ *     everything else is always host memory.
+ *   - Every call is synchronous with respect to its outputs and re-entrant
+ *     per context (a context serialises its own calls; use one context per
+ *     host thread for concurrency).
+ *
+ * Errors (same taxonomy and order as the reference): return
+ * value and err->code are one of POSLO_OK, POSLO_FORMAT_ERROR (FormatError),
+ * POSLO_STATE_ERROR (StateError), POSLO_SEED_NOT_DISCLOSED (SeedNotDisclosed,
+ * err->epoch = the epoch, the lowest one as with workers == 1),
+ * POSLO_CUDA_ERROR, POSLO_INVALID_ARGUMENT. No call ever falls back to a CPU
+ * implementation; without a usable sm_100 device every call returns
+ * POSLO_CUDA_ERROR. */
+#ifndef POSLO_GPU_H
+#define POSLO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POSLO_OK 0
+#define POSLO_FORMAT_ERROR 1
+#define POSLO_STATE_ERROR 2
+#define POSLO_SEED_NOT_DISCLOSED 3
+#define POSLO_CUDA_ERROR 4
+#define POSLO_INVALID_ARGUMENT 5
+
+typedef struct poslo_gpu_ctx poslo_gpu_ctx;
+
+typedef struct poslo_error {
+    int32_t code;
+    uint32_t epoch; /* offending epoch for POSLO_SEED_NOT_DISCLOSED / StateError */
+    char message[240];
+} poslo_error;
+
+/* A packed batch: the `std::map<uint32_t, std::vector<Bytes>> batches`
+ * argument of agg_ekeys/paver (batch_verify.hpp:20-30) plus the
+ * SuiteConfig and SeedStack it is verified against. */
+typedef struct poslo_batch {
+    uint8_t suite;                 /* SuiteId: 1 SHA-256, 2 MMO/MDC-2, 3 MMO/ADD_Q */
+    uint32_t n2;                   /* entries per epoch (SuiteConfig::n2) */
+    const uint8_t* payload;        /* entry bytes */
+    uint64_t payload_bytes;
+    const uint64_t* offsets;       /* n_entries + 1 byte offsets, or NULL */
+    uint32_t entry_len;            /* fixed entry length when offsets == NULL */
+    uint64_t n_entries;
+    const uint32_t* epochs;        /* n_epochs queried epoch indices, strictly ascending (host) */
+    const uint64_t* epoch_starts;  /* n_epochs + 1 entry indices (host), or NULL = uniform n2 */
+    uint32_t n_epochs;
+    const uint8_t* ds;             /* SeedStack wire bytes (host) */
+    uint32_t ds_len;
+    uint32_t ds_capacity;          /* D = log2(n1) */
+    int32_t device_resident;       /* payload/offsets live in device memory */
+} poslo_batch;
+
+/* ---- context -------------------------------------------------------------- */
+int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);
+void poslo_gpu_destroy(poslo_gpu_ctx* ctx);
+/* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
+int poslo_gpu_set_stream(poslo_gpu_ctx* ctx, void* cuda_stream);
+/* Device stage timings (ms) of the last call when enabled: [seed, hash,
+ * epoch_finalize, sum, group, total]. */
+int poslo_gpu_enable_timing(poslo_gpu_ctx* ctx, int on);
+int poslo_gpu_last_timings(poslo_gpu_ctx* ctx, float out_ms[6]);
+/* Number of kernels the last call launched. */
+uint32_t poslo_gpu_last_launches(poslo_gpu_ctx* ctx);
+const char* poslo_gpu_version(void);
+
+/* ---- agg_ekeys (batch_verify.cpp:11-62) -------------------------------------
+ * e_tilde_out: n_epochs x 32 B (LE), per queried epoch in the given
+ * (ascending) order — EpochKeyAggregate::e; may be NULL.
+ * e_hat_out: 32 B, sum of all e~ mod l (aggregate_ekey, poslo_c.cpp:177-190);
+ * may be NULL. Errors: SeedNotDisclosed / FormatError (suite 3, L > 31) for
+ * the lowest offending epoch, seed retrieval first. */
+int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* batch, uint8_t* e_tilde_out,
+                        uint8_t* e_hat_out, poslo_error* err);
+
+/* ---- paver (batch_verify.cpp:64-87) -----------------------------------------
+ * Checks every epoch holds n2 entries (StateError), folds R-hat from
+ * r_hats (n_epochs x 32 B, pk.r_hats[epoch] in batch order) unless
+ * r_hat_agg (32 B) is given, computes e-hat and returns
+ * *verdict = (commit_check(Y, e-hat, s-hat) == R-hat). */
+int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                    const uint8_t s_hat[32], const uint8_t* r_hat_agg, const uint8_t* r_hats,
+                    uint8_t* verdict, poslo_error* err);
+
+/* ---- per-epoch verification (distill_epoch verdicts, distiller.cpp:60-89) ---
+ * verdicts[k] = (commit_check(Y, e~_k, s_hats[k]) == r_hats[k]) for every
+ * queried epoch; e_tilde_out optional (n_epochs x 32 B). */
+int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                           const uint8_t* s_hats, const uint8_t* r_hats, uint8_t* verdicts,
+                           uint8_t* e_tilde_out, poslo_error* err);
+
+/* ---- SeBVer (distiller.cpp:156-233) over a coarse CCD --------------------------
+ * The batch holds epochs 0..n_epochs-1 (all distilled epochs, n2 each).
+ * invalid: n_invalid ascending epoch indices (CCD invalid list).
+ * Mode V: v_s/v_r = CCD valid aggregate -> *v_bit.
+ * Mode U: n_umb umbrella records (index u, s, r; width w = n1/n_u) -> u_bits.
+ * Mode I: one bit per invalid record (s, r) -> i_bits.
+ * Any output pointer may be NULL to skip that mode. */
+int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                     uint32_t n1, uint32_t n_u, const uint32_t* invalid, const uint8_t* invalid_s,
+                     const uint8_t* invalid_r, uint32_t n_invalid, const uint8_t* v_s,
+                     const uint8_t* v_r, uint8_t* v_bit, const uint32_t* umb_index,
+                     const uint8_t* umb_s, const uint8_t* umb_r, uint32_t n_umb, uint8_t* u_bits,
+                     uint8_t* i_bits, poslo_error* err);
+
+/* ---- group primitives (group.cpp), batched on the device ----------------------
+ * commit_check: out[i] = encode(Y^e[i] * alpha^s[i]) (group.cpp:144-167).
+ * Y = identity gives exp_base. */
+int poslo_gpu_commit_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], const uint8_t* e,
+                           const uint8_t* s, uint8_t* out, poslo_error* err);
+/* group_combine fold of n points (agg_elements, poslo_c.cpp:170-174). */
+int poslo_gpu_group_fold(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* pts, uint8_t out[32],
+                         poslo_error* err);
+/* GroupElement::from_bytes validity (group.cpp:107-114): ok[i] in {0,1}. */
+int poslo_gpu_point_valid(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* pts, uint8_t* ok,
+                          poslo_error* err);
+
+/* Batched check: verdicts[i] = (commit_check(Y, e[i], s[i]) == r[i]) — the
+ * final step of paver (batch_verify.cpp:86), used for multi-GPU combines. */
+int poslo_gpu_group_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], const uint8_t* e,
+                          const uint8_t* s, const uint8_t* r, uint8_t* verdicts, poslo_error* err);
+/* out = sum of n scalars mod l (Scalar::add fold, batch_verify.cpp:84-85);
+ * used to fold per-shard partial e-hat in rank order. */
+int poslo_gpu_scalar_sum(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* scalars, uint8_t out[32],
+                         poslo_error* err);
+
+/* ---- stage-level entry points (parity/debug) ----------------------------------
+ * sr (seed_manager.cpp:71-85) for each epoch: x0_out n x 16 B. */
+int poslo_gpu_seed_retrieve(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t* ds, uint32_t ds_len,
+                            uint32_t ds_capacity, const uint32_t* epochs, uint32_t n,
+                            uint8_t* x0_out, poslo_error* err);
+/* Per-entry e = hash_to_scalar(m, onetime_seed(x0, j)) mod l for every entry
+ * of the batch (n_entries x 32 B LE), through the generic device path. */
+int poslo_gpu_entry_scalars(poslo_gpu_ctx* ctx, const poslo_batch* batch, uint8_t* e_out,
+                            poslo_error* err);
+
+/* Counter-based synthetic log (include/poslo_synth.h) written to device
+ * memory d_out: entries [first, first + n) of entry_len bytes each. Bench and
+ * fixture tooling; byte-identical to the CPU harness's generator. */
+int poslo_gpu_synth_log(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint64_t n,
+                        uint32_t entry_len, void* d_out, poslo_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POSLO_GPU_H */

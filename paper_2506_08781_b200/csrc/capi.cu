@@ -1,0 +1,797 @@
+// C-ABI of the B200 batch verifier (include/poslo_gpu.h).
+//
+// Host orchestration of one verification call on the context's stream:
+//   validate + parse ds (SeedStack wire, seed_manager.cpp:41-53)
+//   -> [H2D of the packed log when it is host-resident]
+//   -> K0 seed_derive -> K1+K2 hash/segmented sum -> epoch finalize
+//   -> sum mod l (e-hat) / R-hat fold -> K3 group check -> D2H of verdicts.
+// Errors follow the reference's taxonomy and order; the
+// lowest offending epoch wins, seed retrieval before hashing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/poslo_gpu.h"
+#include "aes128.cuh"
+#include "poslo_internal.h"
+
+using namespace poslo_gpu;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace
+
+struct poslo_gpu_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::mutex mtx;
+    uint32_t* d_t0 = nullptr;
+    DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
+        b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
+        b_y, b_pts, b_foldscratch, b_rhat;
+    bool timing = false;
+    cudaEvent_t ev[7] = {};
+    float last_ms[6] = {};
+    uint32_t launches = 0;
+};
+
+namespace {
+
+constexpr int kEvSeed = 0, kEvHash = 1, kEvFin = 2, kEvSum = 3, kEvGroup = 4, kEvEnd = 5;
+
+int set_err(poslo_error* err, int code, uint32_t epoch, const char* fmt, ...) {
+    if (err) {
+        err->code = code;
+        err->epoch = epoch;
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(err->message, sizeof err->message, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+int ok(poslo_error* err) {
+    if (err) {
+        err->code = POSLO_OK;
+        err->epoch = 0;
+        err->message[0] = 0;
+    }
+    return POSLO_OK;
+}
+
+#define CU(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(err, POSLO_CUDA_ERROR, 0, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+int ensure(DevBuf& b, size_t count, T** out, poslo_error* err) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    if (b.cap < bytes) {
+        size_t want = std::max(bytes, b.cap * 3 / 2);
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        CU(cudaMalloc(&b.p, want));
+        b.cap = want;
+    }
+    *out = static_cast<T*>(b.p);
+    return POSLO_OK;
+}
+
+#define ENSURE(buf, n, ptr)                                  \
+    do {                                                     \
+        int rc_ = ensure(ctx->buf, (n), &(ptr), err);        \
+        if (rc_) return rc_;                                 \
+    } while (0)
+
+void mark(poslo_gpu_ctx* ctx, int i) {
+    if (ctx->timing) cudaEventRecord(ctx->ev[i], ctx->stream);
+}
+
+// SeedStack::deserialize + push invariants (seed_manager.cpp:18-23, 41-53).
+int parse_ds(const uint8_t* w, uint32_t n, uint32_t cap, DsParam& ds, poslo_error* err) {
+    if (!w || n < 1) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated input");
+    uint32_t count = w[0];
+    size_t off = 1;
+    ds.count = 0;
+    for (uint32_t k = 0; k < count; k++) {
+        if (n - off < 21) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated input");
+        if (k >= cap) return set_err(err, POSLO_STATE_ERROR, 0, "seed stack overflow");
+        if (k >= 32) return set_err(err, POSLO_FORMAT_ERROR, 0, "seed stack deeper than 32");
+        DsNode& nd = ds.nodes[k];
+        nd.depth = w[off];
+        nd.index = (uint32_t)w[off + 1] << 24 | (uint32_t)w[off + 2] << 16 | (uint32_t)w[off + 3] << 8 | w[off + 4];
+        std::memcpy(nd.value, w + off + 5, 16);
+        if (k > 0 && ds.nodes[k - 1].depth <= nd.depth)
+            return set_err(err, POSLO_STATE_ERROR, 0, "seed stack depth order violated");
+        if (nd.depth > 32) return set_err(err, POSLO_FORMAT_ERROR, 0, "seed node depth out of range");
+        ds.count = (int)k + 1;
+        off += 21;
+    }
+    return POSLO_OK;
+}
+
+struct Prepared {
+    EntryLayout lay{};
+    TileMap tm{};
+    bool fast = false;
+    bool uniform = false;
+    uint32_t* d_etilde = nullptr;
+};
+
+bool is_uniform(const poslo_batch* b) {
+    if (!b->epoch_starts) return true;
+    for (uint32_t k = 0; k <= b->n_epochs; k++)
+        if (b->epoch_starts[k] != (uint64_t)k * b->n2) return false;
+    return true;
+}
+
+// Stages 0-2 for a batch: leaves per-epoch e~ (8 limbs each) in
+// ctx->b_etilde and returns the status after reading the error word.
+int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error* err) {
+    if (!b) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null batch");
+    if (b->suite < 1 || b->suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
+    if (b->n_epochs && !b->epochs) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null epochs");
+    for (uint32_t k = 1; k < b->n_epochs; k++)
+        if (b->epochs[k] <= b->epochs[k - 1])
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epochs must be strictly ascending");
+    DsParam ds;
+    int rc = parse_ds(b->ds, b->ds_len, b->ds_capacity, ds, err);
+    if (rc) return rc;
+    P.uniform = is_uniform(b);
+    uint64_t n_entries = P.uniform ? (uint64_t)b->n_epochs * b->n2 : b->epoch_starts[b->n_epochs];
+    if (b->epoch_starts && b->epoch_starts[0] != 0)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epoch_starts[0] must be 0");
+    if (n_entries > b->n_entries)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "batch describes more entries than given");
+    if (n_entries && !b->payload && !(b->offsets == nullptr && b->entry_len == 0))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null payload");
+
+    cudaStream_t s = ctx->stream;
+    uint32_t n_ep = b->n_epochs;
+    uint32_t* d_epochs;
+    uint4* d_x0;
+    unsigned long long* d_err;
+    ENSURE(b_epochs, n_ep, d_epochs);
+    ENSURE(b_x0, n_ep, d_x0);
+    ENSURE(b_err, 1, d_err);
+    ENSURE(b_etilde, (size_t)n_ep * 8, P.d_etilde);
+
+    // entry layout (H2D when host-resident)
+    P.lay.entry_len = b->entry_len;
+    if (b->device_resident) {
+        P.lay.payload = b->payload;
+        P.lay.offsets = b->offsets;
+    } else {
+        uint8_t* d_pay;
+        ENSURE(b_payload, b->payload_bytes, d_pay);
+        if (b->payload_bytes) CU(cudaMemcpyAsync(d_pay, b->payload, b->payload_bytes, cudaMemcpyHostToDevice, s));
+        P.lay.payload = d_pay;
+        P.lay.offsets = nullptr;
+        if (b->offsets) {
+            uint64_t* d_off;
+            ENSURE(b_offsets, b->n_entries + 1, d_off);
+            CU(cudaMemcpyAsync(d_off, b->offsets, (b->n_entries + 1) * 8, cudaMemcpyHostToDevice, s));
+            P.lay.offsets = d_off;
+        }
+    }
+
+    mark(ctx, kEvSeed);
+    unsigned long long init = ~0ull;
+    CU(cudaMemcpyAsync(d_err, &init, 8, cudaMemcpyHostToDevice, s));
+    if (n_ep) CU(cudaMemcpyAsync(d_epochs, b->epochs, (size_t)n_ep * 4, cudaMemcpyHostToDevice, s));
+    launch_seed_derive(b->suite, ds, d_epochs, n_ep, d_x0, d_err, ctx->d_t0, s);
+    ctx->launches += n_ep ? 1 : 0;
+    mark(ctx, kEvHash);
+
+    // tiles
+    TileMap& tm = P.tm;
+    tm.n_epochs = n_ep;
+    tm.n2 = b->n2;
+    bool aligned = ((uintptr_t)P.lay.payload & 15) == 0;
+    P.fast = P.uniform && !b->offsets && b->entry_len == 32 && (b->suite == 1 || b->suite == 2) && aligned;
+    uint32_t* d_partial = nullptr;
+    if (P.uniform) {
+        if (P.fast)
+            tm.tile_entries = b->n2 <= 128 ? 128 : (b->n2 <= 256 ? 256 : 1024);
+        else
+            tm.tile_entries = 1024;
+        tm.tiles_per_epoch = b->n2 ? (b->n2 + tm.tile_entries - 1) / tm.tile_entries : 0;
+        tm.n_tiles = n_ep * tm.tiles_per_epoch;
+    } else {
+        std::vector<uint4> tiles;
+        std::vector<uint32_t> tbegin(n_ep + 1);
+        const uint32_t te = 1024;
+        for (uint32_t k = 0; k < n_ep; k++) {
+            tbegin[k] = (uint32_t)tiles.size();
+            uint64_t cnt = b->epoch_starts[k + 1] - b->epoch_starts[k];
+            if (b->epoch_starts[k + 1] < b->epoch_starts[k])
+                return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epoch_starts must be non-decreasing");
+            for (uint64_t j0 = 0; j0 < cnt; j0 += te)
+                tiles.push_back(make_uint4(k, (uint32_t)j0, (uint32_t)std::min<uint64_t>(te, cnt - j0), 0));
+        }
+        tbegin[n_ep] = (uint32_t)tiles.size();
+        uint4* d_tiles;
+        uint64_t* d_starts;
+        uint32_t* d_tb;
+        ENSURE(b_tiles, tiles.size(), d_tiles);
+        ENSURE(b_starts, n_ep + 1, d_starts);
+        ENSURE(b_tbegin, n_ep + 1, d_tb);
+        if (!tiles.empty()) CU(cudaMemcpyAsync(d_tiles, tiles.data(), tiles.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(d_starts, b->epoch_starts, (n_ep + 1) * 8, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(d_tb, tbegin.data(), (n_ep + 1) * 4, cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));  // host vectors go out of scope
+        tm.tiles = d_tiles;
+        tm.epoch_starts = d_starts;
+        tm.epoch_tile_begin = d_tb;
+        tm.n_tiles = (uint32_t)tiles.size();
+    }
+    ENSURE(b_partial, (size_t)std::max<uint32_t>(tm.n_tiles, 1) * 17, d_partial);
+    bool need_finalize = true;
+    if (P.fast) {
+        if (b->suite == 1)
+            launch_hash_s1_l32(P.lay, tm, d_x0, d_partial, P.d_etilde, s);
+        else
+            launch_hash_s2_l32(P.lay, tm, d_x0, d_partial, P.d_etilde, ctx->d_t0, s);
+        ctx->launches += tm.n_tiles ? 1 : 0;
+        need_finalize = tm.tiles_per_epoch != 1;
+    } else {
+        launch_hash_generic(b->suite, P.lay, tm, d_x0, d_partial, nullptr, d_err, ctx->d_t0, s);
+        ctx->launches += tm.n_tiles ? 1 : 0;
+    }
+    mark(ctx, kEvFin);
+    if (need_finalize && n_ep) {
+        launch_epoch_finalize(tm, d_partial, P.d_etilde, s);
+        ctx->launches += 1;
+    }
+    CU(cudaGetLastError());
+    return POSLO_OK;
+}
+
+// Reads the error word (synchronises) and maps it to the reference error.
+int check_hash_errors(poslo_gpu_ctx* ctx, const poslo_batch* b, poslo_error* err) {
+    unsigned long long key;
+    CU(cudaMemcpyAsync(&key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (key == ~0ull) return POSLO_OK;
+    uint32_t k = (uint32_t)(key >> 1);
+    uint32_t epoch = k < b->n_epochs ? b->epochs[k] : 0;
+    if ((key & 1) == 0)
+        return set_err(err, POSLO_SEED_NOT_DISCLOSED, epoch, "seed for epoch %u not yet disclosed", epoch);
+    return set_err(err, POSLO_FORMAT_ERROR, epoch, "modular-addition hash: entry too long for this suite");
+}
+
+void finish_timing(poslo_gpu_ctx* ctx) {
+    if (!ctx->timing) return;
+    cudaEventRecord(ctx->ev[kEvEnd], ctx->stream);
+    cudaEventSynchronize(ctx->ev[kEvEnd]);
+    cudaEventElapsedTime(&ctx->last_ms[0], ctx->ev[kEvSeed], ctx->ev[kEvHash]);
+    cudaEventElapsedTime(&ctx->last_ms[1], ctx->ev[kEvHash], ctx->ev[kEvFin]);
+    cudaEventElapsedTime(&ctx->last_ms[2], ctx->ev[kEvFin], ctx->ev[kEvSum]);
+    cudaEventElapsedTime(&ctx->last_ms[3], ctx->ev[kEvSum], ctx->ev[kEvGroup]);
+    cudaEventElapsedTime(&ctx->last_ms[4], ctx->ev[kEvGroup], ctx->ev[kEvEnd]);
+    cudaEventElapsedTime(&ctx->last_ms[5], ctx->ev[kEvSeed], ctx->ev[kEvEnd]);
+}
+
+struct Guard {
+    poslo_gpu_ctx* ctx;
+    std::lock_guard<std::mutex> lk;
+    explicit Guard(poslo_gpu_ctx* c) : ctx(c), lk(c->mtx) {
+        cudaSetDevice(c->device);
+        c->launches = 0;
+    }
+};
+
+int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void** out, poslo_error* err) {
+    uint8_t* d;
+    int rc = ensure(buf, bytes, &d, err);
+    if (rc) return rc;
+    if (bytes) CU(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    *out = d;
+    return POSLO_OK;
+}
+
+#define UPLOAD(buf, src, bytes, ptr)                                              \
+    do {                                                                          \
+        void* p_;                                                                 \
+        int rc_ = upload(ctx, ctx->buf, (src), (bytes), &p_, err);                \
+        if (rc_) return rc_;                                                      \
+        ptr = static_cast<decltype(ptr)>(p_);                                     \
+    } while (0)
+
+// Batched group check on device arrays; verdicts/encodings to host.
+int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const uint32_t* d_e,
+                    const uint32_t* d_s, const uint8_t* d_r, uint8_t* h_verdict, uint8_t* h_enc,
+                    poslo_error* err) {
+    uint8_t* d_y;
+    int* d_flags;
+    uint8_t* d_verdict = nullptr;
+    uint8_t* d_enc = nullptr;
+    UPLOAD(b_y, y, 32, d_y);
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    if (h_verdict) ENSURE(b_verdict, n, d_verdict);
+    if (h_enc) ENSURE(b_enc, (size_t)n * 32, d_enc);
+    launch_group_check(d_y, n, d_e, d_s, d_r, d_enc, d_verdict, d_flags, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    int ybad = 0;
+    CU(cudaMemcpyAsync(&ybad, d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_verdict && n) CU(cudaMemcpyAsync(h_verdict, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_enc && n) CU(cudaMemcpyAsync(h_enc, d_enc, (size_t)n * 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ybad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    return POSLO_OK;
+}
+
+// LE 32-byte scalar -> 8 limbs (identical memory image on little-endian hosts).
+bool scalar_canonical(const uint8_t* s) {
+    static const uint8_t L[32] = {0xed, 0xd3, 0xf5, 0x5c, 0x1a, 0x63, 0x12, 0x58, 0xd6, 0x9c, 0xf7,
+                                  0xa2, 0xde, 0xf9, 0xde, 0x14, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0,
+                                  0, 0, 0, 0x10};
+    for (int i = 31; i >= 0; i--) {
+        if (s[i] < L[i]) return true;
+        if (s[i] > L[i]) return false;
+    }
+    return false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* poslo_gpu_version(void) { return "poslo-b200 0.1 (sm_100a)"; }
+
+int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
+    if (!out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(err, POSLO_CUDA_ERROR, 0, "no CUDA device %d (have %d)", device, ndev);
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return set_err(err, POSLO_CUDA_ERROR, 0, "device %d is sm_%d%d; this build targets sm_100a",
+                       device, prop.major, prop.minor);
+    CU(cudaSetDevice(device));
+    poslo_gpu_ctx* ctx = new poslo_gpu_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
+    }
+    ctx->stream = ctx->own;
+    uint32_t t0[256];
+    for (int x = 0; x < 256; x++) t0[x] = aes_t0_entry(aes_sbox_compute(x));
+    e = cudaMalloc(&ctx->d_t0, sizeof t0);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_t0, t0, sizeof t0, cudaMemcpyHostToDevice);
+    for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreate(&ctx->ev[i]);
+    if (e != cudaSuccess) {
+        poslo_gpu_destroy(ctx);
+        return set_err(err, POSLO_CUDA_ERROR, 0, "init: %s", cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return ok(err);
+}
+
+void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    DevBuf* bufs[] = {&ctx->b_epochs, &ctx->b_x0, &ctx->b_partial, &ctx->b_etilde, &ctx->b_sum,
+                      &ctx->b_scratch, &ctx->b_tiles, &ctx->b_starts, &ctx->b_tbegin, &ctx->b_err,
+                      &ctx->b_flags, &ctx->b_payload, &ctx->b_offsets, &ctx->b_e, &ctx->b_s,
+                      &ctx->b_r, &ctx->b_enc, &ctx->b_verdict, &ctx->b_mask, &ctx->b_seg, &ctx->b_y,
+                      &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->d_t0) cudaFree(ctx->d_t0);
+    for (auto& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+int poslo_gpu_set_stream(poslo_gpu_ctx* ctx, void* stream) {
+    if (!ctx) return POSLO_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mtx);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return POSLO_OK;
+}
+
+int poslo_gpu_enable_timing(poslo_gpu_ctx* ctx, int on) {
+    if (!ctx) return POSLO_INVALID_ARGUMENT;
+    ctx->timing = on != 0;
+    return POSLO_OK;
+}
+
+int poslo_gpu_last_timings(poslo_gpu_ctx* ctx, float out_ms[6]) {
+    if (!ctx || !out_ms) return POSLO_INVALID_ARGUMENT;
+    std::memcpy(out_ms, ctx->last_ms, sizeof ctx->last_ms);
+    return POSLO_OK;
+}
+
+uint32_t poslo_gpu_last_launches(poslo_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_tilde_out,
+                        uint8_t* e_hat_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    Guard g(ctx);
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    mark(ctx, kEvSum);
+    uint32_t* d_sum = nullptr;
+    if (e_hat_out) {
+        uint32_t* d_scr;
+        ENSURE(b_sum, 8, d_sum);
+        ENSURE(b_scratch, 17 * 1024, d_scr);
+        launch_sum_mod_l(P.d_etilde, 8, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
+        ctx->launches += 2;
+    }
+    mark(ctx, kEvGroup);
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    if (e_tilde_out && b->n_epochs)
+        CU(cudaMemcpyAsync(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost, ctx->stream));
+    if (e_hat_out) CU(cudaMemcpyAsync(e_hat_out, d_sum, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    finish_timing(ctx);
+    return ok(err);
+}
+
+int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
+                    const uint8_t s_hat[32], const uint8_t* r_hat_agg, const uint8_t* r_hats,
+                    uint8_t* verdict, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !y || !s_hat || !verdict) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    // 1. every batch holds exactly n2 entries (batch_verify.cpp:68-70)
+    if (b->epoch_starts)
+        for (uint32_t k = 0; k < b->n_epochs; k++)
+            if (b->epoch_starts[k + 1] - b->epoch_starts[k] != b->n2)
+                return set_err(err, POSLO_STATE_ERROR, b->epochs[k], "every batch must hold exactly n2 entries");
+    // 2. R-hat: given aggregate or fold of the per-epoch commitments (:71-82)
+    if (!r_hat_agg && !r_hats && b->n_epochs)
+        return set_err(err, POSLO_STATE_ERROR, b->epochs[0], "commitment for epoch %u no longer in public key",
+                       b->epochs[0]);
+    if (!scalar_canonical(s_hat)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    uint8_t* d_rhat;
+    ENSURE(b_rhat, 32, d_rhat);
+    int* d_flags;
+    ENSURE(b_flags, 4, d_flags);
+    if (r_hat_agg) {
+        CU(cudaMemcpyAsync(d_rhat, r_hat_agg, 32, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        uint8_t* d_pts;
+        void* d_fs;
+        UPLOAD(b_pts, r_hats, (size_t)b->n_epochs * 32, d_pts);
+        ENSURE(b_foldscratch, 1024 * 128, d_fs);
+        CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+        launch_point_fold(d_pts, b->n_epochs, d_rhat, d_flags + 1, d_fs, ctx->stream);
+        ctx->launches += 2;
+    }
+    // 3. e-hat = sum of agg_ekeys (:83-85)
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    mark(ctx, kEvSum);
+    uint32_t *d_sum, *d_scr, *d_s;
+    ENSURE(b_sum, 8, d_sum);
+    ENSURE(b_scratch, 17 * 1024, d_scr);
+    launch_sum_mod_l(P.d_etilde, 8, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
+    ctx->launches += 2;
+    UPLOAD(b_s, s_hat, 32, d_s);
+    mark(ctx, kEvGroup);
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    if (!r_hat_agg) {
+        int bad = 0;
+        CU(cudaMemcpy(&bad, d_flags + 1, 4, cudaMemcpyDeviceToHost));
+        if (bad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    }
+    // 4. one commitment check (:86)
+    uint32_t launches = ctx->launches;
+    rc = group_check_dev(ctx, y, 1, d_sum, d_s, d_rhat, verdict, nullptr, err);
+    if (rc) return rc;
+    ctx->launches = launches + 1;
+    finish_timing(ctx);
+    return ok(err);
+}
+
+int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
+                           const uint8_t* s_hats, const uint8_t* r_hats, uint8_t* verdicts,
+                           uint8_t* e_tilde_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !y || (b->n_epochs && (!s_hats || !r_hats || !verdicts)))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    for (uint32_t k = 0; k < b->n_epochs; k++)
+        if (!scalar_canonical(s_hats + 32 * (size_t)k))
+            return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    mark(ctx, kEvSum);
+    uint32_t* d_s;
+    uint8_t* d_r;
+    UPLOAD(b_s, s_hats, (size_t)b->n_epochs * 32, d_s);
+    UPLOAD(b_r, r_hats, (size_t)b->n_epochs * 32, d_r);
+    mark(ctx, kEvGroup);
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    uint32_t launches = ctx->launches;
+    rc = group_check_dev(ctx, y, b->n_epochs, P.d_etilde, d_s, d_r, verdicts, nullptr, err);
+    if (rc) return rc;
+    ctx->launches = launches + (b->n_epochs ? 1 : 0);
+    if (e_tilde_out && b->n_epochs)
+        CU(cudaMemcpy(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost));
+    finish_timing(ctx);
+    return ok(err);
+}
+
+int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32], uint32_t n1,
+                     uint32_t n_u, const uint32_t* invalid, const uint8_t* invalid_s,
+                     const uint8_t* invalid_r, uint32_t n_invalid, const uint8_t* v_s,
+                     const uint8_t* v_r, uint8_t* v_bit, const uint32_t* umb_index,
+                     const uint8_t* umb_s, const uint8_t* umb_r, uint32_t n_umb, uint8_t* u_bits,
+                     uint8_t* i_bits, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !y || n_u == 0 || n1 % n_u) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    Guard g(ctx);
+    for (uint32_t k = 0; k < b->n_epochs; k++)
+        if (b->epochs[k] != k) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "sebver batch must hold epochs 0..n-1");
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    cudaStream_t s = ctx->stream;
+    uint32_t n_ep = b->n_epochs;
+    std::vector<uint8_t> mask(std::max<uint32_t>(n_ep, 1), 0);
+    for (uint32_t k = 0; k < n_invalid; k++)
+        if (invalid[k] < n_ep) mask[invalid[k]] = 1;
+    uint8_t* d_mask;
+    UPLOAD(b_mask, mask.data(), mask.size(), d_mask);
+    uint32_t w = n1 / n_u;
+    // groups: [V] + U umbrellas + I records, e per group on device
+    uint32_t nV = v_bit ? 1 : 0, nU = u_bits ? n_umb : 0, nI = i_bits ? n_invalid : 0;
+    uint32_t ng = nV + nU + nI;
+    if (!ng) return ok(err);
+    std::vector<uint64_t> seg;
+    std::vector<uint8_t> hs((size_t)ng * 32), hr((size_t)ng * 32);
+    uint32_t gi = 0;
+    auto clip = [&](uint64_t v) { return std::min<uint64_t>(v, n_ep); };
+    if (nV) {
+        seg.push_back(0);
+        seg.push_back(n_ep);
+        std::memcpy(&hs[0], v_s, 32);
+        std::memcpy(&hr[0], v_r, 32);
+        gi++;
+    }
+    for (uint32_t u = 0; u < nU; u++, gi++) {
+        seg.push_back(clip((uint64_t)umb_index[u] * w));
+        seg.push_back(clip((uint64_t)(umb_index[u] + 1) * w));
+        std::memcpy(&hs[32 * gi], umb_s + 32 * (size_t)u, 32);
+        std::memcpy(&hr[32 * gi], umb_r + 32 * (size_t)u, 32);
+    }
+    // segsum takes [seg[g], seg[g+1]) over consecutive pairs; use a flat
+    // pair list with a stride-2 view by summing per group separately.
+    uint32_t* d_e;
+    ENSURE(b_e, (size_t)ng * 8, d_e);
+    uint32_t n_seg_groups = nV + nU;
+    if (n_seg_groups) {
+        // pair list -> launch one segsum per pair via seg array of 2 per group
+        uint64_t* d_seg;
+        UPLOAD(b_seg, seg.data(), seg.size() * 8, d_seg);
+        for (uint32_t g2 = 0; g2 < n_seg_groups; g2++) {
+            launch_segsum_mod_l(P.d_etilde, d_seg + 2 * g2, 1, d_mask, d_e + 8 * g2, s);
+            ctx->launches += 1;
+        }
+    }
+    for (uint32_t k = 0; k < nI; k++, gi++) {
+        uint32_t ep = invalid[k];
+        if (ep >= n_ep) return set_err(err, POSLO_FORMAT_ERROR, ep, "messages for invalid epoch missing");
+        CU(cudaMemcpyAsync(d_e + 8 * (size_t)gi, P.d_etilde + 8 * (size_t)ep, 32, cudaMemcpyDeviceToDevice, s));
+        std::memcpy(&hs[32 * gi], invalid_s + 32 * (size_t)k, 32);
+        std::memcpy(&hr[32 * gi], invalid_r + 32 * (size_t)k, 32);
+    }
+    uint32_t* d_s;
+    uint8_t* d_r;
+    UPLOAD(b_s, hs.data(), hs.size(), d_s);
+    UPLOAD(b_r, hr.data(), hr.size(), d_r);
+    std::vector<uint8_t> bits(ng);
+    uint32_t launches = ctx->launches;
+    rc = group_check_dev(ctx, y, ng, d_e, d_s, d_r, bits.data(), nullptr, err);
+    if (rc) return rc;
+    ctx->launches = launches + 1;
+    gi = 0;
+    if (nV) *v_bit = bits[gi++];
+    for (uint32_t u = 0; u < nU; u++) u_bits[u] = bits[gi++];
+    for (uint32_t k = 0; k < nI; k++) i_bits[k] = bits[gi++];
+    return ok(err);
+}
+
+int poslo_gpu_commit_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], const uint8_t* e,
+                           const uint8_t* s, uint8_t* out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!y || (n && (!e || !s || !out))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    for (uint32_t i = 0; i < n; i++)
+        if (!scalar_canonical(e + 32 * (size_t)i) || !scalar_canonical(s + 32 * (size_t)i))
+            return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    uint32_t *d_e, *d_s;
+    UPLOAD(b_e, e, (size_t)n * 32, d_e);
+    UPLOAD(b_s, s, (size_t)n * 32, d_s);
+    int rc = group_check_dev(ctx, y, n, d_e, d_s, nullptr, nullptr, out, err);
+    if (rc) return rc;
+    return ok(err);
+}
+
+int poslo_gpu_group_fold(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* pts, uint8_t out[32],
+                         poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!out || (n && !pts)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    uint8_t *d_pts, *d_out;
+    void* d_fs;
+    int* d_flags;
+    UPLOAD(b_pts, pts, n * 32, d_pts);
+    ENSURE(b_foldscratch, 1024 * 128, d_fs);
+    ENSURE(b_rhat, 32, d_out);
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    launch_point_fold(d_pts, n, d_out, d_flags, d_fs, ctx->stream);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    int bad = 0;
+    CU(cudaMemcpyAsync(&bad, d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(out, d_out, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (bad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    return ok(err);
+}
+
+int poslo_gpu_point_valid(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* pts, uint8_t* okv,
+                          poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (n && (!pts || !okv)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    uint8_t *d_pts, *d_ok;
+    UPLOAD(b_pts, pts, (size_t)n * 32, d_pts);
+    ENSURE(b_verdict, n, d_ok);
+    launch_point_validate(d_pts, n, d_ok, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    if (n) CU(cudaMemcpyAsync(okv, d_ok, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
+int poslo_gpu_seed_retrieve(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t* ds, uint32_t ds_len,
+                            uint32_t ds_capacity, const uint32_t* epochs, uint32_t n,
+                            uint8_t* x0_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (n && (!epochs || !x0_out)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (suite < 1 || suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
+    Guard g(ctx);
+    DsParam dsp;
+    int rc = parse_ds(ds, ds_len, ds_capacity, dsp, err);
+    if (rc) return rc;
+    uint32_t* d_ep;
+    uint4* d_x0;
+    unsigned long long* d_err;
+    UPLOAD(b_epochs, epochs, (size_t)n * 4, d_ep);
+    ENSURE(b_x0, n, d_x0);
+    ENSURE(b_err, 1, d_err);
+    unsigned long long init = ~0ull;
+    CU(cudaMemcpyAsync(d_err, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
+    launch_seed_derive(suite, dsp, d_ep, n, d_x0, d_err, ctx->d_t0, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    unsigned long long key;
+    CU(cudaMemcpyAsync(&key, d_err, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (n) CU(cudaMemcpyAsync(x0_out, d_x0, (size_t)n * 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (key != ~0ull) {
+        uint32_t ep = epochs[key >> 1];
+        return set_err(err, POSLO_SEED_NOT_DISCLOSED, ep, "seed for epoch %u not yet disclosed", ep);
+    }
+    return ok(err);
+}
+
+int poslo_gpu_entry_scalars(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !e_out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    // Force the generic path with per-entry output.
+    Prepared P;
+    poslo_batch nb = *b;
+    int rc = run_hash(ctx, &nb, P, err);  // also validates + derives seeds
+    if (rc) return rc;
+    uint64_t n_entries = P.uniform ? (uint64_t)b->n_epochs * b->n2 : b->epoch_starts[b->n_epochs];
+    uint32_t *d_ent, *d_partial;
+    ENSURE(b_e, std::max<uint64_t>(n_entries, 1) * 8, d_ent);
+    TileMap tm = P.tm;
+    if (P.fast) {  // the fast path used its own tile size; re-tile for generic
+        tm.tile_entries = 1024;
+        tm.tiles_per_epoch = b->n2 ? (b->n2 + 1023) / 1024 : 0;
+        tm.n_tiles = tm.n_epochs * tm.tiles_per_epoch;
+    }
+    ENSURE(b_scratch, (size_t)std::max<uint32_t>(tm.n_tiles, 1024) * 17, d_partial);
+    launch_hash_generic(b->suite, P.lay, tm, static_cast<const uint4*>(ctx->b_x0.p), d_partial, d_ent,
+                        static_cast<unsigned long long*>(ctx->b_err.p), ctx->d_t0, ctx->stream);
+    ctx->launches += 1;
+    CU(cudaGetLastError());
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    if (n_entries) CU(cudaMemcpy(e_out, d_ent, n_entries * 32, cudaMemcpyDeviceToHost));
+    return ok(err);
+}
+
+int poslo_gpu_scalar_sum(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* scalars, uint8_t out[32],
+                         poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!out || (n && !scalars)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    for (uint64_t i = 0; i < n; i++)
+        if (!scalar_canonical(scalars + 32 * i)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    uint32_t *d_in, *d_sum, *d_scr;
+    UPLOAD(b_e, scalars, n * 32, d_in);
+    ENSURE(b_sum, 8, d_sum);
+    ENSURE(b_scratch, 17 * 1024, d_scr);
+    launch_sum_mod_l(d_in, 8, n, nullptr, d_sum, d_scr, ctx->stream);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, d_sum, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
+int poslo_gpu_group_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], const uint8_t* e,
+                          const uint8_t* s, const uint8_t* r, uint8_t* verdicts, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!y || (n && (!e || !s || !r || !verdicts))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    for (uint32_t i = 0; i < n; i++)
+        if (!scalar_canonical(e + 32 * (size_t)i) || !scalar_canonical(s + 32 * (size_t)i))
+            return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    uint32_t *d_e, *d_s;
+    uint8_t* d_r;
+    UPLOAD(b_e, e, (size_t)n * 32, d_e);
+    UPLOAD(b_s, s, (size_t)n * 32, d_s);
+    UPLOAD(b_r, r, (size_t)n * 32, d_r);
+    int rc = group_check_dev(ctx, y, n, d_e, d_s, d_r, verdicts, nullptr, err);
+    if (rc) return rc;
+    return ok(err);
+}
+
+int poslo_gpu_synth_log(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint64_t n,
+                        uint32_t entry_len, void* d_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (n && !d_out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    launch_synth_fixed(seed, first, n, entry_len, static_cast<uint8_t*>(d_out), ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
+}  // extern "C"

@@ -1,0 +1,178 @@
+// Per-entry challenge computation e_i^j = hash_to_scalar(m, onetime_seed(x0_i, j))
+// as a raw 512-bit integer (before the deferred mod-l reduction), for every
+// suite, plus the seed-tree PRF step. Host+device (PHD) so the kernels and
+// the CPU unit tests in tests/native run the same code.
+//   prf            primitives.cpp:113-127
+//   onetime_seed   primitives.cpp:209-223
+//   hash_to_scalar primitives.cpp:149-193 (digest pair H(m||x) || H(0x01||m||x))
+#pragma once
+#include "aes128.cuh"
+#include "sha256.cuh"
+
+namespace poslo_gpu {
+
+// PRF_b(x) = F(x || b)[0:16] on little-endian memory words.
+template <class T0>
+PHD void prf_dev(int suite, const T0& t0, uint32_t x[4], int bit) {
+    if (suite == 1) {
+        uint32_t xw[4] = {bswap32(x[0]), bswap32(x[1]), bswap32(x[2]), bswap32(x[3])}, o[4];
+        prf_sha256(xw, bit, o);
+#pragma unroll
+        for (int k = 0; k < 4; k++) x[k] = bswap32(o[k]);
+    } else {
+        // MMO over 17 bytes: block0 = x, block1 = bit || 0x80 || 0^14
+        uint32_t h[4] = {MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD};
+        uint32_t b1[4] = {(uint32_t)(bit & 1) | 0x8000u, 0, 0, 0};
+        mmo_step(t0, h, x);
+        mmo_step(t0, h, b1);
+#pragma unroll
+        for (int k = 0; k < 4; k++) x[k] = h[k];
+    }
+}
+
+
+struct PlainMsg {  // the untagged stream m || x
+    const uint8_t* m;
+    uint32_t L;
+    uint32_t x[4];  // memory words
+    PHDM uint32_t operator()(uint64_t p) const {
+        if (p < L) return m[p];
+        uint32_t q = (uint32_t)(p - L);
+        return (x[q >> 2] >> (8 * (q & 3))) & 0xffu;
+    }
+};
+struct TaggedMsg {  // 0x01 || m || x
+    PlainMsg inner;
+    PHDM uint32_t operator()(uint64_t p) const { return p == 0 ? 1u : inner(p - 1); }
+};
+struct OtsMsg {  // x0 || be32(j) (AES suites)
+    uint32_t x0[4];
+    uint32_t j;
+    PHDM uint32_t operator()(uint64_t p) const {
+        if (p < 16) return (x0[p >> 2] >> (8 * (p & 3))) & 0xffu;
+        return (j >> (8 * (19 - p))) & 0xffu;
+    }
+};
+
+// Per-entry contribution as a 512-bit integer (16 limbs); false on a
+// suite-3 over-length entry (primitives.cpp:179-181).
+template <class T0>
+PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L,
+                            const uint32_t x0m[4], uint32_t j, uint32_t limbs[16]) {
+    uint32_t x[4];
+    if (suite == 1) {
+        const uint32_t x0w[4] = {bswap32(x0m[0]), bswap32(x0m[1]), bswap32(x0m[2]), bswap32(x0m[3])};
+        uint32_t pre[8], xw[4];
+        ots_pre(x0w, pre);
+        ots_finish(x0w, pre, j, xw);
+#pragma unroll
+        for (int k = 0; k < 4; k++) x[k] = bswap32(xw[k]);
+    } else {
+        OtsMsg om{{x0m[0], x0m[1], x0m[2], x0m[3]}, j};
+        mmo_hash_dev(t0, om, 20, x);
+    }
+    if (suite == 3) {
+        if (L > 31) return false;
+        // (int_be(m) + int_be(x)) < 2^248 + 2^128 < l: no reduction needed
+#pragma unroll
+        for (int k = 0; k < 16; k++) limbs[k] = 0;
+        for (uint32_t p = 0; p < L; p++) {
+            uint32_t bitpos = 8 * (L - 1 - p);
+            limbs[bitpos >> 5] |= (uint32_t)m[p] << (bitpos & 31);
+        }
+        uint32_t xv[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) xv[k] = bswap32(x[3 - k]);  // int_be(x) as LE limbs
+        uint64_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            c += (uint64_t)limbs[k] + (k < 4 ? xv[k] : 0u);
+            limbs[k] = (uint32_t)c;
+            c >>= 32;
+        }
+        return true;
+    }
+    PlainMsg pm{m, L, {x[0], x[1], x[2], x[3]}};
+    TaggedMsg tm{pm};
+    if (suite == 1) {
+        uint32_t H[8];
+        sha256_stream(pm, (uint64_t)L + 16, H);
+#pragma unroll
+        for (int k = 0; k < 8; k++) limbs[15 - k] = H[k];
+        sha256_stream(tm, (uint64_t)L + 17, H);
+#pragma unroll
+        for (int k = 0; k < 8; k++) limbs[7 - k] = H[k];
+    } else {
+        uint32_t h[4], h2[4];
+        mdc2_hash_dev(t0, pm, (uint64_t)L + 16, h, h2);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            limbs[15 - k] = bswap32(h[k]);
+            limbs[11 - k] = bswap32(h2[k]);
+        }
+        mdc2_hash_dev(t0, tm, (uint64_t)L + 17, h, h2);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            limbs[7 - k] = bswap32(h[k]);
+            limbs[3 - k] = bswap32(h2[k]);
+        }
+    }
+    return true;
+}
+
+
+// ---- fast path, suite 1, 32-byte entry: m as 8 big-endian words, x0w the
+// epoch seed as big-endian words with its hoisted onetime_seed mid-state.
+PHD void entry_limbs_s1_l32(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j,
+                            const uint32_t m[8], uint32_t limbs[16]) {
+    uint32_t x[4];
+    ots_finish(x0w, pre, j, x);
+    h2s_sha256_len32(m, x, limbs);
+}
+
+// ---- fast path, suite 2 (MMO/MDC-2), 32-byte entry -----------------------
+// onetime_seed = MMO(x0 || be32 j) over 2 blocks; the first block (x0 under
+// the constant IV key) is hoisted per epoch into hpre. hash_to_scalar =
+// MDC-2(m || x) (48 B -> 4 blocks incl. a full pad block) and
+// MDC-2(0x01 || m || x) (49 B -> 4 blocks), 2 AES per block.
+template <class T0>
+PHD void mdc2_digest_limbs(const T0& t0, const uint32_t blk[16],
+                                                  uint32_t limbs_hi_index, uint32_t limbs[16]) {
+    uint32_t h[4] = {MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD};
+    uint32_t h2[4] = {MDC2_IV2_WORD, MDC2_IV2_WORD, MDC2_IV2_WORD, MDC2_IV2_WORD};
+#pragma unroll
+    for (int b = 0; b < 4; b++) mdc2_step(t0, h, h2, blk + 4 * b);
+    // digest bytes h || h2 read as big-endian words 0..7
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        limbs[limbs_hi_index - k] = bswap32(h[k]);
+        limbs[limbs_hi_index - 4 - k] = bswap32(h2[k]);
+    }
+}
+
+
+template <class T0>
+PHD void entry_limbs_s2_l32(const T0& t0, const uint32_t hpre[4], uint32_t j, const uint32_t m[8],
+                            uint32_t limbs[16]) {
+    // x = MMO(x0 || be32 j): second block = be32(j) || 0x80 || 0^11
+    uint32_t x[4] = {hpre[0], hpre[1], hpre[2], hpre[3]};
+    const uint32_t b1[4] = {bswap32(j), 0x80u, 0, 0};
+    mmo_step(t0, x, b1);
+    // untagged stream m || x || pad (48 B + full pad block)
+    uint32_t blk[16] = {m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7],
+                        x[0], x[1], x[2], x[3], 0x80u, 0, 0, 0};
+    mdc2_digest_limbs(t0, blk, 15, limbs);
+    // tagged stream 0x01 || m || x || 0x80 || 0^14 (49 B -> 64 B):
+    // memory word k = bytes 4k-1 .. 4k+2 of the untagged stream
+    uint32_t tb[16];
+    const uint32_t u[13] = {m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], x[0], x[1], x[2], x[3], 0x80u};
+    tb[0] = 0x01u | (u[0] << 8);
+#pragma unroll
+    for (int k = 1; k < 13; k++) tb[k] = fshr32(u[k - 1], u[k], 24);
+    tb[13] = 0;  // (u[12] >> 24) | (u[13] << 8) with u[13] = 0
+    tb[14] = 0;
+    tb[15] = 0;
+    mdc2_digest_limbs(t0, tb, 7, limbs);
+}
+
+}  // namespace poslo_gpu

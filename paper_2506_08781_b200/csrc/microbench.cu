@@ -1,0 +1,69 @@
+// Integer-pipe peak microbenchmark (SURVEY.md §8d "P_int"): the roofline
+// denominator for the integer-bound hashing kernel. MEASURED_PEAKS.json has
+// HBM and bf16 peaks only, so bench.py measures this live, under the same
+// clocks as the timed region. Modes:
+//   0  ALU pipe only  (LOP3 chains)
+//   1  FMA pipe only  (IMAD chains, multiplier opaque to the compiler)
+//   2  both pipes     (interleaved LOP3 + IMAD, the dual-issue ceiling)
+// Every thread runs 8 independent chains; lane-ops = threads * iters * 8 (16 for mode 2).
+// Not part of the verifier ABI (separate library libposlo_microbench.so).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
+    uint32_t x[8], y[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        x[k] = threadIdx.x * (k + 1) ^ a;
+        y[k] = blockIdx.x + k * b;
+    }
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (MODE == 0 || MODE == 2)
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(x[(k + 1) & 7]));
+            if (MODE == 1 || MODE == 2)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(a), "r"(y[(k + 3) & 7]));
+        }
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) r ^= x[k] + y[k];
+    if (r == 0x12345678u) out[0] = r;
+}
+
+extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s, double* ms_out) {
+    if (cudaSetDevice(device) != cudaSuccess) return 1;
+    cudaDeviceProp p;
+    cudaGetDeviceProperties(&p, device);
+    uint32_t* out;
+    cudaMalloc(&out, 4);
+    int blocks = p.multiProcessorCount * 8;  // 2048 threads per SM
+    int iters = 1 << 16;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto launch = [&]() {
+        if (mode == 0) k_int_peak<0><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
+        else if (mode == 1) k_int_peak<1><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
+        else k_int_peak<2><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
+    };
+    launch();  // warm-up (clock ramp)
+    launch();
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; r++) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double per_iter = mode == 2 ? 16.0 : 8.0;
+    double ops = (double)blocks * 256 * iters * per_iter * reps;
+    *ops_per_s = ops / (ms * 1e-3);
+    if (ms_out) *ms_out = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}

@@ -1,0 +1,95 @@
+// Internal launcher interface between the C-ABI layer (capi.cu) and the
+// kernels (verify_kernels.cu, group_kernels.cu). Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace poslo_gpu {
+
+// One disclosed-seed-stack node, parsed from the SeedStack wire format
+// (proj/src/seed_manager.cpp:32-53).
+struct DsNode {
+    uint32_t depth;
+    uint32_t index;
+    uint32_t value[4];  // 16 seed bytes as little-endian memory words
+};
+struct DsParam {
+    int count;
+    DsNode nodes[32];
+};
+
+// How the entries of the queried epochs are laid out in device memory.
+struct EntryLayout {
+    const uint8_t* payload;   // entry bytes
+    const uint64_t* offsets;  // n_entries + 1 byte offsets, or nullptr (fixed stride)
+    uint32_t entry_len;       // stride / length when offsets == nullptr
+};
+
+// Tiles: a tile is a contiguous run of entries of ONE epoch that one CTA
+// hashes and sums. Uniform batches (every epoch n2 entries, the k-th queried
+// epoch's entries at [k*n2, (k+1)*n2)) use implicit tiles; ragged batches
+// pass an explicit tile table built on the host from epoch_starts.
+struct TileMap {
+    uint32_t n_epochs;
+    uint32_t n2;                    // uniform only
+    uint32_t tile_entries;          // entries per tile (uniform only)
+    uint32_t tiles_per_epoch;       // uniform only
+    const uint4* tiles;             // explicit: {epoch_idx, j0, count, 0}; nullptr = uniform
+    const uint64_t* epoch_starts;   // explicit: n_epochs + 1 entry indices
+    const uint32_t* epoch_tile_begin;  // explicit: n_epochs + 1 tile indices
+    uint32_t n_tiles;
+};
+
+void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
+                        uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s);
+
+// Fast path: suite 1, 32-byte entries, uniform epochs. Writes per-tile
+// 17-limb partial sums, or e_tilde directly when one tile covers an epoch.
+void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
+                        uint32_t* d_partial, uint32_t* d_etilde, cudaStream_t s);
+
+// Fast path: suite 2 (MMO/MDC-2 over AES-128), 32-byte entries, uniform.
+void launch_hash_s2_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
+                        uint32_t* d_partial, uint32_t* d_etilde, const uint32_t* d_t0, cudaStream_t s);
+
+// Generic path: any suite, any entry length, uniform or ragged epochs.
+// Optional per-entry scalars (debug/parity: e_i^j mod l, 8 limbs each).
+void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
+                         uint32_t* d_partial, uint32_t* d_entry_e, unsigned long long* d_err,
+                         const uint32_t* d_t0, cudaStream_t s);
+
+// Per-epoch e~ from tile partials (skipped when tiles_per_epoch == 1 on the
+// fast paths, which finalise in the hashing kernel).
+void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,
+                           cudaStream_t s);
+
+// out (8 limbs) = sum of n items mod l; items are `limbs`-limb little-endian
+// integers (8 for scalars, 17 for partial accumulators). Optional mask: skip
+// item i when mask[i] != 0. d_scratch >= 17 * 1024 u32.
+void launch_sum_mod_l(const uint32_t* d_items, int limbs, uint64_t n, const uint8_t* d_mask,
+                      uint32_t* d_out, uint32_t* d_scratch, cudaStream_t s);
+
+// Segmented variant: out[g] = sum of items [seg[g], seg[g+1]) (mask honoured).
+void launch_segsum_mod_l(const uint32_t* d_items, const uint64_t* d_seg, uint32_t n_groups,
+                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s);
+
+// Batched commit_check: enc[i] = encode(Y^e_i * alpha^s_i); verdict[i] =
+// (enc[i] == r[i]) when r != nullptr. Y is decoded once (d_ybad set when Y
+// is not a valid encoding). e/s are 8-limb canonical scalars.
+void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
+                        const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, int* d_ybad,
+                        cudaStream_t s);
+
+// Fold of n encoded points with the group law (group_combine); d_bad counts
+// invalid encodings. d_scratch >= 1024 * 128 bytes.
+void launch_point_fold(const uint8_t* d_pts, uint64_t n, uint8_t* d_out, int* d_bad,
+                       void* d_scratch, cudaStream_t s);
+
+// Point validation (GroupElement::from_bytes): ok[i] = 1 if valid.
+void launch_point_validate(const uint8_t* d_pts, uint32_t n, uint8_t* d_ok, cudaStream_t s);
+
+// Synthetic fixed-length log entries [first, first+n) (include/poslo_synth.h).
+void launch_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L, uint8_t* d_out,
+                        cudaStream_t s);
+
+}  // namespace poslo_gpu

@@ -1,0 +1,365 @@
+// ristretto255 over edwards25519 for the device group check (stage 3).
+//
+// Replaces the libsodium calls behind the reference's group layer
+// (proj/src/group.cpp): crypto_core_ristretto255_is_valid_point (:107-114),
+// crypto_scalarmult_ristretto255 / _base and _add inside commit_check
+// (:144-167) and group_combine (:169-178), plus the byte-equality of
+// GroupElement::operator== (include/poslo/group.hpp:59).
+//
+// Field GF(2^255-19): 8 x 32-bit limbs, values kept loosely in [0, 2^256)
+// and canonicalised only for encode/compare (2^256 == 38 mod p). Points are
+// extended twisted-Edwards (X:Y:Z:T), a = -1. Ristretto decode/encode and
+// SQRT_RATIO_M1 follow the published ristretto255 definition (RFC 9496 §4);
+// constants were derived from their definitions (oracle/ristretto.py) and the
+// whole layer is pinned against the reference's own outputs
+// (tests/golden/kat.json) on CPU (tests/native) and GPU (tests/test_gpu_*).
+//
+// Verification handles public data only, so everything is variable-time.
+#pragma once
+#include "poslo_common.cuh"
+
+#define FE_D_LIMBS 0x135978a3u, 0x75eb4dcau, 0x4141d8abu, 0x00700a4du, 0x7779e898u, 0x8cc74079u, 0x2b6ffe73u, 0x52036ceeu
+#define FE_D2_LIMBS 0x26b2f159u, 0xebd69b94u, 0x8283b156u, 0x00e0149au, 0xeef3d130u, 0x198e80f2u, 0x56dffce7u, 0x2406d9dcu
+#define FE_SQRTM1_LIMBS 0x4a0ea0b0u, 0xc4ee1b27u, 0xad2fe478u, 0x2f431806u, 0x3dfbd7a7u, 0x2b4d0099u, 0x4fc1df0bu, 0x2b832480u
+#define FE_INVSQRT_A_MINUS_D_LIMBS 0x805d40eau, 0x99c8fdaau, 0x5a4172beu, 0x9d2f1617u, 0xfe01d840u, 0x16c27b91u, 0xcfaffca2u, 0x786c8905u
+#define FE_BASE_X_LIMBS 0x8f25d51au, 0xc9562d60u, 0x9525a7b2u, 0x692cc760u, 0xfdd6dc5cu, 0xc0a4e231u, 0xcd6e53feu, 0x216936d3u
+#define FE_BASE_Y_LIMBS 0x66666658u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u
+#define FE_BASE_T_LIMBS 0xa5b7dda3u, 0x6dde8ab3u, 0x775152f5u, 0x20f09f80u, 0x64abe37du, 0x66ea4e8eu, 0xd78b7665u, 0x67875f0fu
+
+struct fe {
+    uint32_t v[8];
+};
+
+struct gpt {  // extended coordinates, x = X/Z, y = Y/Z, xy = T/Z
+    fe X, Y, Z, T;
+};
+
+PHD fe fe_from(const uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4, uint32_t a5,
+               uint32_t a6, uint32_t a7) {
+    fe r;
+    r.v[0] = a0; r.v[1] = a1; r.v[2] = a2; r.v[3] = a3;
+    r.v[4] = a4; r.v[5] = a5; r.v[6] = a6; r.v[7] = a7;
+    return r;
+}
+#define FE_CONST(LIMBS) fe_from(LIMBS)
+
+PHD fe fe_zero() { return fe_from(0, 0, 0, 0, 0, 0, 0, 0); }
+PHD fe fe_one() { return fe_from(1, 0, 0, 0, 0, 0, 0, 0); }
+
+// r = a + 38 * c folded until no carry remains (c is the overflow count).
+PHD void fe_fold(uint32_t r[8], uint64_t c) {
+    for (int pass = 0; pass < 2; pass++) {
+        uint64_t t = c * 38;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            t += r[i];
+            r[i] = (uint32_t)t;
+            t >>= 32;
+        }
+        c = t;
+    }
+}
+
+PHD fe fe_add(const fe& a, const fe& b) {
+    fe r;
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        c += (uint64_t)a.v[i] + b.v[i];
+        r.v[i] = (uint32_t)c;
+        c >>= 32;
+    }
+    fe_fold(r.v, c);
+    return r;
+}
+
+PHD fe fe_sub(const fe& a, const fe& b) {
+    fe r;
+    int64_t bw = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int64_t t = (int64_t)a.v[i] - b.v[i] + bw;
+        r.v[i] = (uint32_t)t;
+        bw = t >> 32;
+    }
+    // a wrapped: true value = r - 2^256 == r - 38 (mod p); at most twice
+    for (int pass = 0; pass < 2 && bw; pass++) {
+        int64_t t2 = -38;
+        bw = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            int64_t t = (int64_t)r.v[i] + (i == 0 ? t2 : 0) + bw;
+            r.v[i] = (uint32_t)t;
+            bw = t >> 32;
+        }
+    }
+    return r;
+}
+
+PHD fe fe_mul(const fe& a, const fe& b) {
+    uint32_t t[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) t[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            uint64_t p = (uint64_t)a.v[i] * b.v[j] + t[i + j] + carry;
+            t[i + j] = (uint32_t)p;
+            carry = p >> 32;
+        }
+        t[i + 8] = (uint32_t)carry;
+    }
+    fe r;
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        c += (uint64_t)t[i] + (uint64_t)t[i + 8] * 38;
+        r.v[i] = (uint32_t)c;
+        c >>= 32;
+    }
+    fe_fold(r.v, c);
+    return r;
+}
+
+PHD fe fe_sq(const fe& a) { return fe_mul(a, a); }
+
+PHD fe fe_sqn(fe a, int n) {
+    for (int i = 0; i < n; i++) a = fe_sq(a);
+    return a;
+}
+
+// Canonical representative in [0, p).
+PHD fe fe_canon(const fe& a) {
+    fe r = a;
+    // fold bit 255: r = (r mod 2^255) + 19 * (r >> 255)  (< 2^255 + 19)
+    uint32_t top = r.v[7] >> 31;
+    r.v[7] &= 0x7fffffffu;
+    uint64_t c = (uint64_t)top * 19;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        c += r.v[i];
+        r.v[i] = (uint32_t)c;
+        c >>= 32;
+    }
+    // r >= p  <=>  r + 19 >= 2^255
+    fe s;
+    c = 19;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        c += r.v[i];
+        s.v[i] = (uint32_t)c;
+        c >>= 32;
+    }
+    if (s.v[7] >> 31) {
+        s.v[7] &= 0x7fffffffu;
+        return s;
+    }
+    return r;
+}
+
+PHD bool fe_is_neg(const fe& a) { return fe_canon(a).v[0] & 1; }
+
+PHD bool fe_is_zero(const fe& a) {
+    fe c = fe_canon(a);
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) x |= c.v[i];
+    return x == 0;
+}
+
+PHD bool fe_eq(const fe& a, const fe& b) { return fe_is_zero(fe_sub(a, b)); }
+
+PHD fe fe_neg(const fe& a) { return fe_sub(fe_zero(), a); }
+
+PHD fe fe_abs(const fe& a) { return fe_is_neg(a) ? fe_neg(a) : a; }
+
+// z^((p-5)/8) = z^(2^252 - 3)
+PHD fe fe_pow22523(const fe& z) {
+    fe z2 = fe_sq(z);
+    fe z3 = fe_mul(z2, z);                       // 2^2 - 1
+    fe z15 = fe_mul(fe_sqn(z3, 2), z3);          // 2^4 - 1
+    fe z31 = fe_mul(fe_sq(z15), z);              // 2^5 - 1
+    fe z10 = fe_mul(fe_sqn(z31, 5), z31);        // 2^10 - 1
+    fe z20 = fe_mul(fe_sqn(z10, 10), z10);       // 2^20 - 1
+    fe z40 = fe_mul(fe_sqn(z20, 20), z20);       // 2^40 - 1
+    fe z50 = fe_mul(fe_sqn(z40, 10), z10);       // 2^50 - 1
+    fe z100 = fe_mul(fe_sqn(z50, 50), z50);      // 2^100 - 1
+    fe z200 = fe_mul(fe_sqn(z100, 100), z100);   // 2^200 - 1
+    fe z250 = fe_mul(fe_sqn(z200, 50), z50);     // 2^250 - 1
+    return fe_mul(fe_sqn(z250, 2), z);           // 2^252 - 3
+}
+
+// SQRT_RATIO_M1(u, v): returns was_square, r = non-negative root.
+PHD bool fe_sqrt_ratio_m1(const fe& u, const fe& v, fe& r) {
+    const fe sqrtm1 = FE_CONST(FE_SQRTM1_LIMBS);
+    fe v3 = fe_mul(fe_sq(v), v);
+    fe v7 = fe_mul(fe_sq(v3), v);
+    r = fe_mul(fe_mul(u, v3), fe_pow22523(fe_mul(u, v7)));
+    fe check = fe_mul(v, fe_sq(r));
+    fe nu = fe_neg(u);
+    bool correct = fe_eq(check, u);
+    bool flipped = fe_eq(check, nu);
+    bool flipped_i = fe_eq(check, fe_mul(nu, sqrtm1));
+    if (flipped || flipped_i) r = fe_mul(r, sqrtm1);
+    r = fe_abs(r);
+    return correct || flipped;
+}
+
+PHD fe fe_from_bytes_le(const uint8_t b[32]) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        r.v[i] = (uint32_t)b[4 * i] | (uint32_t)b[4 * i + 1] << 8 | (uint32_t)b[4 * i + 2] << 16 |
+                 (uint32_t)b[4 * i + 3] << 24;
+    return r;
+}
+
+PHD void fe_to_bytes_le(const fe& a, uint8_t b[32]) {
+    fe c = fe_canon(a);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        b[4 * i] = (uint8_t)c.v[i];
+        b[4 * i + 1] = (uint8_t)(c.v[i] >> 8);
+        b[4 * i + 2] = (uint8_t)(c.v[i] >> 16);
+        b[4 * i + 3] = (uint8_t)(c.v[i] >> 24);
+    }
+}
+
+PHD gpt pt_identity() {
+    gpt p;
+    p.X = fe_zero(); p.Y = fe_one(); p.Z = fe_one(); p.T = fe_zero();
+    return p;
+}
+
+PHD gpt pt_base() {
+    gpt p;
+    p.X = FE_CONST(FE_BASE_X_LIMBS);
+    p.Y = FE_CONST(FE_BASE_Y_LIMBS);
+    p.Z = fe_one();
+    p.T = FE_CONST(FE_BASE_T_LIMBS);
+    return p;
+}
+
+// add-2008-hwcd-3 (a = -1, k = 2d)
+PHD gpt pt_add(const gpt& p, const gpt& q) {
+    const fe d2 = FE_CONST(FE_D2_LIMBS);
+    fe A = fe_mul(fe_sub(p.Y, p.X), fe_sub(q.Y, q.X));
+    fe B = fe_mul(fe_add(p.Y, p.X), fe_add(q.Y, q.X));
+    fe C = fe_mul(fe_mul(p.T, d2), q.T);
+    fe D = fe_mul(fe_add(p.Z, p.Z), q.Z);
+    fe E = fe_sub(B, A), F = fe_sub(D, C), G = fe_add(D, C), H = fe_add(B, A);
+    gpt r;
+    r.X = fe_mul(E, F);
+    r.Y = fe_mul(G, H);
+    r.T = fe_mul(E, H);
+    r.Z = fe_mul(F, G);
+    return r;
+}
+
+// dbl-2008-hwcd (a = -1): D = -A, G = B - A, F = G - C, H = -A - B
+PHD gpt pt_dbl(const gpt& p) {
+    fe A = fe_sq(p.X);
+    fe B = fe_sq(p.Y);
+    fe C = fe_sq(p.Z);
+    C = fe_add(C, C);
+    fe E = fe_sub(fe_sub(fe_sq(fe_add(p.X, p.Y)), A), B);
+    fe G = fe_sub(B, A);
+    fe F = fe_sub(G, C);
+    fe H = fe_neg(fe_add(A, B));
+    gpt r;
+    r.X = fe_mul(E, F);
+    r.Y = fe_mul(G, H);
+    r.T = fe_mul(E, H);
+    r.Z = fe_mul(F, G);
+    return r;
+}
+
+PHD gpt pt_neg(const gpt& p) {
+    gpt r = p;
+    r.X = fe_neg(p.X);
+    r.T = fe_neg(p.T);
+    return r;
+}
+
+// Ristretto decode with full validation (RFC 9496 §4.3.1); false = invalid
+// encoding, exactly the set crypto_core_ristretto255_is_valid_point rejects.
+PHD bool rist_decode(const uint8_t b[32], gpt& out) {
+    fe s = fe_from_bytes_le(b);
+    // canonical: s < p (so bit 255 clear) and non-negative
+    fe sc = fe_canon(s);
+    bool canonical = true;
+#pragma unroll
+    for (int i = 0; i < 8; i++) canonical = canonical && (sc.v[i] == s.v[i]);
+    if (!canonical || (s.v[0] & 1)) return false;
+    const fe d = FE_CONST(FE_D_LIMBS);
+    fe ss = fe_sq(s);
+    fe u1 = fe_sub(fe_one(), ss);
+    fe u2 = fe_add(fe_one(), ss);
+    fe u2sq = fe_sq(u2);
+    fe v = fe_sub(fe_neg(fe_mul(d, fe_sq(u1))), u2sq);
+    fe inv;
+    bool was_square = fe_sqrt_ratio_m1(fe_one(), fe_mul(v, u2sq), inv);
+    fe den_x = fe_mul(inv, u2);
+    fe den_y = fe_mul(fe_mul(inv, den_x), v);
+    fe x = fe_abs(fe_mul(fe_add(s, s), den_x));
+    fe y = fe_mul(u1, den_y);
+    fe t = fe_mul(x, y);
+    if (!was_square || fe_is_neg(t) || fe_is_zero(y)) return false;
+    out.X = x;
+    out.Y = y;
+    out.Z = fe_one();
+    out.T = t;
+    return true;
+}
+
+// Ristretto encode (RFC 9496 §4.3.2) -> 32 canonical bytes.
+PHD void rist_encode(const gpt& p, uint8_t out[32]) {
+    const fe sqrtm1 = FE_CONST(FE_SQRTM1_LIMBS);
+    const fe isqrt_amd = FE_CONST(FE_INVSQRT_A_MINUS_D_LIMBS);
+    fe u1 = fe_mul(fe_add(p.Z, p.Y), fe_sub(p.Z, p.Y));
+    fe u2 = fe_mul(p.X, p.Y);
+    fe inv;
+    fe_sqrt_ratio_m1(fe_one(), fe_mul(u1, fe_sq(u2)), inv);
+    fe den1 = fe_mul(inv, u1);
+    fe den2 = fe_mul(inv, u2);
+    fe z_inv = fe_mul(fe_mul(den1, den2), p.T);
+    fe ix0 = fe_mul(p.X, sqrtm1);
+    fe iy0 = fe_mul(p.Y, sqrtm1);
+    fe enchanted = fe_mul(den1, isqrt_amd);
+    bool rotate = fe_is_neg(fe_mul(p.T, z_inv));
+    fe x = rotate ? iy0 : p.X;
+    fe y = rotate ? ix0 : p.Y;
+    fe den_inv = rotate ? enchanted : den2;
+    if (fe_is_neg(fe_mul(x, z_inv))) y = fe_neg(y);
+    fe s = fe_abs(fe_mul(den_inv, fe_sub(p.Z, y)));
+    fe_to_bytes_le(s, out);
+}
+
+// Scalar bit i of a canonical 32-byte little-endian scalar held as 8 limbs.
+PHD int sc_bit(const uint32_t s[8], int i) { return (s[i >> 5] >> (i & 31)) & 1; }
+
+// Y^e * alpha^s as a point: joint (Shamir) double-and-add over 253 bits.
+PHD gpt double_scalarmult(const gpt& Y, const uint32_t e[8], const uint32_t s[8]) {
+    gpt B = pt_base();
+    gpt YB = pt_add(Y, B);
+    gpt acc = pt_identity();
+    bool started = false;
+    for (int i = 252; i >= 0; i--) {
+        if (started) acc = pt_dbl(acc);
+        int be = sc_bit(e, i), bs = sc_bit(s, i);
+        if (be | bs) {
+            const gpt& q = (be && bs) ? YB : (be ? Y : B);
+            acc = started ? pt_add(acc, q) : q;
+            started = true;
+        }
+    }
+    return acc;
+}
+
+// commit_check(Y, e, s) (group.cpp:144-167) -> encoding of Y^e * alpha^s.
+PHD void commit_check_enc(const gpt& Y, const uint32_t e[8], const uint32_t s[8], uint8_t out[32]) {
+    gpt P = double_scalarmult(Y, e, s);
+    rist_encode(P, out);
+}

@@ -1,0 +1,266 @@
+// Stages 0-2 of the batch verifier on sm_100a:
+//   K0 seed_derive   sr -> sc -> prf      (seed_manager.cpp:71-85, :5-16; primitives.cpp:113-127)
+//   K1 hash          onetime_seed + hash_to_scalar (primitives.cpp:149-223)
+//   K2 segmented sum Scalar::add folds    (batch_verify.cpp:37-42, :84-85; distiller.cpp:160-176)
+// K1 and the entry->epoch level of K2 are one fused kernel: each CTA hashes a
+// tile of one epoch, keeps the raw 512-bit digests in a 17-limb per-thread
+// accumulator (deferred reduction, see scalar.cuh), reduces across the CTA
+// with warp shuffles + shared memory, and reduces mod l once per epoch.
+#include "../../include/poslo_synth.h"
+#include "entry_hash.cuh"
+#include "tile_common.cuh"
+
+namespace poslo_gpu {
+
+namespace {
+
+using namespace tilec;
+
+// ---------------------------------------------------------------- K0
+__global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict__ epochs,
+                              uint32_t n, uint4* __restrict__ x0, unsigned long long* err,
+                              const uint32_t* __restrict__ t0g) {
+    extern __shared__ uint32_t sT0[];
+    if (suite != 1) load_t0(sT0, t0g);
+    SmemT0 t0{sT0, threadIdx.x & 31u};
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint32_t q = epochs[k];
+    // sr: scan from the top of the stack (seed_manager.cpp:74-84)
+    for (int c = ds.count - 1; c >= 0; c--) {
+        const DsNode& nd = ds.nodes[c];
+        uint64_t lo = (uint64_t)nd.index << nd.depth;
+        uint64_t hi = (uint64_t)(uint32_t)(nd.index + 1u) << nd.depth;
+        if (q >= hi && c == ds.count - 1) break;
+        if (q >= lo && q < hi) {
+            uint32_t x[4] = {nd.value[0], nd.value[1], nd.value[2], nd.value[3]};
+            uint32_t rel = q - (uint32_t)lo;
+            for (int j = (int)nd.depth - 1; j >= 0; j--) prf_dev(suite, t0, x, (rel >> j) & 1);
+            x0[k] = make_uint4(x[0], x[1], x[2], x[3]);
+            return;
+        }
+    }
+    x0[k] = make_uint4(0, 0, 0, 0);
+    err_min(err, (unsigned long long)k << 1);  // SeedNotDisclosed, before hashing errors
+}
+
+// ---------------------------------------------------------------- generic K1+K2
+__global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay, TileMap tm,
+                                                      const uint4* __restrict__ x0,
+                                                      uint32_t* __restrict__ partial,
+                                                      uint32_t* __restrict__ entry_e,
+                                                      unsigned long long* err,
+                                                      const uint32_t* __restrict__ t0g) {
+    extern __shared__ uint32_t sT0[];
+    __shared__ uint32_t red[8 * 17];
+    if (suite != 1) load_t0(sT0, t0g);
+    SmemT0 t0{sT0, threadIdx.x & 31u};
+    const uint32_t tile = blockIdx.x;
+    uint32_t ep, j0, count;
+    uint64_t ebase;
+    if (tm.tiles) {
+        uint4 t = tm.tiles[tile];
+        ep = t.x; j0 = t.y; count = t.z;
+        ebase = tm.epoch_starts[ep];
+    } else {
+        ep = tile / tm.tiles_per_epoch;
+        uint32_t sub = tile - ep * tm.tiles_per_epoch;
+        j0 = sub * tm.tile_entries;
+        count = min(tm.tile_entries, tm.n2 - j0);
+        ebase = (uint64_t)ep * tm.n2;
+    }
+    const uint4 xr = __ldg(x0 + ep);
+    const uint32_t x0m[4] = {xr.x, xr.y, xr.z, xr.w};
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint32_t idx = threadIdx.x; idx < count; idx += blockDim.x) {
+        const uint32_t j = j0 + idx;
+        const uint64_t ent = ebase + j;
+        const uint8_t* m;
+        uint32_t L;
+        if (lay.offsets) {
+            uint64_t o0 = lay.offsets[ent], o1 = lay.offsets[ent + 1];
+            m = lay.payload + o0;
+            L = (uint32_t)(o1 - o0);
+        } else {
+            m = lay.payload + ent * lay.entry_len;
+            L = lay.entry_len;
+        }
+        uint32_t limbs[16];
+        if (!entry_limbs(suite, t0, m, L, x0m, j, limbs)) {
+            err_min(err, ((unsigned long long)ep << 1) | 1ull);  // FormatError
+            continue;
+        }
+        acc17_add16(acc, limbs);
+        if (entry_e) {
+            uint32_t e[8];
+            sc_reduce_limbs(limbs, 16, e);
+#pragma unroll
+            for (int k = 0; k < 8; k++) entry_e[ent * 8 + k] = e[k];
+        }
+    }
+    block_reduce_acc17(acc, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < 17; k++) partial[(size_t)tile * 17 + k] = acc[k];
+}
+
+// ---------------------------------------------------------------- epoch finalize
+__global__ void k_epoch_finalize(TileMap tm, const uint32_t* __restrict__ partial,
+                                 uint32_t* __restrict__ etilde) {
+    uint32_t ep = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ep >= tm.n_epochs) return;
+    uint32_t b, e;
+    if (tm.tiles) {
+        b = tm.epoch_tile_begin[ep];
+        e = tm.epoch_tile_begin[ep + 1];
+    } else {
+        b = ep * tm.tiles_per_epoch;
+        e = b + tm.tiles_per_epoch;
+    }
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint32_t t = b; t < e; t++) {
+        uint32_t v[17];
+#pragma unroll
+        for (int k = 0; k < 17; k++) v[k] = partial[(size_t)t * 17 + k];
+        acc17_add17(acc, v);
+    }
+    uint32_t r[8];
+    sc_reduce_limbs(acc, 17, r);
+#pragma unroll
+    for (int k = 0; k < 8; k++) etilde[(size_t)ep * 8 + k] = r[k];
+}
+
+// ---------------------------------------------------------------- sums mod l
+__device__ __forceinline__ void load_item(const uint32_t* items, int limbs, uint64_t i, uint32_t v[17]) {
+#pragma unroll
+    for (int k = 0; k < 17; k++) v[k] = k < limbs ? items[i * limbs + k] : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_sum_stage1(const uint32_t* __restrict__ items, int limbs,
+                                                    uint64_t n, const uint8_t* __restrict__ mask,
+                                                    uint32_t* __restrict__ out) {
+    __shared__ uint32_t red[8 * 17];
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (mask && mask[i]) continue;
+        uint32_t v[17];
+        load_item(items, limbs, i, v);
+        acc17_add17(acc, v);
+    }
+    block_reduce_acc17(acc, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < 17; k++) out[blockIdx.x * 17 + k] = acc[k];
+}
+
+__global__ void __launch_bounds__(256) k_sum_stage2(const uint32_t* __restrict__ parts, uint32_t n,
+                                                    uint32_t* __restrict__ out) {
+    __shared__ uint32_t red[8 * 17];
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        uint32_t v[17];
+        load_item(parts, 17, i, v);
+        acc17_add17(acc, v);
+    }
+    block_reduce_acc17(acc, red);
+    if (threadIdx.x == 0) {
+        uint32_t r[8];
+        sc_reduce_limbs(acc, 17, r);
+#pragma unroll
+        for (int k = 0; k < 8; k++) out[k] = r[k];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_segsum(const uint32_t* __restrict__ items,
+                                                const uint64_t* __restrict__ seg,
+                                                const uint8_t* __restrict__ mask,
+                                                uint32_t* __restrict__ out) {
+    __shared__ uint32_t red[8 * 17];
+    const uint32_t g = blockIdx.x;
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint64_t i = seg[g] + threadIdx.x; i < seg[g + 1]; i += blockDim.x) {
+        if (mask && mask[i]) continue;
+        uint32_t v[17];
+        load_item(items, 8, i, v);
+        acc17_add17(acc, v);
+    }
+    block_reduce_acc17(acc, red);
+    if (threadIdx.x == 0) {
+        uint32_t r[8];
+        sc_reduce_limbs(acc, 17, r);
+#pragma unroll
+        for (int k = 0; k < 8; k++) out[(size_t)g * 8 + k] = r[k];
+    }
+}
+
+// ---------------------------------------------------------------- synthetic logs
+// Counter-based synthetic entries (include/poslo_synth.h), byte-identical to
+// what the CPU reference harness regenerates (oracle/ref_tools/ref_tool.cpp).
+__global__ void k_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L,
+                              uint8_t* __restrict__ out) {
+    uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    uint64_t k = first + t;
+    if ((L & 7) == 0 && ((uintptr_t)out & 7) == 0) {
+        uint64_t* o = reinterpret_cast<uint64_t*>(out + t * L);
+        for (uint32_t w = 0; w < L / 8; w++) o[w] = poslo_synth_word(seed, k, w);
+    } else {
+        for (uint32_t b = 0; b < L; b++) out[t * L + b] = poslo_synth_byte(seed, k, b);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
+                        uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s) {
+    if (n_epochs == 0) return;
+    int T = 128;
+    size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
+    if (smem) cudaFuncSetAttribute(k_seed_derive, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_seed_derive<<<(n_epochs + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, n_epochs, d_x0, d_err, d_t0);
+}
+
+void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
+                         uint32_t* d_partial, uint32_t* d_entry_e, unsigned long long* d_err,
+                         const uint32_t* d_t0, cudaStream_t s) {
+    uint32_t n_tiles = tm.tiles ? tm.n_tiles : tm.n_epochs * tm.tiles_per_epoch;
+    if (!n_tiles) return;
+    size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
+    if (smem) cudaFuncSetAttribute(k_hash_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_hash_generic<<<n_tiles, 256, smem, s>>>(suite, lay, tm, d_x0, d_partial, d_entry_e, d_err, d_t0);
+}
+
+void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,
+                           cudaStream_t s) {
+    if (!tm.n_epochs) return;
+    k_epoch_finalize<<<(tm.n_epochs + 127) / 128, 128, 0, s>>>(tm, d_partial, d_etilde);
+}
+
+void launch_sum_mod_l(const uint32_t* d_items, int limbs, uint64_t n, const uint8_t* d_mask,
+                      uint32_t* d_out, uint32_t* d_scratch, cudaStream_t s) {
+    uint64_t want = (n + 255) / 256;
+    uint32_t blocks = (uint32_t)(want < 1 ? 1 : (want > 1024 ? 1024 : want));
+    k_sum_stage1<<<blocks, 256, 0, s>>>(d_items, limbs, n, d_mask, d_scratch);
+    k_sum_stage2<<<1, 256, 0, s>>>(d_scratch, blocks, d_out);
+}
+
+void launch_segsum_mod_l(const uint32_t* d_items, const uint64_t* d_seg, uint32_t n_groups,
+                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s) {
+    if (!n_groups) return;
+    k_segsum<<<n_groups, 256, 0, s>>>(d_items, d_seg, d_mask, d_out);
+}
+
+void launch_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L, uint8_t* d_out,
+                        cudaStream_t s) {
+    if (!n) return;
+    k_synth_fixed<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, first, n, L, d_out);
+}
+
+}  // namespace poslo_gpu

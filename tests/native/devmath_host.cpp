@@ -1,0 +1,130 @@
+// CPU harness over the device math headers (paper_2506_08781_b200/csrc/*.cuh)
+// compiled as plain C++: lets tests/test_devmath_host.py pin the kernels'
+// arithmetic (SHA-256/AES/MMO/MDC-2 per-entry paths, deferred mod-l
+// reduction, ristretto255) against the reference's golden vectors without a
+// GPU. Test infrastructure only — the product never runs this code on a CPU.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2506_08781_b200/csrc/entry_hash.cuh"
+#include "../../paper_2506_08781_b200/csrc/ristretto.cuh"
+#include "../../paper_2506_08781_b200/csrc/scalar.cuh"
+
+using namespace poslo_gpu;
+
+namespace {
+struct HostT0 {
+    uint32_t t[256];
+    HostT0() {
+        for (int x = 0; x < 256; x++) t[x] = aes_t0_entry(aes_sbox_compute(x));
+    }
+    uint32_t operator()(uint32_t x) const { return t[x]; }
+};
+const HostT0& T0() {
+    static HostT0 t;
+    return t;
+}
+void words_le(const uint8_t* b, uint32_t* w, int n) {
+    for (int i = 0; i < n; i++) w[i] = b[4 * i] | b[4 * i + 1] << 8 | b[4 * i + 2] << 16 | (uint32_t)b[4 * i + 3] << 24;
+}
+void le_words_out(const uint32_t* w, uint8_t* b, int n) {
+    for (int i = 0; i < n; i++)
+        for (int k = 0; k < 4; k++) b[4 * i + k] = (uint8_t)(w[i] >> (8 * k));
+}
+}  // namespace
+
+extern "C" {
+
+// prf (seed tree step)
+void dm_prf(int suite, int bit, const uint8_t x[16], uint8_t out[16]) {
+    uint32_t w[4];
+    words_le(x, w, 4);
+    prf_dev(suite, T0(), w, bit);
+    le_words_out(w, out, 4);
+}
+
+// e = hash_to_scalar(m, onetime_seed(x0, j)) mod l via the generic path;
+// returns 0, or 1 for FormatError
+int dm_entry_generic(int suite, const uint8_t* m, uint32_t L, const uint8_t x0[16], uint32_t j,
+                     uint8_t e_out[32], uint32_t limbs_out[16]) {
+    uint32_t x0m[4], limbs[16], e[8];
+    words_le(x0, x0m, 4);
+    if (!entry_limbs(suite, T0(), m, L, x0m, j, limbs)) return 1;
+    sc_reduce_limbs(limbs, 16, e);
+    le_words_out(e, e_out, 8);
+    if (limbs_out) std::memcpy(limbs_out, limbs, 64);
+    return 0;
+}
+
+// the 32-byte fast paths (suite 1 / suite 2)
+void dm_entry_fast32(int suite, const uint8_t m[32], const uint8_t x0[16], uint32_t j,
+                     uint32_t limbs_out[16]) {
+    uint32_t x0m[4], mm[8];
+    words_le(x0, x0m, 4);
+    words_le(m, mm, 8);
+    if (suite == 1) {
+        uint32_t x0w[4], mw[8], pre[8];
+        for (int k = 0; k < 4; k++) x0w[k] = bswap32(x0m[k]);
+        for (int k = 0; k < 8; k++) mw[k] = bswap32(mm[k]);
+        ots_pre(x0w, pre);
+        entry_limbs_s1_l32(x0w, pre, j, mw, limbs_out);
+    } else {
+        uint32_t hpre[4] = {MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD};
+        mmo_step(T0(), hpre, x0m);
+        entry_limbs_s2_l32(T0(), hpre, j, mm, limbs_out);
+    }
+}
+
+// sum of n 16-limb values via the 17-limb accumulator, reduced mod l
+void dm_sum_reduce(const uint32_t* limbs16, uint32_t n, uint8_t e_out[32]) {
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint32_t i = 0; i < n; i++) acc17_add16(acc, limbs16 + 16 * i);
+    uint32_t e[8];
+    sc_reduce_limbs(acc, 17, e);
+    le_words_out(e, e_out, 8);
+}
+
+void dm_reduce_wide_be(const uint8_t in[64], uint8_t out[32]) {
+    uint32_t limbs[16];
+    for (int k = 0; k < 16; k++) limbs[15 - k] = load_be32p(in + 4 * k);
+    uint32_t e[8];
+    sc_reduce_limbs(limbs, 16, e);
+    le_words_out(e, out, 8);
+}
+
+void dm_sc_add(const uint8_t a[32], const uint8_t b[32], uint8_t out[32]) {
+    uint32_t x[8], y[8], r[8];
+    words_le(a, x, 8);
+    words_le(b, y, 8);
+    sc_add(x, y, r);
+    le_words_out(r, out, 8);
+}
+
+int dm_point_valid(const uint8_t p[32]) {
+    gpt P;
+    return rist_decode(p, P) ? 1 : 0;
+}
+
+int dm_commit_check(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32], uint8_t out[32]) {
+    gpt Y;
+    if (!rist_decode(y, Y)) return 1;
+    uint32_t ee[8], ss[8];
+    words_le(e, ee, 8);
+    words_le(s, ss, 8);
+    commit_check_enc(Y, ee, ss, out);
+    return 0;
+}
+
+int dm_fold(uint32_t n, const uint8_t* pts, uint8_t out[32]) {
+    gpt acc = pt_identity();
+    for (uint32_t i = 0; i < n; i++) {
+        gpt P;
+        if (!rist_decode(pts + 32 * i, P)) return 1;
+        acc = pt_add(acc, P);
+    }
+    rist_encode(acc, out);
+    return 0;
+}
+
+}  // extern "C"

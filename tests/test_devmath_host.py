@@ -1,0 +1,106 @@
+"""The device math headers (paper_2506_08781_b200/csrc/*.cuh) compiled for the
+host by tests/native/devmath_host.cpp, checked against the pinned oracle and
+the reference's golden vectors. Catches arithmetic bugs before GPU time; the
+GPU parity tests re-check the same on the device. CPU only."""
+import ctypes
+import os
+import random
+import subprocess
+
+import pytest
+
+from oracle import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "native", "devmath_host.cpp")
+LIB = os.path.join(ROOT, "tests", "native", "build", "libdevmath_host.so")
+
+
+@pytest.fixture(scope="module")
+def dm():
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-Wno-unknown-pragmas",
+                           "-o", LIB, SRC])
+    return ctypes.CDLL(LIB)
+
+
+def out(n):
+    return ctypes.create_string_buffer(n)
+
+
+@pytest.mark.parametrize("suite", [1, 2, 3])
+def test_prf(dm, kat, suite):
+    x0 = bytes(range(16))
+    for bit, key in ((0, "prf0"), (1, "prf1")):
+        o = out(16)
+        dm.dm_prf(suite, bit, x0, o)
+        assert o.raw.hex() == kat[f"suite{suite}"][key]
+
+
+@pytest.mark.parametrize("suite", [1, 2, 3])
+def test_entry_generic(dm, suite):
+    rng = random.Random(suite)
+    for t in range(200):
+        L = rng.randint(1, 31) if suite == 3 else rng.choice([0, 1, 15, 16, 17, 31, 32, 33, 47, 48, 55, 56,
+                                                              63, 64, 100, 200, rng.randint(0, 300)])
+        m = bytes(rng.getrandbits(8) for _ in range(L))
+        x0 = bytes(rng.getrandbits(8) for _ in range(16))
+        j = t if t < 8 else rng.getrandbits(32)
+        o = out(32)
+        assert dm.dm_entry_generic(suite, m, L, x0, j, o, None) == 0
+        assert o.raw == O.hash_to_scalar(suite, m, O.onetime_seed(suite, x0, j))
+    if suite == 3:
+        assert dm.dm_entry_generic(3, bytes(32), 32, bytes(16), 0, out(32), None) == 1
+
+
+@pytest.mark.parametrize("suite", [1, 2])
+def test_entry_fast32_and_deferred_sum(dm, suite):
+    rng = random.Random(10 + suite)
+    n = 64
+    limbs = (ctypes.c_uint32 * (16 * n))()
+    ref = bytes(32)
+    for t in range(n):
+        m = bytes(rng.getrandbits(8) for _ in range(32))
+        x0 = bytes(rng.getrandbits(8) for _ in range(16))
+        j = rng.getrandbits(32)
+        one = (ctypes.c_uint32 * 16)()
+        dm.dm_entry_fast32(suite, m, x0, j, one)
+        for k in range(16):
+            limbs[16 * t + k] = one[k]
+        ref = O.sc_add(ref, O.hash_to_scalar(suite, m, O.onetime_seed(suite, x0, j)))
+    o = out(32)
+    dm.dm_sum_reduce(limbs, n, o)
+    assert o.raw == ref  # sum of raw digests reduced once == sum of reductions
+
+
+def test_deferred_sum_worst_case(dm):
+    # all-ones digests maximise carries through the 17-limb accumulator
+    n = 4096
+    limbs = (ctypes.c_uint32 * (16 * n))(*([0xFFFFFFFF] * (16 * n)))
+    o = out(32)
+    dm.dm_sum_reduce(limbs, n, o)
+    assert int.from_bytes(o.raw, "little") == (n * (2**512 - 1)) % O.L
+
+
+def test_scalar_ops(dm, kat):
+    for w, r in kat["reduce_wide_be"]:
+        o = out(32)
+        dm.dm_reduce_wide_be(bytes.fromhex(w), o)
+        assert o.raw.hex() == r
+    for a, b, c, _ in kat["scalar_add"]:
+        o = out(32)
+        dm.dm_sc_add(bytes.fromhex(a), bytes.fromhex(b), o)
+        assert o.raw.hex() == c
+
+
+def test_group_ops(dm, kat):
+    for Y, e, s, P in kat["commit_check"]:
+        o = out(32)
+        assert dm.dm_commit_check(bytes.fromhex(Y), bytes.fromhex(e), bytes.fromhex(s), o) == 0
+        assert o.raw.hex() == P
+    for p, v in kat["point_valid"]:
+        assert dm.dm_point_valid(bytes.fromhex(p)) == v
+    for a, b, c in kat["group_combine"]:
+        o = out(32)
+        assert dm.dm_fold(2, bytes.fromhex(a) + bytes.fromhex(b), o) == 0
+        assert o.raw.hex() == c

@@ -1,0 +1,243 @@
+"""Device parity: every stage of the CUDA path against the reference's own
+golden outputs (tests/golden, from the UNMODIFIED reference) and the pinned
+CPU oracle on the same seeded inputs. Bit-exact throughout (integer work)."""
+import random
+
+import numpy as np
+import pytest
+
+from conftest import STREAMS, load_golden
+from golden_util import Stream
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def A():
+    from paper_2506_08781_b200 import api
+    return api
+
+
+# ------------------------------------------------------------------ golden streams
+@pytest.mark.parametrize("name", STREAMS)
+def test_agg_ekeys_matches_reference(verifier, name):
+    st = Stream(load_golden(name + ".json"))
+    suite, pk, ds = st.api_objects()
+    parts, e_hat = verifier.agg_ekeys(suite, st.batches, ds, 4)
+    assert [p[0] for p in parts] == sorted(st.batches)
+    assert [p[1] for p in parts] == st.e_tilde
+    assert e_hat == st.e_hat
+
+
+@pytest.mark.parametrize("name", STREAMS)
+def test_paver_matches_reference(verifier, name):
+    st = Stream(load_golden(name + ".json"))
+    suite, pk, ds = st.api_objects()
+    assert verifier.paver(pk, st.batches, st.s_hat, None, ds, 8) == bool(st.d["paver"])
+    assert verifier.paver(pk, st.batches, st.s_hat, st.r_hat_agg, ds, 2) == bool(st.d["paver_agg"])
+
+
+@pytest.mark.parametrize("name", STREAMS)
+def test_epoch_verdicts_match_reference(verifier, name):
+    """Per-epoch accept/reject (the distiller's per-epoch aver, tamper localisation)."""
+    st = Stream(load_golden(name + ".json"))
+    suite, pk, ds = st.api_objects()
+    s_hats = {i: st.sigs[i].s_hat_le for i in range(st.n1)}
+    # each epoch signature carries its own ds; the final ds covers every epoch
+    verdicts = verifier.epoch_verify(pk, st.batches, s_hats, ds)
+    assert [int(v) for v in verdicts] == st.d["epoch_verdicts"]
+    assert [i for i, v in enumerate(verdicts) if not v] == st.d["invalid_epochs"]
+
+
+@pytest.mark.parametrize("name", STREAMS)
+def test_sebver_matches_reference(verifier, name):
+    st = Stream(load_golden(name + ".json"))
+    api = A()
+    c = st.ccd
+    suite = api.SuiteConfig(c["suite"], c["n1"], c["n2"], c["n_u"])
+    ds, _ = api.SeedStack.deserialize(c["ds"], c["depth"])
+    res = verifier.sebver(st.pk.y, suite, st.batches, ds, c["next"], c["invalid"], c["umbrellas"],
+                          c["valid"] if c["has_valid"] else None)
+    assert [int(b) for b in res["U"]] == st.d["sebver_U"]
+    assert [int(b) for b in res["I"]] == st.d["sebver_I"]
+    if "sebver_V" in st.d:
+        assert [int(b) for b in res["V"]] == st.d["sebver_V"]
+
+
+# ------------------------------------------------------------------ stage parity
+@pytest.mark.parametrize("suite", [1, 2, 3])
+def test_seed_retrieve_matches_reference(verifier, kat, suite):
+    api = A()
+    d = kat[f"suite{suite}"]
+    ds, _ = api.SeedStack.deserialize(bytes.fromhex(d["ds_after_11"]), 4)
+    got = verifier.seed_retrieve(suite, ds, list(range(12)))
+    assert [g.hex() for g in got] == d["sr"]
+    with pytest.raises(api.SeedNotDisclosed) as ei:
+        verifier.seed_retrieve(suite, ds, [3, 12, 13])
+    assert ei.value.epoch == 12
+
+
+@pytest.mark.parametrize("suite", [1, 2, 3])
+def test_entry_scalars_match_oracle(verifier, suite):
+    api = A()
+    rng = random.Random(100 + suite)
+    n1, n2 = 8, 16
+    maxlen = 31 if suite == 3 else 300
+    batches = {i: [bytes(rng.getrandbits(8) for _ in range(rng.randint(1, maxlen))) for _ in range(n2)]
+               for i in range(n1)}
+    root = bytes(rng.getrandbits(8) for _ in range(16))
+    ds = api.SeedStack(3, [api.SeedNode(3, 0, root)])
+    got = verifier.entry_scalars(api.SuiteConfig(suite, n1, n2, 1), batches, ds)
+    k = 0
+    for i in range(n1):
+        _, x0 = O.sr(suite, ds.serialize(), 3, i)
+        for j, m in enumerate(batches[i]):
+            assert got[k] == O.hash_to_scalar(suite, m, O.onetime_seed(suite, x0, j)), (i, j)
+            k += 1
+
+
+def test_group_primitives_match_reference(verifier, kat):
+    rows = kat["commit_check"]
+    for Y, e, s, P in rows:
+        assert verifier.commit_check(bytes.fromhex(Y), bytes.fromhex(e), bytes.fromhex(s)).hex() == P
+    for s, p in kat["exp_base"]:
+        assert verifier.exp_base(bytes.fromhex(s)).hex() == p
+    for a, b, c in kat["group_combine"]:
+        assert verifier.group_combine(bytes.fromhex(a), bytes.fromhex(b)).hex() == c
+    pts = [bytes.fromhex(p) for p, _ in kat["point_valid"]]
+    assert verifier.is_valid_point_batch(pts) == [bool(v) for _, v in kat["point_valid"]]
+
+
+def test_commit_check_batched(verifier, kat):
+    rows = kat["commit_check"][5:]
+    Y = bytes.fromhex(rows[0][0])
+    es = [bytes.fromhex(r[1]) for r in rows]
+    ss = [bytes.fromhex(r[2]) for r in rows]
+    got = verifier.commit_check_batch(Y, es, ss)
+    from oracle import ristretto as R
+    for e, s, g in zip(es, ss, got):
+        assert g == R.commit_check(Y, e, s)
+
+
+# ------------------------------------------------------------------ synthetic scale parity
+def _synthetic(suite, n1, n2, L, seed, ragged=False):
+    api = A()
+    rng = np.random.default_rng(seed)
+    if ragged:
+        lens = rng.integers(0 if suite != 3 else 1, (31 if suite == 3 else 700) + 1, size=n1 * n2)
+        pay = rng.integers(0, 256, size=int(lens.sum()), dtype=np.uint8).tobytes()
+        offs = np.zeros(len(lens) + 1, dtype=np.uint64)
+        np.cumsum(lens, out=offs[1:])
+        ents = [pay[offs[t]:offs[t + 1]] for t in range(n1 * n2)]
+    else:
+        pay = rng.integers(0, 256, size=n1 * n2 * L, dtype=np.uint8).tobytes()
+        ents = [pay[t * L:(t + 1) * L] for t in range(n1 * n2)]
+    batches = {i: ents[i * n2:(i + 1) * n2] for i in range(n1)}
+    D = max(1, (n1 - 1).bit_length())
+    root = bytes(rng.integers(0, 256, 16, dtype=np.uint8))
+    ds = api.SeedStack(D, [api.SeedNode(D, 0, root)])
+    return api.SuiteConfig(suite, 1 << D, n2, 1), batches, ds
+
+
+def _oracle_etilde(suite, batches, ds):
+    epochs = sorted(batches)
+    flat = [m for i in epochs for m in batches[i]]
+    offs = np.zeros(len(flat) + 1, dtype=np.uint64)
+    np.cumsum([len(m) for m in flat], out=offs[1:])
+    starts = np.zeros(len(epochs) + 1, dtype=np.uint64)
+    np.cumsum([len(batches[i]) for i in epochs], out=starts[1:])
+    rc, _, et = O.agg_ekeys_packed(suite, b"".join(flat), offs, 0, epochs, starts, ds.serialize(),
+                                   ds.capacity)
+    assert rc == 0
+    return et
+
+
+@pytest.mark.parametrize("suite,n1,n2,L", [
+    (1, 64, 256, 32), (1, 16, 1024, 32), (1, 4, 3000, 32), (1, 300, 5, 32),
+    (2, 32, 256, 32), (2, 4, 1100, 32), (1, 32, 64, 48), (2, 16, 64, 17), (3, 32, 64, 31),
+])
+def test_uniform_batches_match_oracle(verifier, suite, n1, n2, L):
+    cfg, batches, ds = _synthetic(suite, n1, n2, L, seed=n1 * 7 + n2 + L + suite)
+    parts, e_hat = verifier.agg_ekeys(cfg, batches, ds, 1)
+    ref = _oracle_etilde(suite, batches, ds)
+    assert [p[1] for p in parts] == ref
+    assert e_hat == O.sum_scalars(ref)
+
+
+@pytest.mark.parametrize("suite", [1, 2, 3])
+def test_ragged_batches_match_oracle(verifier, suite):
+    """Variable-length entries (incl. empty ones) and uneven epoch sizes."""
+    cfg, batches, ds = _synthetic(suite, 24, 40, 0, seed=77 + suite, ragged=True)
+    rng = random.Random(suite)
+    for i in list(batches)[::3]:
+        batches[i] = batches[i][:rng.randint(0, len(batches[i]))]  # uneven / empty epochs
+    parts, e_hat = verifier.agg_ekeys(cfg, batches, ds, 1)
+    ref = _oracle_etilde(suite, batches, ds)
+    assert [p[1] for p in parts] == ref
+    assert e_hat == O.sum_scalars(ref)
+
+
+def test_sparse_epoch_query(verifier):
+    """Queried epochs need not be contiguous (map keys)."""
+    cfg, batches, ds = _synthetic(1, 64, 32, 32, seed=5)
+    sub = {i: batches[i] for i in (0, 3, 17, 40, 63)}
+    parts, e_hat = verifier.agg_ekeys(cfg, sub, ds, 1)
+    assert [p[1] for p in parts] == _oracle_etilde(1, sub, ds)
+
+
+def test_empty_batch(verifier):
+    cfg, batches, ds = _synthetic(1, 4, 4, 32, seed=1)
+    parts, e_hat = verifier.agg_ekeys(cfg, {}, ds, 1)
+    assert parts == [] and e_hat == bytes(32)
+
+
+# ------------------------------------------------------------------ error taxonomy and order
+def test_errors_follow_reference_order(verifier):
+    api = A()
+    st = Stream(load_golden("stream_s1_tamper.json"))
+    suite, pk, ds = st.api_objects()
+    # workers == 0 -> StateError (batch_verify.cpp:15, test_batch_verify.cpp:66-73)
+    with pytest.raises(api.StateError):
+        verifier.agg_ekeys(suite, st.batches, ds, 0)
+    with pytest.raises(api.StateError):
+        verifier.paver(pk, st.batches, st.s_hat, None, ds, 0)
+    # undisclosed epoch -> SeedNotDisclosed naming it (test_batch_verify.cpp:75-80)
+    b2 = dict(st.batches)
+    b2[40] = b2[0]
+    b2[35] = b2[1]
+    with pytest.raises(api.SeedNotDisclosed) as ei:
+        verifier.agg_ekeys(suite, b2, ds, 4)
+    assert ei.value.epoch == 35  # lowest, as with workers == 1
+    # batch size != n2 -> StateError before anything else (batch_verify.cpp:68-70)
+    b3 = dict(b2)
+    b3[2] = b3[2][:-1]
+    with pytest.raises(api.StateError):
+        verifier.paver(pk, b3, st.s_hat, None, ds, 1)
+    # missing commitment -> StateError (batch_verify.cpp:76-79)
+    pk2 = api.PoslocPublicKey(pk.suite, pk.y, {k: v for k, v in pk.r_hats.items() if k != 7})
+    with pytest.raises(api.StateError):
+        verifier.paver(pk2, st.batches, st.s_hat, None, ds, 1)
+    # ... but not with an aggregate commitment
+    assert verifier.paver(pk2, st.batches, st.s_hat, st.r_hat_agg, ds, 1) is False
+
+
+def test_suite3_format_error_vs_seed_error_order(verifier):
+    api = A()
+    cfg, batches, ds = _synthetic(3, 4, 4, 16, seed=3)
+    ds = api.SeedStack(ds.capacity, [api.SeedNode(1, 0, ds.nodes[0].value)])  # covers epochs 0,1
+    bad = dict(batches)
+    bad[1] = [bad[1][0] + bytes(20)] + bad[1][1:]  # 36-byte entry in epoch 1
+    with pytest.raises(api.FormatError):
+        verifier.agg_ekeys(cfg, bad, ds, 1)  # epoch 1 hashing error before epoch 2's seed error
+    ok = dict(batches)
+    ok[3] = [ok[3][0] + bytes(20)] + ok[3][1:]
+    with pytest.raises(api.SeedNotDisclosed) as ei:
+        verifier.agg_ekeys(cfg, ok, ds, 1)  # epoch 2 undisclosed wins over epoch 3
+    assert ei.value.epoch == 2
+
+
+def test_device_reports_launches(verifier):
+    st = Stream(load_golden("stream_s1_n256.json"))
+    suite, pk, ds = st.api_objects()
+    verifier.paver(pk, st.batches, st.s_hat, None, ds, 1)
+    assert verifier.last_launches() >= 4
