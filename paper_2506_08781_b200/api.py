@@ -416,6 +416,21 @@ class Verifier:
     def exp_base(self, s: bytes) -> bytes:
         return self.commit_check(bytes(32), bytes(32), s)
 
+    def scalar_sum(self, scalars: Sequence[bytes]) -> bytes:
+        """Sum mod l on the device (rank-ordered fold of shard partials)."""
+        out = ctypes.create_string_buffer(32)
+        self._call(self._lib.poslo_gpu_scalar_sum, len(scalars),
+                   _buf(b"".join(scalars)) if scalars else None, out)
+        return out.raw
+
+    def group_check(self, y: bytes, es: Sequence[bytes], ss: Sequence[bytes], rs: Sequence[bytes]):
+        """verdict[i] = (commit_check(Y, e_i, s_i) == R_i) (batch_verify.cpp:86)."""
+        n = len(es)
+        out = ctypes.create_string_buffer(max(n, 1))
+        self._call(self._lib.poslo_gpu_group_check, n, _buf(y), _buf(b"".join(es)), _buf(b"".join(ss)),
+                   _buf(b"".join(rs)), out)
+        return [bool(out.raw[k]) for k in range(n)]
+
     def group_fold(self, pts: Sequence[bytes]) -> bytes:
         out = ctypes.create_string_buffer(32)
         self._call(self._lib.poslo_gpu_group_fold, len(pts), _buf(b"".join(pts)) if pts else None,

