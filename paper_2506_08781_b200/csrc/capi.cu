@@ -35,11 +35,19 @@ struct poslo_gpu_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;  // H2D of host-resident logs, overlapped with hashing
+    std::vector<cudaEvent_t> chunk_ev;
     std::mutex mtx;
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
         b_y, b_pts, b_foldscratch, b_rhat;
+    // fixed-base comb tables: generator (built once) and the last Y seen
+    void* d_tabB = nullptr;
+    void* d_tabY = nullptr;
+    void* d_pk = nullptr;
+    uint8_t tabY_key[32] = {};
+    bool tabY_valid = false;
     bool timing = false;
     cudaEvent_t ev[7] = {};
     float last_ms[6] = {};
@@ -48,6 +56,7 @@ struct poslo_gpu_ctx {
 
 namespace {
 
+constexpr uint64_t kChunkBytes = 64ull << 20;
 constexpr int kEvSeed = 0, kEvHash = 1, kEvFin = 2, kEvSum = 3, kEvGroup = 4, kEvEnd = 5;
 
 int set_err(poslo_error* err, int code, uint32_t epoch, const char* fmt, ...) {
@@ -172,15 +181,21 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     ENSURE(b_err, 1, d_err);
     ENSURE(b_etilde, (size_t)n_ep * 8, P.d_etilde);
 
-    // entry layout (H2D when host-resident)
+    // entry layout (H2D when host-resident). Large uniform fixed-length logs
+    // stream in epoch-aligned 64 MiB chunks on the copy stream, each chunk's
+    // hashing waiting only for its own bytes (SPEC.md:496 chunked streaming).
     P.lay.entry_len = b->entry_len;
+    const uint64_t epoch_bytes = (uint64_t)b->n2 * b->entry_len;
+    const bool chunked = !b->device_resident && P.uniform && !b->offsets && epoch_bytes > 0 &&
+                         b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
     if (b->device_resident) {
         P.lay.payload = b->payload;
         P.lay.offsets = b->offsets;
     } else {
         uint8_t* d_pay;
         ENSURE(b_payload, b->payload_bytes, d_pay);
-        if (b->payload_bytes) CU(cudaMemcpyAsync(d_pay, b->payload, b->payload_bytes, cudaMemcpyHostToDevice, s));
+        if (b->payload_bytes && !chunked)
+            CU(cudaMemcpyAsync(d_pay, b->payload, b->payload_bytes, cudaMemcpyHostToDevice, s));
         P.lay.payload = d_pay;
         P.lay.offsets = nullptr;
         if (b->offsets) {
@@ -242,17 +257,43 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         tm.n_tiles = (uint32_t)tiles.size();
     }
     ENSURE(b_partial, (size_t)std::max<uint32_t>(tm.n_tiles, 1) * 17, d_partial);
-    bool need_finalize = true;
-    if (P.fast) {
-        if (b->suite == 1)
-            launch_hash_s1_l32(P.lay, tm, d_x0, d_partial, P.d_etilde, s);
-        else
-            launch_hash_s2_l32(P.lay, tm, d_x0, d_partial, P.d_etilde, ctx->d_t0, s);
-        ctx->launches += tm.n_tiles ? 1 : 0;
-        need_finalize = tm.tiles_per_epoch != 1;
-    } else {
-        launch_hash_generic(b->suite, P.lay, tm, d_x0, d_partial, nullptr, d_err, ctx->d_t0, s);
-        ctx->launches += tm.n_tiles ? 1 : 0;
+    bool need_finalize = P.fast ? tm.tiles_per_epoch != 1 : true;
+    auto launch_hash = [&](const TileMap& t) {
+        if (P.fast) {
+            if (b->suite == 1)
+                launch_hash_s1_l32(P.lay, t, d_x0, d_partial, P.d_etilde, s);
+            else
+                launch_hash_s2_l32(P.lay, t, d_x0, d_partial, P.d_etilde, ctx->d_t0, s);
+        } else {
+            launch_hash_generic(b->suite, P.lay, t, d_x0, d_partial, nullptr, d_err, ctx->d_t0, s);
+        }
+        ctx->launches += 1;
+    };
+    if (chunked) {
+        const uint32_t epc = (uint32_t)std::max<uint64_t>(1, kChunkBytes / epoch_bytes);
+        const uint32_t n_chunks = (n_ep + epc - 1) / epc;
+        while (ctx->chunk_ev.size() < n_chunks + 1) {
+            cudaEvent_t ev;
+            CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            ctx->chunk_ev.push_back(ev);
+        }
+        // the copy stream must not overwrite the buffer before earlier work on s is done
+        CU(cudaEventRecord(ctx->chunk_ev[n_chunks], s));
+        CU(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[n_chunks], 0));
+        uint8_t* d_pay = const_cast<uint8_t*>(P.lay.payload);
+        for (uint32_t c = 0; c < n_chunks; c++) {
+            uint32_t e0 = c * epc, e1 = std::min<uint32_t>(n_ep, e0 + epc);
+            uint64_t off = (uint64_t)e0 * epoch_bytes, bytes = (uint64_t)(e1 - e0) * epoch_bytes;
+            CU(cudaMemcpyAsync(d_pay + off, b->payload + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
+            CU(cudaEventRecord(ctx->chunk_ev[c], ctx->copy));
+            CU(cudaStreamWaitEvent(s, ctx->chunk_ev[c], 0));
+            TileMap t = tm;
+            t.tile_begin = e0 * tm.tiles_per_epoch;
+            t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
+            if (t.tile_count) launch_hash(t);
+        }
+    } else if (tm.n_tiles) {
+        launch_hash(tm);
     }
     mark(ctx, kEvFin);
     if (need_finalize && n_ep) {
@@ -314,20 +355,48 @@ int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void*
         ptr = static_cast<decltype(ptr)>(p_);                                     \
     } while (0)
 
+// Comb tables of alpha (once per context) and of Y (cached per Y value).
+// Y validation (GroupElement::from_bytes) happens in the table build.
+int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err) {
+    if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * 128));
+    if (!ctx->d_tabB) {
+        CU(cudaMalloc(&ctx->d_tabB, kCombTableBytes));
+        launch_build_table(nullptr, ctx->d_pk, ctx->d_tabB, d_flags, ctx->stream);
+        ctx->launches += 2;
+    }
+    if (!ctx->d_tabY) CU(cudaMalloc(&ctx->d_tabY, kCombTableBytes));
+    if (!ctx->tabY_valid || std::memcmp(ctx->tabY_key, y, 32) != 0) {
+        uint8_t* d_y;
+        UPLOAD(b_y, y, 32, d_y);
+        launch_build_table(d_y, ctx->d_pk, ctx->d_tabY, d_flags, ctx->stream);
+        ctx->launches += 2;
+        int bad = 0;
+        CU(cudaMemcpyAsync(&bad, d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (bad) {
+            ctx->tabY_valid = false;
+            return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+        }
+        std::memcpy(ctx->tabY_key, y, 32);
+        ctx->tabY_valid = true;
+    }
+    return POSLO_OK;
+}
+
 // Batched group check on device arrays; verdicts/encodings to host.
 int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const uint32_t* d_e,
                     const uint32_t* d_s, const uint8_t* d_r, uint8_t* h_verdict, uint8_t* h_enc,
                     poslo_error* err) {
-    uint8_t* d_y;
     int* d_flags;
     uint8_t* d_verdict = nullptr;
     uint8_t* d_enc = nullptr;
-    UPLOAD(b_y, y, 32, d_y);
     ENSURE(b_flags, 4, d_flags);
     CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    int rc = ensure_tables(ctx, y, d_flags, err);
+    if (rc) return rc;
     if (h_verdict) ENSURE(b_verdict, n, d_verdict);
     if (h_enc) ENSURE(b_enc, (size_t)n * 32, d_enc);
-    launch_group_check(d_y, n, d_e, d_s, d_r, d_enc, d_verdict, d_flags, ctx->stream);
+    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, n, d_e, d_s, d_r, d_enc, d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     int ybad = 0;
@@ -378,6 +447,11 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
         return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
     }
     ctx->stream = ctx->own;
+    e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        poslo_gpu_destroy(ctx);
+        return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
+    }
     uint32_t t0[256];
     for (int x = 0; x < 256; x++) t0[x] = aes_t0_entry(aes_sbox_compute(x));
     e = cudaMalloc(&ctx->d_t0, sizeof t0);
@@ -402,8 +476,12 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
+    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_pk})
+        if (p) cudaFree(p);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->chunk_ev) cudaEventDestroy(ev);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }
@@ -507,10 +585,8 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
         if (bad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
     }
     // 4. one commitment check (:86)
-    uint32_t launches = ctx->launches;
     rc = group_check_dev(ctx, y, 1, d_sum, d_s, d_rhat, verdict, nullptr, err);
     if (rc) return rc;
-    ctx->launches = launches + 1;
     finish_timing(ctx);
     return ok(err);
 }
@@ -536,10 +612,8 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     mark(ctx, kEvGroup);
     rc = check_hash_errors(ctx, b, err);
     if (rc) return rc;
-    uint32_t launches = ctx->launches;
     rc = group_check_dev(ctx, y, b->n_epochs, P.d_etilde, d_s, d_r, verdicts, nullptr, err);
     if (rc) return rc;
-    ctx->launches = launches + (b->n_epochs ? 1 : 0);
     if (e_tilde_out && b->n_epochs)
         CU(cudaMemcpy(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost));
     finish_timing(ctx);
@@ -617,10 +691,8 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[3
     UPLOAD(b_s, hs.data(), hs.size(), d_s);
     UPLOAD(b_r, hr.data(), hr.size(), d_r);
     std::vector<uint8_t> bits(ng);
-    uint32_t launches = ctx->launches;
     rc = group_check_dev(ctx, y, ng, d_e, d_s, d_r, bits.data(), nullptr, err);
     if (rc) return rc;
-    ctx->launches = launches + 1;
     gi = 0;
     if (nV) *v_bit = bits[gi++];
     for (uint32_t u = 0; u < nU; u++) u_bits[u] = bits[gi++];

@@ -123,11 +123,12 @@ PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L,
 
 // ---- fast path, suite 1, 32-byte entry: m as 8 big-endian words, x0w the
 // epoch seed as big-endian words with its hoisted onetime_seed mid-state.
+template <int MODE = 0>
 PHD void entry_limbs_s1_l32(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j,
-                            const uint32_t m[8], uint32_t limbs[16]) {
+                            const uint32_t m[8], uint32_t limbs[16], uint32_t one = 1) {
     uint32_t x[4];
-    ots_finish(x0w, pre, j, x);
-    h2s_sha256_len32(m, x, limbs);
+    ots_finish<MODE>(x0w, pre, j, x, one);
+    h2s_sha256_len32<MODE>(m, x, limbs, one);
 }
 
 // ---- fast path, suite 2 (MMO/MDC-2), 32-byte entry -----------------------

@@ -102,6 +102,121 @@ __global__ void k_validate(const uint8_t* __restrict__ pts, uint32_t n, uint8_t*
     ok[i] = rist_decode(b, P) ? 1 : 0;
 }
 
+// ---- comb tables ------------------------------------------------------------
+// Builds the fixed-base table of P (decoded from `enc`, or the ristretto255
+// generator when enc == nullptr). Stage A (one thread): P_k = 16^k P. Stage B
+// (one thread per entry): (i+1) P_k in cached form.
+__global__ void k_table_pow16(const uint8_t* __restrict__ enc, gpt* __restrict__ pk, int* bad) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    gpt P;
+    if (enc) {
+        uint8_t b[32];
+        load32(enc, b);
+        if (!rist_decode(b, P)) {
+            atomicOr(bad, 1);
+            P = pt_identity();
+        }
+    } else {
+        P = pt_base();
+    }
+    for (int k = 0; k < 64; k++) {
+        pk[k] = P;
+        P = pt_dbl(pt_dbl(pt_dbl(pt_dbl(P))));
+    }
+}
+
+__global__ void k_table_fill(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 512) return;
+    int k = t >> 3, i = t & 7;
+    gpt base = pk[k];
+    gpt q = base;
+    for (int m = 0; m < i; m++) q = pt_add(q, base);
+    tab[t] = pt_to_cached(q);
+}
+
+// One CTA of 128 threads per check (latency mode, few checks): thread t < 64
+// takes window t of e from Y's table, thread 64 + t window t of s from the
+// generator's table; a 7-level shared-memory tree adds the 128 points.
+__global__ void __launch_bounds__(128) k_check_cta(const gcached* __restrict__ tabY,
+                                                   const gcached* __restrict__ tabB,
+                                                   const uint32_t* __restrict__ e,
+                                                   const uint32_t* __restrict__ s,
+                                                   const uint8_t* __restrict__ r,
+                                                   uint8_t* __restrict__ enc,
+                                                   uint8_t* __restrict__ verdict) {
+    __shared__ int8_t dig[128];
+    __shared__ gpt sh[128];
+    const uint32_t i = blockIdx.x;
+    if (threadIdx.x < 2) {
+        uint32_t v[8];
+        const uint32_t* src = threadIdx.x == 0 ? e : s;
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = src[(size_t)i * 8 + k];
+        int8_t d[64];
+        sc_signed_radix16(v, d);
+        for (int k = 0; k < 64; k++) dig[64 * threadIdx.x + k] = d[k];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int dgt = dig[t];
+    gpt acc = pt_identity();
+    if (dgt) acc = pt_add_cached(acc, table_pick(t < 64 ? tabY : tabB, t & 63, dgt));
+    sh[t] = acc;
+    __syncthreads();
+    for (int w = 64; w >= 1; w >>= 1) {
+        if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
+        __syncthreads();
+    }
+    if (t == 0) {
+        uint8_t out[32];
+        rist_encode(sh[0], out);
+        if (enc)
+#pragma unroll
+            for (int k = 0; k < 32; k++) enc[(size_t)i * 32 + k] = out[k];
+        if (r && verdict) {
+            uint32_t diff = 0;
+#pragma unroll
+            for (int k = 0; k < 32; k++) diff |= out[k] ^ r[(size_t)i * 32 + k];
+            verdict[i] = diff == 0;
+        }
+    }
+}
+
+// One thread per check (throughput mode, e.g. 2^20 per-epoch checks).
+__global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict__ tabY,
+                                                      const gcached* __restrict__ tabB, uint32_t n,
+                                                      const uint32_t* __restrict__ e,
+                                                      const uint32_t* __restrict__ s,
+                                                      const uint8_t* __restrict__ r,
+                                                      uint8_t* __restrict__ enc,
+                                                      uint8_t* __restrict__ verdict) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t v[8];
+    int8_t d[64];
+    gpt acc = pt_identity();
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = e[(size_t)i * 8 + k];
+    sc_signed_radix16(v, d);
+    acc = comb_mul_add(acc, tabY, d);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = s[(size_t)i * 8 + k];
+    sc_signed_radix16(v, d);
+    acc = comb_mul_add(acc, tabB, d);
+    uint8_t out[32];
+    rist_encode(acc, out);
+    if (enc)
+#pragma unroll
+        for (int k = 0; k < 32; k++) enc[(size_t)i * 32 + k] = out[k];
+    if (r && verdict) {
+        uint32_t diff = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k++) diff |= out[k] ^ r[(size_t)i * 32 + k];
+        verdict[i] = diff == 0;
+    }
+}
+
 }  // namespace
 
 void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
@@ -123,6 +238,24 @@ void launch_point_fold(const uint8_t* d_pts, uint64_t n, uint8_t* d_out, int* d_
 void launch_point_validate(const uint8_t* d_pts, uint32_t n, uint8_t* d_ok, cudaStream_t s) {
     if (!n) return;
     k_validate<<<(n + 127) / 128, 128, 0, s>>>(d_pts, n, d_ok);
+}
+
+void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
+                        cudaStream_t s) {
+    k_table_pow16<<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
+    k_table_fill<<<4, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
+}
+
+void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n, const uint32_t* d_e,
+                             const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
+                             cudaStream_t s) {
+    if (!n) return;
+    const gcached* ty = static_cast<const gcached*>(d_tabY);
+    const gcached* tb = static_cast<const gcached*>(d_tabB);
+    if (n <= 1024)
+        k_check_cta<<<n, 128, 0, s>>>(ty, tb, d_e, d_s, d_r, d_enc, d_verdict);
+    else
+        k_check_thread<<<(n + 127) / 128, 128, 0, s>>>(ty, tb, n, d_e, d_s, d_r, d_enc, d_verdict);
 }
 
 }  // namespace poslo_gpu

@@ -17,12 +17,12 @@ __global__ void __launch_bounds__(T) k_hash_s2_l32(const uint4* __restrict__ pay
                                                    uint32_t tpe, const uint4* __restrict__ x0,
                                                    uint32_t* __restrict__ partial,
                                                    uint32_t* __restrict__ etilde,
-                                                   const uint32_t* __restrict__ t0g) {
+                                                   const uint32_t* __restrict__ t0g, uint32_t tile0) {
     extern __shared__ uint32_t sT0[];
     __shared__ uint32_t red[(T / 32) * 17];
     load_t0(sT0, t0g);
     SmemT0 t0{sT0, threadIdx.x & 31u};
-    const uint32_t tile = blockIdx.x;
+    const uint32_t tile = tile0 + blockIdx.x;
     const uint32_t ep = tile / tpe, sub = tile - ep * tpe;
     const uint4 xr = __ldg(x0 + ep);
     const uint32_t x0m[4] = {xr.x, xr.y, xr.z, xr.w};
@@ -52,19 +52,19 @@ __global__ void __launch_bounds__(T) k_hash_s2_l32(const uint4* __restrict__ pay
 
 void launch_hash_s2_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
                         uint32_t* d_partial, uint32_t* d_etilde, const uint32_t* d_t0, cudaStream_t s) {
-    uint32_t n_tiles = tm.n_epochs * tm.tiles_per_epoch;
+    uint32_t n_tiles = tm.tile_count ? tm.tile_count : tm.n_epochs * tm.tiles_per_epoch;
     if (!n_tiles) return;
     const uint4* pay = reinterpret_cast<const uint4*>(lay.payload);
     size_t smem = kAesSmemWords * sizeof(uint32_t);
     if (tm.tile_entries == 256 * 4) {
         cudaFuncSetAttribute(k_hash_s2_l32<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_hash_s2_l32<256, 4><<<n_tiles, 256, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0);
+        k_hash_s2_l32<256, 4><<<n_tiles, 256, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0, tm.tile_begin);
     } else if (tm.tile_entries == 128 * 2) {
         cudaFuncSetAttribute(k_hash_s2_l32<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_hash_s2_l32<128, 2><<<n_tiles, 128, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0);
+        k_hash_s2_l32<128, 2><<<n_tiles, 128, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0, tm.tile_begin);
     } else {
         cudaFuncSetAttribute(k_hash_s2_l32<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_hash_s2_l32<128, 1><<<n_tiles, 128, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0);
+        k_hash_s2_l32<128, 1><<<n_tiles, 128, smem, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, d_t0, tm.tile_begin);
     }
 }
 

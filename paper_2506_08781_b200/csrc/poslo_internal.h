@@ -38,6 +38,8 @@ struct TileMap {
     const uint64_t* epoch_starts;   // explicit: n_epochs + 1 entry indices
     const uint32_t* epoch_tile_begin;  // explicit: n_epochs + 1 tile indices
     uint32_t n_tiles;
+    uint32_t tile_begin;  // launch only tiles [tile_begin, tile_begin + tile_count) (chunked H2D)
+    uint32_t tile_count;  // 0 = all tiles
 };
 
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
@@ -79,6 +81,17 @@ void launch_segsum_mod_l(const uint32_t* d_items, const uint64_t* d_seg, uint32_
 void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
                         const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, int* d_ybad,
                         cudaStream_t s);
+
+// Fixed-base comb table (512 cached points, 64 KiB) of the point encoded at
+// d_enc, or of the generator when d_enc == nullptr. d_pk_scratch >= 64 * 128 B.
+constexpr size_t kCombTableBytes = 512 * 128;
+void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
+                        cudaStream_t s);
+// commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,
+// thread-per-check above).
+void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n, const uint32_t* d_e,
+                             const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
+                             cudaStream_t s);
 
 // Fold of n encoded points with the group law (group_combine); d_bad counts
 // invalid encodings. d_scratch >= 1024 * 128 bytes.

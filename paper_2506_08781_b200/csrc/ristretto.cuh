@@ -363,3 +363,71 @@ PHD void commit_check_enc(const gpt& Y, const uint32_t e[8], const uint32_t s[8]
     gpt P = double_scalarmult(Y, e, s);
     rist_encode(P, out);
 }
+
+// ---- fixed-base comb tables (stage 3 v2) ---------------------------------
+// For a base P: tab[8k + i] = (i+1) * 16^k * P, k = 0..63, i = 0..7, in the
+// "cached" form (Y+X, Y-X, 2Z, 2dT) so one table addition costs 8 muls. With
+// signed radix-16 digits s = sum d_k 16^k, d_k in [-8, 8), a scalar
+// multiplication is 64 table additions and NO doublings. Y is fixed per
+// public key and alpha is fixed forever, so both exponentiations of
+// commit_check become fixed-base.
+struct gcached {
+    fe YpX, YmX, Z2, T2d;
+};
+
+PHD gcached pt_to_cached(const gpt& p) {
+    const fe d2 = FE_CONST(FE_D2_LIMBS);
+    gcached c;
+    c.YpX = fe_add(p.Y, p.X);
+    c.YmX = fe_sub(p.Y, p.X);
+    c.Z2 = fe_add(p.Z, p.Z);
+    c.T2d = fe_mul(p.T, d2);
+    return c;
+}
+
+PHD gcached cached_neg(const gcached& c) {
+    gcached r;
+    r.YpX = c.YmX;
+    r.YmX = c.YpX;
+    r.Z2 = c.Z2;
+    r.T2d = fe_neg(c.T2d);
+    return r;
+}
+
+PHD gpt pt_add_cached(const gpt& p, const gcached& q) {
+    fe A = fe_mul(fe_sub(p.Y, p.X), q.YmX);
+    fe B = fe_mul(fe_add(p.Y, p.X), q.YpX);
+    fe C = fe_mul(p.T, q.T2d);
+    fe D = fe_mul(p.Z, q.Z2);
+    fe E = fe_sub(B, A), F = fe_sub(D, C), G = fe_add(D, C), H = fe_add(B, A);
+    gpt r;
+    r.X = fe_mul(E, F);
+    r.Y = fe_mul(G, H);
+    r.T = fe_mul(E, H);
+    r.Z = fe_mul(F, G);
+    return r;
+}
+
+// Signed radix-16 recoding of a canonical scalar (< 2^253): d[k] in [-8, 8),
+// sum d[k] 16^k = s.
+PHD void sc_signed_radix16(const uint32_t s[8], int8_t d[64]) {
+    int carry = 0;
+    for (int k = 0; k < 64; k++) {
+        int v = (int)((s[k >> 3] >> (4 * (k & 7))) & 15u) + carry;
+        carry = (v + 8) >> 4;
+        d[k] = (int8_t)(v - (carry << 4));
+    }
+}
+
+PHD gcached table_pick(const gcached* tab, int k, int digit) {
+    int a = digit < 0 ? -digit : digit;
+    gcached c = tab[8 * k + a - 1];
+    return digit < 0 ? cached_neg(c) : c;
+}
+
+// acc + s * P via the comb table of P (64 additions, skipping zero digits).
+PHD gpt comb_mul_add(gpt acc, const gcached* tab, const int8_t d[64]) {
+    for (int k = 0; k < 64; k++)
+        if (d[k]) acc = pt_add_cached(acc, table_pick(tab, k, d[k]));
+    return acc;
+}

@@ -44,35 +44,110 @@ PHD void sha256_init(uint32_t st[8]) {
     st[4] = SHA_IV4; st[5] = SHA_IV5; st[6] = SHA_IV6; st[7] = SHA_IV7;
 }
 
+// Pipe balancing (B200): the SM issues one warp-instruction per cycle per
+// sub-partition, but LOP3/SHF/IADD3 all run on the ALU pipe (16 lanes/clk)
+// while the FMA pipe (IMAD) idles. SHA-256 is rotation/XOR heavy, so in
+// MODE >= 1 every addition whose operands are not compile-time constants is
+// emitted as IMAD (a * one + b, `one` = 1 from an opaque kernel parameter)
+// to move it to the FMA pipe; MODE 2 also moves the logical shifts of
+// sigma0/1 to IMAD.HI. MODE 0 is plain C (host tests, cold paths). CM / ZM
+// are bit masks of the message words W0..W15 that are compile-time
+// constants / zero (ZM documents which constants are zero), so constant
+// terms fold and zero terms vanish.
+// Inline PTX so LLVM cannot reassociate chains of a*one+b back into IADD3s.
+PHD uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+    return r;
+#else
+    return a * one + b;
+#endif
+}
+
+template <int MODE>
+PHD uint32_t shr_via(uint32_t w, int n, uint32_t one) {
+#ifdef __CUDA_ARCH__
+    if (MODE >= 2) return __umulhi(w, one << (32 - n));
+#endif
+    return w >> n;
+}
+
+// Constness of all 64 schedule words, evaluated at compile time: W[t] is a
+// constant iff all four words it is derived from are.
+template <uint32_t CM>
+struct WConst {
+    static constexpr uint64_t compute() {
+        uint64_t m = CM;
+        for (int t = 16; t < 64; t++) {
+            bool c = ((m >> (t - 16)) & 1) && ((m >> (t - 15)) & 1) && ((m >> (t - 7)) & 1) && ((m >> (t - 2)) & 1);
+            if (c) m |= 1ull << t;
+        }
+        return m;
+    }
+    static constexpr uint64_t value = compute();
+};
+
 // Rounds [R0, R1) of one compression over the message words W (rolling
 // 16-word schedule, updated in place). The working variables live in st[]
-// (a..h); the caller adds the chaining value at the end (sha256_feed_forward)
-// so a hoisted mid-state can resume at round R0 > 0.
-template <int R0, int R1>
-PHD void sha256_rounds(uint32_t st[8], uint32_t W[16]) {
+// (a..h); the caller adds the chaining value, so a hoisted mid-state can
+// resume at round R0 > 0.
+template <int R0, int R1, uint32_t CM = 0, uint32_t ZM = 0, int MODE = 0>
+PHD void sha256_rounds(uint32_t st[8], uint32_t W[16], uint32_t one = 1) {
+    constexpr uint64_t CMASK = WConst<CM>::value;
     uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
 #pragma unroll
     for (int t = R0; t < R1; t++) {
         uint32_t w;
+        const bool wc = (CMASK >> t) & 1;
         if (t < 16) {
             w = W[t];
         } else {
-            w = W[t & 15] + sha_s0(W[(t - 15) & 15]) + W[(t - 7) & 15] + sha_s1(W[(t - 2) & 15]);
+            const int i16 = t - 16, i15 = t - 15, i7 = t - 7, i2 = t - 2;
+            const uint32_t x16 = W[i16 & 15], x15 = W[i15 & 15], x7 = W[i7 & 15], x2 = W[i2 & 15];
+            if (MODE == 0 || wc) {
+                w = x16 + sha_s0(x15) + x7 + sha_s1(x2);
+            } else {
+                // constant terms first (folded), variable terms chained on IMAD
+                uint32_t acc = 0;
+                const bool c16 = (CMASK >> i16) & 1, c15 = (CMASK >> i15) & 1;
+                const bool c7 = (CMASK >> i7) & 1, c2 = (CMASK >> i2) & 1;
+                if (c16) acc += x16;  // zero words (ZM) are constants and fold away here
+                if (c15) acc += sha_s0(x15);
+                if (c7) acc += x7;
+                if (c2) acc += sha_s1(x2);
+                if (!c2) acc = fadd(rotr32(x2, 17) ^ rotr32(x2, 19) ^ shr_via<MODE>(x2, 10, one), acc, one);
+                if (!c15) acc = fadd(rotr32(x15, 7) ^ rotr32(x15, 18) ^ shr_via<MODE>(x15, 3, one), acc, one);
+                if (!c7) acc = fadd(x7, acc, one);
+                if (!c16) acc = fadd(x16, acc, one);
+                w = acc;
+            }
             W[t & 15] = w;
         }
-        uint32_t t1 = h + sha_S1(e) + sha_ch(e, f, g) + sha_k(t) + w;
-        uint32_t t2 = sha_S0(a) + sha_maj(a, b, c);
-        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+        uint32_t na, ne;
+        if (MODE == 0 || (R0 == 0 && t < 4)) {  // plain (or partially-constant IV start: fold)
+            const uint32_t t1 = h + sha_S1(e) + sha_ch(e, f, g) + sha_k(t) + w;
+            na = t1 + sha_S0(a) + sha_maj(a, b, c);
+            ne = d + t1;
+        } else {
+            const uint32_t kw = wc ? sha_k(t) + w : fadd(w, sha_k(t), one);
+            const uint32_t t1 = fadd(sha_ch(e, f, g), fadd(sha_S1(e), fadd(h, kw, one), one), one);
+            na = fadd(sha_maj(a, b, c), fadd(sha_S0(a), t1, one), one);
+            ne = fadd(d, t1, one);
+        }
+        h = g; g = f; f = e; e = ne;
+        d = c; c = b; b = a; a = na;
     }
     st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
 }
 
 // Full compression of one block into chaining value H.
-PHD void sha256_compress(uint32_t H[8], uint32_t W[16]) {
+template <uint32_t CM = 0, uint32_t ZM = 0, int MODE = 0>
+PHD void sha256_compress(uint32_t H[8], uint32_t W[16], uint32_t one = 1) {
     uint32_t st[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) st[i] = H[i];
-    sha256_rounds<0, 64>(st, W);
+    sha256_rounds<0, 64, CM, ZM, MODE>(st, W, one);
 #pragma unroll
     for (int i = 0; i < 8; i++) H[i] += st[i];
 }
@@ -87,12 +162,15 @@ PHD void ots_pre(const uint32_t x0w[4], uint32_t pre[8]) {
     sha256_rounds<0, 4>(pre, W);
 }
 
-PHD void ots_finish(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j, uint32_t out[4]) {
+template <int MODE = 0>
+PHD void ots_finish(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j, uint32_t out[4],
+                    uint32_t one = 1) {
     uint32_t W[16] = {x0w[0], x0w[1], x0w[2], x0w[3], j, 0x80000000u, 0, 0, 0, 0, 0, 0, 0, 0, 0, 160u};
     uint32_t st[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) st[i] = pre[i];
-    sha256_rounds<4, 64>(st, W);
+    // W5..W15 constant, W6..W14 zero
+    sha256_rounds<4, 64, 0xFFE0u, 0x7FC0u, MODE>(st, W, one);
     out[0] = st[0] + SHA_IV0;
     out[1] = st[1] + SHA_IV1;
     out[2] = st[2] + SHA_IV2;
@@ -115,12 +193,14 @@ PHD void prf_sha256(const uint32_t xw[4], int j, uint32_t out[4]) {
 // H1 = SHA256(0x01 || m || x) (49 B, one block; every word is the byte-shifted
 // funnel of two neighbours). Returns the 512-bit integer H0 || H1 as 16
 // little-endian 32-bit limbs (H0 is the high half, primitives.cpp:166-176).
-PHD void h2s_sha256_len32(const uint32_t m[8], const uint32_t x[4], uint32_t limbs[16]) {
+template <int MODE = 0>
+PHD void h2s_sha256_len32(const uint32_t m[8], const uint32_t x[4], uint32_t limbs[16],
+                          uint32_t one = 1) {
     uint32_t W[16] = {m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7],
                       x[0], x[1], x[2], x[3], 0x80000000u, 0, 0, 384u};
     uint32_t H[8];
     sha256_init(H);
-    sha256_compress(H, W);
+    sha256_compress<0xF000u, 0x6000u, MODE>(H, W, one);  // W12..15 constant, W13/W14 zero
 #pragma unroll
     for (int k = 0; k < 8; k++) limbs[15 - k] = H[k];
     uint32_t V[16];
@@ -136,7 +216,7 @@ PHD void h2s_sha256_len32(const uint32_t m[8], const uint32_t x[4], uint32_t lim
     V[14] = 0;
     V[15] = 392u;
     sha256_init(H);
-    sha256_compress(H, V);
+    sha256_compress<0xE000u, 0x6000u, MODE>(H, V, one);  // W13..15 constant, W13/W14 zero
 #pragma unroll
     for (int k = 0; k < 8; k++) limbs[7 - k] = H[k];
 }
@@ -165,5 +245,166 @@ PHD void sha256_stream(const Src& src, uint64_t n, uint32_t H[8]) {
             W[15] = (uint32_t)(n * 8);
         }
         sha256_compress(H, W);
+    }
+}
+
+// ---- compact form (instruction-cache friendly) ----------------------------
+// The fully unrolled compressions above are ~1.4k SASS instructions each;
+// three of them per entry (x E entries per thread) overflow the SM's
+// instruction caches and ncu shows warps stalled on "no instruction" most
+// of the time. The compact form keeps rounds 0..15 unrolled and runs rounds
+// 16..63 as a 3-trip loop over a 16-round unrolled body (K from constant
+// memory, indexed by the uniform trip counter); the three compressions of an
+// entry share one copy of this code.
+#ifdef __CUDACC__
+__constant__ uint32_t c_sha_k[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u,
+    0xab1c5ed5u, 0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu,
+    0x9bdc06a7u, 0xc19bf174u, 0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu,
+    0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau, 0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u,
+    0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u, 0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu,
+    0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u, 0xa2bfe8a1u, 0xa81a664bu,
+    0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u, 0x19a4c116u,
+    0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u,
+    0xc67178f2u};
+#endif
+
+PHD uint32_t sha_kc(int t) {
+#ifdef __CUDA_ARCH__
+    return c_sha_k[t];
+#else
+    return sha_k(t);
+#endif
+}
+
+#define SHA_RND(a, b, c, d, e, f, g, h, w, k)                                         \
+    do {                                                                              \
+        uint32_t t1_ = (h) + sha_S1(e) + sha_ch((e), (f), (g)) + (k) + (w);            \
+        (d) += t1_;                                                                   \
+        (h) = t1_ + sha_S0(a) + sha_maj((a), (b), (c));                               \
+    } while (0)
+
+// Pipe-balanced round (FMA >= 1): h + w + K stays one IADD3 on the ALU
+// pipe, the remaining additions go to the FMA pipe as IMADs with the opaque
+// `one` (fadd), so the ALU pipe only carries rotations, LOP3s and one add.
+#define SHA_RND_F(a, b, c, d, e, f, g, h, w, k)                                       \
+    do {                                                                              \
+        uint32_t t1_ = fadd(sha_ch((e), (f), (g)), fadd(sha_S1(e), (h) + (w) + (k), one), one); \
+        (d) = fadd((d), t1_, one);                                                    \
+        (h) = fadd(sha_maj((a), (b), (c)), fadd(sha_S0(a), t1_, one), one);           \
+    } while (0)
+
+#define SHA_SCHED(i)                                                                   \
+    W[i] += sha_s0(W[((i) + 1) & 15]) + W[((i) + 9) & 15] + sha_s1(W[((i) + 14) & 15])
+#define SHA_SCHED_F(i)                                                                 \
+    W[i] = fadd(sha_s0(W[((i) + 1) & 15]), fadd(sha_s1(W[((i) + 14) & 15]),            \
+                fadd(W[((i) + 9) & 15], W[i], one), one), one)
+
+// Working state st (a..h) from round r0 (0 or 4; rounds < r0 already applied)
+// through round 63 over message words W (destroyed).
+template <int FMA = 0>
+PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, uint32_t one = 1) {
+#define RND(...) do { if (FMA) SHA_RND_F(__VA_ARGS__); else SHA_RND(__VA_ARGS__); } while (0)
+    uint32_t a, b, c, d, e, f, g, h;
+    if (r0 == 0) {
+        a = st[0]; b = st[1]; c = st[2]; d = st[3]; e = st[4]; f = st[5]; g = st[6]; h = st[7];
+        RND(a, b, c, d, e, f, g, h, W[0], sha_k(0));
+        RND(h, a, b, c, d, e, f, g, W[1], sha_k(1));
+        RND(g, h, a, b, c, d, e, f, W[2], sha_k(2));
+        RND(f, g, h, a, b, c, d, e, W[3], sha_k(3));
+    } else {  // resume after round 3: the names are rotated by four
+        e = st[0]; f = st[1]; g = st[2]; h = st[3]; a = st[4]; b = st[5]; c = st[6]; d = st[7];
+    }
+    RND(e, f, g, h, a, b, c, d, W[4], sha_k(4));
+    RND(d, e, f, g, h, a, b, c, W[5], sha_k(5));
+    RND(c, d, e, f, g, h, a, b, W[6], sha_k(6));
+    RND(b, c, d, e, f, g, h, a, W[7], sha_k(7));
+    RND(a, b, c, d, e, f, g, h, W[8], sha_k(8));
+    RND(h, a, b, c, d, e, f, g, W[9], sha_k(9));
+    RND(g, h, a, b, c, d, e, f, W[10], sha_k(10));
+    RND(f, g, h, a, b, c, d, e, W[11], sha_k(11));
+    RND(e, f, g, h, a, b, c, d, W[12], sha_k(12));
+    RND(d, e, f, g, h, a, b, c, W[13], sha_k(13));
+    RND(c, d, e, f, g, h, a, b, W[14], sha_k(14));
+    RND(b, c, d, e, f, g, h, a, W[15], sha_k(15));
+#pragma unroll 1
+    for (int blk = 16; blk < 64; blk += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (FMA >= 2) SHA_SCHED_F(i); else SHA_SCHED(i);
+        }
+        RND(a, b, c, d, e, f, g, h, W[0], sha_kc(blk + 0));
+        RND(h, a, b, c, d, e, f, g, W[1], sha_kc(blk + 1));
+        RND(g, h, a, b, c, d, e, f, W[2], sha_kc(blk + 2));
+        RND(f, g, h, a, b, c, d, e, W[3], sha_kc(blk + 3));
+        RND(e, f, g, h, a, b, c, d, W[4], sha_kc(blk + 4));
+        RND(d, e, f, g, h, a, b, c, W[5], sha_kc(blk + 5));
+        RND(c, d, e, f, g, h, a, b, W[6], sha_kc(blk + 6));
+        RND(b, c, d, e, f, g, h, a, W[7], sha_kc(blk + 7));
+        RND(a, b, c, d, e, f, g, h, W[8], sha_kc(blk + 8));
+        RND(h, a, b, c, d, e, f, g, W[9], sha_kc(blk + 9));
+        RND(g, h, a, b, c, d, e, f, W[10], sha_kc(blk + 10));
+        RND(f, g, h, a, b, c, d, e, W[11], sha_kc(blk + 11));
+        RND(e, f, g, h, a, b, c, d, W[12], sha_kc(blk + 12));
+        RND(d, e, f, g, h, a, b, c, W[13], sha_kc(blk + 13));
+        RND(c, d, e, f, g, h, a, b, W[14], sha_kc(blk + 14));
+        RND(b, c, d, e, f, g, h, a, W[15], sha_kc(blk + 15));
+    }
+#undef RND
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
+// Suite-1 per-entry digest pair for a 32-byte entry in compact form: one
+// loop over the three compressions (onetime_seed resumed at round 4 from
+// the hoisted mid-state, then H(m||x) and H(0x01||m||x)) sharing one copy of
+// the round code. Output as in h2s_sha256_len32.
+template <int FMA = 0>
+PHD void entry_limbs_s1_l32_compact(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j,
+                                    const uint32_t m[8], uint32_t limbs[16], uint32_t one = 1) {
+    uint32_t x[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int c = 0; c < 3; c++) {
+        uint32_t W[16], st[8];
+        int r0 = 0;
+        if (c == 0) {
+            W[0] = x0w[0]; W[1] = x0w[1]; W[2] = x0w[2]; W[3] = x0w[3];
+            W[4] = j; W[5] = 0x80000000u;
+#pragma unroll
+            for (int k = 6; k < 15; k++) W[k] = 0;
+            W[15] = 160u;
+#pragma unroll
+            for (int k = 0; k < 8; k++) st[k] = pre[k];
+            r0 = 4;
+        } else if (c == 1) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) W[k] = m[k];
+            W[8] = x[0]; W[9] = x[1]; W[10] = x[2]; W[11] = x[3];
+            W[12] = 0x80000000u; W[13] = 0; W[14] = 0; W[15] = 384u;
+            sha256_init(st);
+        } else {
+            W[0] = 0x01000000u | (m[0] >> 8);
+#pragma unroll
+            for (int k = 1; k < 8; k++) W[k] = fshr32(m[k], m[k - 1], 8);
+            W[8] = fshr32(x[0], m[7], 8);
+            W[9] = fshr32(x[1], x[0], 8);
+            W[10] = fshr32(x[2], x[1], 8);
+            W[11] = fshr32(x[3], x[2], 8);
+            W[12] = (x[3] << 24) | 0x00800000u;
+            W[13] = 0; W[14] = 0; W[15] = 392u;
+            sha256_init(st);
+        }
+        sha256_rounds_compact<FMA>(st, W, r0, one);
+        const uint32_t iv[8] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3, SHA_IV4, SHA_IV5, SHA_IV6, SHA_IV7};
+        if (c == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) x[k] = st[k] + iv[k];
+        } else if (c == 1) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) limbs[15 - k] = st[k] + iv[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) limbs[7 - k] = st[k] + iv[k];
+        }
     }
 }

@@ -17,31 +17,84 @@ namespace {
 using namespace tilec;
 
 // ---------------------------------------------------------------- K0
+// sr for one queried epoch q: scan from the top of the stack
+// (seed_manager.cpp:74-84); returns the covering node index or -1.
+__device__ __forceinline__ int ds_cover(const DsParam& ds, uint32_t q) {
+    for (int c = ds.count - 1; c >= 0; c--) {
+        const DsNode& nd = ds.nodes[c];
+        uint64_t lo = (uint64_t)nd.index << nd.depth;
+        uint64_t hi = (uint64_t)(uint32_t)(nd.index + 1u) << nd.depth;
+        if (q >= hi && c == ds.count - 1) return -1;
+        if (q >= lo && q < hi) return c;
+    }
+    return -1;
+}
+
+// Walks `steps` levels down from x along the bits of rel (sc, :5-16).
+template <class T0>
+__device__ __forceinline__ void ds_walk(int suite, const T0& t0, uint32_t x[4], uint32_t rel, int steps) {
+    for (int j = steps - 1; j >= 0; j--) prf_dev(suite, t0, x, (rel >> j) & 1);
+}
+
+// K0: one thread per group of G = 8 queried epochs. When the group is 8
+// consecutive, 8-aligned epochs under one ds node of depth >= 3 (the dense
+// case: every full verification), the thread walks to their common
+// depth-3 ancestor once and expands its 8 leaves in a depth-first order:
+// (D - 3) + 14 PRFs per 8 epochs instead of 8 * D. Otherwise each epoch of
+// the group is walked on its own, exactly as sr does.
+constexpr int kSeedGroup = 8;
+
 __global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict__ epochs,
                               uint32_t n, uint4* __restrict__ x0, unsigned long long* err,
                               const uint32_t* __restrict__ t0g) {
     extern __shared__ uint32_t sT0[];
     if (suite != 1) load_t0(sT0, t0g);
     SmemT0 t0{sT0, threadIdx.x & 31u};
-    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    uint32_t q = epochs[k];
-    // sr: scan from the top of the stack (seed_manager.cpp:74-84)
-    for (int c = ds.count - 1; c >= 0; c--) {
-        const DsNode& nd = ds.nodes[c];
-        uint64_t lo = (uint64_t)nd.index << nd.depth;
-        uint64_t hi = (uint64_t)(uint32_t)(nd.index + 1u) << nd.depth;
-        if (q >= hi && c == ds.count - 1) break;
-        if (q >= lo && q < hi) {
-            uint32_t x[4] = {nd.value[0], nd.value[1], nd.value[2], nd.value[3]};
-            uint32_t rel = q - (uint32_t)lo;
-            for (int j = (int)nd.depth - 1; j >= 0; j--) prf_dev(suite, t0, x, (rel >> j) & 1);
-            x0[k] = make_uint4(x[0], x[1], x[2], x[3]);
-            return;
-        }
+    const uint32_t k0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSeedGroup;
+    if (k0 >= n) return;
+    const uint32_t q0 = epochs[k0];
+    bool dense = (q0 % kSeedGroup) == 0 && k0 + kSeedGroup <= n;
+    int c0 = ds_cover(ds, q0);
+    if (dense && c0 >= 0 && ds.nodes[c0].depth >= 3) {
+#pragma unroll
+        for (int i = 1; i < kSeedGroup; i++) dense = dense && epochs[k0 + i] == q0 + i;
+    } else {
+        dense = false;
     }
-    x0[k] = make_uint4(0, 0, 0, 0);
-    err_min(err, (unsigned long long)k << 1);  // SeedNotDisclosed, before hashing errors
+    if (dense) {
+        const DsNode& nd = ds.nodes[c0];
+        uint32_t x[4] = {nd.value[0], nd.value[1], nd.value[2], nd.value[3]};
+        const uint32_t rel = q0 - (uint32_t)((uint64_t)nd.index << nd.depth);
+        ds_walk(suite, t0, x, rel >> 3, (int)nd.depth - 3);
+        for (int a = 0; a < 2; a++) {
+            uint32_t x1[4] = {x[0], x[1], x[2], x[3]};
+            prf_dev(suite, t0, x1, a);
+            for (int b = 0; b < 2; b++) {
+                uint32_t x2[4] = {x1[0], x1[1], x1[2], x1[3]};
+                prf_dev(suite, t0, x2, b);
+                for (int c = 0; c < 2; c++) {
+                    uint32_t x3[4] = {x2[0], x2[1], x2[2], x2[3]};
+                    prf_dev(suite, t0, x3, c);
+                    x0[k0 + 4 * a + 2 * b + c] = make_uint4(x3[0], x3[1], x3[2], x3[3]);
+                }
+            }
+        }
+        return;
+    }
+    const uint32_t kend = min(n, k0 + kSeedGroup);
+    for (uint32_t k = k0; k < kend; k++) {
+        const uint32_t q = epochs[k];
+        const int c = ds_cover(ds, q);
+        if (c < 0) {
+            x0[k] = make_uint4(0, 0, 0, 0);
+            err_min(err, (unsigned long long)k << 1);  // SeedNotDisclosed, before hashing errors
+            continue;
+        }
+        const DsNode& nd = ds.nodes[c];
+        uint32_t x[4] = {nd.value[0], nd.value[1], nd.value[2], nd.value[3]};
+        ds_walk(suite, t0, x, q - (uint32_t)((uint64_t)nd.index << nd.depth), (int)nd.depth);
+        x0[k] = make_uint4(x[0], x[1], x[2], x[3]);
+    }
 }
 
 // ---------------------------------------------------------------- generic K1+K2
@@ -55,7 +108,7 @@ __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay
     __shared__ uint32_t red[8 * 17];
     if (suite != 1) load_t0(sT0, t0g);
     SmemT0 t0{sT0, threadIdx.x & 31u};
-    const uint32_t tile = blockIdx.x;
+    const uint32_t tile = tm.tile_begin + blockIdx.x;
     uint32_t ep, j0, count;
     uint64_t ebase;
     if (tm.tiles) {
@@ -221,16 +274,17 @@ __global__ void k_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s) {
     if (n_epochs == 0) return;
-    int T = 128;
+    int T = 64;
     size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
     if (smem) cudaFuncSetAttribute(k_seed_derive, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_seed_derive<<<(n_epochs + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, n_epochs, d_x0, d_err, d_t0);
+    uint32_t groups = (n_epochs + kSeedGroup - 1) / kSeedGroup;
+    k_seed_derive<<<(groups + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, n_epochs, d_x0, d_err, d_t0);
 }
 
 void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
                          uint32_t* d_partial, uint32_t* d_entry_e, unsigned long long* d_err,
                          const uint32_t* d_t0, cudaStream_t s) {
-    uint32_t n_tiles = tm.tiles ? tm.n_tiles : tm.n_epochs * tm.tiles_per_epoch;
+    uint32_t n_tiles = tm.tile_count ? tm.tile_count : (tm.tiles ? tm.n_tiles : tm.n_epochs * tm.tiles_per_epoch);
     if (!n_tiles) return;
     size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
     if (smem) cudaFuncSetAttribute(k_hash_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

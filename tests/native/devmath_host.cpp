@@ -75,6 +75,28 @@ void dm_entry_fast32(int suite, const uint8_t m[32], const uint8_t x0[16], uint3
     }
 }
 
+// the pipe-balanced SHA variants (MODE 1/2) with one = 1: exercises the
+// constant/zero word masks of sha256_rounds on the CPU
+void dm_entry_s1_mode(int mode, const uint8_t m[32], const uint8_t x0[16], uint32_t j,
+                      uint32_t limbs_out[16]) {
+    uint32_t x0m[4], mm[8], x0w[4], mw[8], pre[8];
+    words_le(x0, x0m, 4);
+    words_le(m, mm, 8);
+    for (int k = 0; k < 4; k++) x0w[k] = bswap32(x0m[k]);
+    for (int k = 0; k < 8; k++) mw[k] = bswap32(mm[k]);
+    ots_pre(x0w, pre);
+    if (mode >= 3)
+        (mode == 3 ? entry_limbs_s1_l32_compact<0> : mode == 4 ? entry_limbs_s1_l32_compact<1>
+                                                               : entry_limbs_s1_l32_compact<2>)(
+            x0w, pre, j, mw, limbs_out, 1u);
+    else if (mode == 1)
+        entry_limbs_s1_l32<1>(x0w, pre, j, mw, limbs_out, 1u);
+    else if (mode == 2)
+        entry_limbs_s1_l32<2>(x0w, pre, j, mw, limbs_out, 1u);
+    else
+        entry_limbs_s1_l32<0>(x0w, pre, j, mw, limbs_out, 1u);
+}
+
 // sum of n 16-limb values via the 17-limb accumulator, reduced mod l
 void dm_sum_reduce(const uint32_t* limbs16, uint32_t n, uint8_t e_out[32]) {
     uint32_t acc[17];
@@ -113,6 +135,39 @@ int dm_commit_check(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32
     words_le(e, ee, 8);
     words_le(s, ss, 8);
     commit_check_enc(Y, ee, ss, out);
+    return 0;
+}
+
+// the comb-table path of stage 3 v2 (tables built exactly as the device does)
+static void host_table(const gpt& P0, std::vector<gcached>& tab) {
+    gpt P = P0;
+    tab.resize(512);
+    for (int k = 0; k < 64; k++) {
+        gpt q = P;
+        for (int i = 0; i < 8; i++) {
+            tab[8 * k + i] = pt_to_cached(q);
+            q = pt_add(q, P);
+        }
+        P = pt_dbl(pt_dbl(pt_dbl(pt_dbl(P))));
+    }
+}
+
+int dm_commit_check_comb(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32], uint8_t out[32]) {
+    gpt Y;
+    if (!rist_decode(y, Y)) return 1;
+    std::vector<gcached> ty, tb;
+    host_table(Y, ty);
+    host_table(pt_base(), tb);
+    uint32_t ee[8], ss[8];
+    words_le(e, ee, 8);
+    words_le(s, ss, 8);
+    int8_t d[64];
+    gpt acc = pt_identity();
+    sc_signed_radix16(ee, d);
+    acc = comb_mul_add(acc, ty.data(), d);
+    sc_signed_radix16(ss, d);
+    acc = comb_mul_add(acc, tb.data(), d);
+    rist_encode(acc, out);
     return 0;
 }
 

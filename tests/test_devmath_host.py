@@ -73,6 +73,20 @@ def test_entry_fast32_and_deferred_sum(dm, suite):
     assert o.raw == ref  # sum of raw digests reduced once == sum of reductions
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
+def test_sha_pipe_balance_modes(dm, mode):
+    rng = random.Random(20 + mode)
+    for t in range(64):
+        m = bytes(rng.getrandbits(8) for _ in range(32))
+        x0 = bytes(rng.getrandbits(8) for _ in range(16))
+        j = rng.getrandbits(32) if t else 0
+        limbs = (ctypes.c_uint32 * 16)()
+        dm.dm_entry_s1_mode(mode, m, x0, j, limbs)
+        o = out(32)
+        dm.dm_sum_reduce(limbs, 1, o)
+        assert o.raw == O.hash_to_scalar(1, m, O.onetime_seed(1, x0, j))
+
+
 def test_deferred_sum_worst_case(dm):
     # all-ones digests maximise carries through the 17-limb accumulator
     n = 4096
@@ -97,6 +111,10 @@ def test_group_ops(dm, kat):
     for Y, e, s, P in kat["commit_check"]:
         o = out(32)
         assert dm.dm_commit_check(bytes.fromhex(Y), bytes.fromhex(e), bytes.fromhex(s), o) == 0
+        assert o.raw.hex() == P
+    for Y, e, s, P in kat["commit_check"][:16]:
+        o = out(32)
+        assert dm.dm_commit_check_comb(bytes.fromhex(Y), bytes.fromhex(e), bytes.fromhex(s), o) == 0
         assert o.raw.hex() == P
     for p, v in kat["point_valid"]:
         assert dm.dm_point_valid(bytes.fromhex(p)) == v

@@ -241,3 +241,67 @@ def test_device_reports_launches(verifier):
     suite, pk, ds = st.api_objects()
     verifier.paver(pk, st.batches, st.s_hat, None, ds, 1)
     assert verifier.last_launches() >= 4
+
+
+# ------------------------------------------------------------------ K0 dense/sparse seed paths
+@pytest.mark.parametrize("suite", [1, 2])
+def test_seed_derivation_dense_and_sparse_stacks(verifier, suite):
+    """Grouped (8 aligned consecutive epochs under one node) and per-epoch
+    paths of K0 against the oracle's sr, over a multi-node stack."""
+    api = A()
+    rng = random.Random(suite)
+    vals = [bytes(rng.getrandbits(8) for _ in range(16)) for _ in range(4)]
+    # D = 6: nodes cover [0,32) depth 5, [32,48) depth 4, [48,50) depth 1, [50,51) depth 0
+    ds = api.SeedStack(6, [api.SeedNode(5, 0, vals[0]), api.SeedNode(4, 2, vals[1]),
+                           api.SeedNode(1, 24, vals[2]), api.SeedNode(0, 50, vals[3])])
+    w = ds.serialize()
+    for epochs in (list(range(51)), list(range(8, 48)), [0, 2, 3, 9, 16, 17, 18, 19, 20, 21, 22, 23, 49, 50],
+                   list(range(40, 51))):
+        got = verifier.seed_retrieve(suite, ds, epochs)
+        for q, g in zip(epochs, got):
+            st, ref = O.sr(suite, w, 6, q)
+            assert st == 0 and g == ref, (epochs, q)
+    with pytest.raises(api.SeedNotDisclosed) as ei:
+        verifier.seed_retrieve(suite, ds, list(range(40, 56)))
+    assert ei.value.epoch == 51
+
+
+def test_chunked_host_path_matches_device_resident(verifier):
+    """A host-resident log > 128 MiB streams in 64 MiB chunks on a copy
+    stream; results must equal the device-resident call bit for bit."""
+    import ctypes
+
+    import torch
+    from paper_2506_08781_b200 import _native as N
+    api = A()
+    n2, L, n1 = 256, 32, 1 << 14  # 2^22 entries, 128 MiB
+    n = n1 * n2
+    rng = np.random.default_rng(9)
+    host = torch.from_numpy(rng.integers(0, 256, size=n * L, dtype=np.uint8)).pin_memory()
+    dev = host.cuda()
+    root = bytes(range(16))
+    ds = api.SeedStack(14, [api.SeedNode(14, 0, root)])
+    dsb = ds.serialize()
+    dsbuf = ctypes.create_string_buffer(dsb, len(dsb))
+    epochs = np.arange(n1, dtype=np.uint32)
+
+    def run(ptr, resident):
+        b = N.PosloBatch()
+        b.suite, b.n2, b.payload, b.payload_bytes = 1, n2, ptr, n * L
+        b.offsets, b.entry_len, b.n_entries = None, L, n
+        b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, n1
+        b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(dsbuf), len(dsb), 14, resident
+        et = ctypes.create_string_buffer(n1 * 32)
+        eh = ctypes.create_string_buffer(32)
+        err = N.PosloError()
+        assert verifier._lib.poslo_gpu_agg_ekeys(verifier._ctx, ctypes.byref(b), et, eh, ctypes.byref(err)) == 0
+        return et.raw, eh.raw
+
+    et_h, eh_h = run(host.data_ptr(), 0)
+    et_d, eh_d = run(dev.data_ptr(), 1)
+    assert et_h == et_d and eh_h == eh_d
+    # sampled epochs against the oracle
+    for k in (0, 1, 4097, n1 - 1):
+        ents = [bytes(host[(k * n2 + j) * L:(k * n2 + j + 1) * L].numpy()) for j in range(n2)]
+        ref = _oracle_etilde(1, {k: ents}, ds)
+        assert et_h[32 * k:32 * k + 32] == ref[0]
