@@ -49,18 +49,43 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-log2n", type=int, default=21)
+    ap.add_argument("--varlen", action="store_true",
+                    help="syslog-style entries of 64..1024 printable bytes (BASELINE config 4)")
+    ap.add_argument("--mode", default="coarse", choices=["coarse", "epoch"],
+                    help="coarse: one aggregate (config 2); epoch: per-epoch verdicts (config 3)")
     return ap.parse_args()
 
 
+def synth_varlen(seed, first, n):
+    """numpy port of poslo_synth_varlen (include/poslo_synth.h)."""
+    import numpy as np
+    with np.errstate(over="ignore"):
+        k = np.arange(first, first + n, dtype=np.uint64)
+        z = np.uint64((seed ^ 0x6c656e677468) & (2**64 - 1)) + np.uint64(0x9E3779B97F4A7C15) * ((k << np.uint64(8)) + np.uint64(1))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (np.uint64(64) + z % np.uint64(961)).astype(np.uint64)
+
+
 def config_dict(a, n_gpus):
+    if a.varlen:
+        return {"workload": f"BASELINE config 4 (per GPU): 2^{a.log2n} syslog-style entries of 64..1024 printable "
+                            f"bytes, {a.mode} verify (epoch = {a.n2} entries, suite {a.suite}), inputs resident in HBM",
+                "entries_per_gpu": 1 << a.log2n, "entry_len": "U[64,1024] (mean 544)", "n2": a.n2,
+                "suite": a.suite, "mode": a.mode,
+                "parallelism": f"epoch-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
+                "l2": "inputs larger than L2"}
     return {
-        "workload": f"BASELINE config 2: 2^{a.log2n} x {a.entry_len}-byte entries per GPU, coarse single-aggregate "
-                    f"PAVer (suite {a.suite}, n2={a.n2}), inputs resident in HBM",
+        "workload": (f"BASELINE config 2: 2^{a.log2n} x {a.entry_len}-byte entries per GPU, coarse single-aggregate "
+                     f"PAVer (suite {a.suite}, n2={a.n2}), inputs resident in HBM") if a.mode == "coarse" else
+                    (f"BASELINE config 3: 2^{a.log2n} x {a.entry_len}-byte entries per GPU, per-epoch verify "
+                     f"(epoch = {a.n2} entries, {(1 << a.log2n) // a.n2} group checks; suite {a.suite}), inputs resident in HBM"),
         "entries_per_gpu": 1 << a.log2n,
         "entry_len": a.entry_len,
         "n2": a.n2,
         "suite": a.suite,
-        "mode": "coarse",
+        "mode": a.mode,
         "parallelism": f"epoch-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
         "l2": "inputs larger than L2 (2 GiB log per GPU vs 126 MB L2)",
     }
@@ -228,9 +253,17 @@ def main():
     from paper_2506_08781_b200 import api
     from paper_2506_08781_b200 import _native as N
 
+    # one process per GPU; POSLO_DIST_BACKEND=gloo lets the N > 1 path be
+    # exercised with several ranks sharing one device (tests only)
+    backend = os.environ.get("POSLO_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    from paper_2506_08781_b200 import multi_gpu as MG
     v = api.Verifier(local)
     stream = torch.cuda.current_stream()
     v.set_stream(stream.cuda_stream)
@@ -246,20 +279,39 @@ def main():
     ds = api.SeedStack(D, [api.SeedNode(D, 0, root)])  # fully disclosed tree: D PRFs per epoch
 
     # synthetic log of this rank's epochs, generated on the device
-    log = torch.empty(n * L, dtype=torch.uint8, device="cuda")
-    err = N.PosloError()
-    rc = lib.poslo_gpu_synth_log(v._ctx, a.seed, rank * n, n, L, ctypes.c_void_p(log.data_ptr()),
-                                 ctypes.byref(err))
-    assert rc == 0, err.message
     import numpy as np
+    err = N.PosloError()
+    offsets_dev = None
+    if a.varlen:
+        lens = synth_varlen(a.seed, rank * n, n)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        np.cumsum(lens, out=offs[1:])
+        payload_bytes = int(offs[-1])
+        offsets_dev = torch.from_numpy(offs.view(np.int64)).cuda()
+        log = torch.empty(payload_bytes, dtype=torch.uint8, device="cuda")
+        rc = lib.poslo_gpu_synth_varlog(v._ctx, a.seed, rank * n, n, ctypes.c_void_p(offsets_dev.data_ptr()),
+                                        ctypes.c_void_p(log.data_ptr()), ctypes.byref(err))
+        L = 0
+    else:
+        payload_bytes = n * L
+        log = torch.empty(n * L, dtype=torch.uint8, device="cuda")
+        rc = lib.poslo_gpu_synth_log(v._ctx, a.seed, rank * n, n, L, ctypes.c_void_p(log.data_ptr()),
+                                     ctypes.byref(err))
+    assert rc == 0, err.message
     epochs = np.arange(rank * n1_local, (rank + 1) * n1_local, dtype=np.uint32)
     ds_bytes = ds.serialize()
     ds_buf = ctypes.create_string_buffer(ds_bytes, len(ds_bytes))
 
+    host_offs = None
+
     def batch(payload_ptr, device_resident):
         b = N.PosloBatch()
-        b.suite, b.n2, b.payload, b.payload_bytes = a.suite, a.n2, payload_ptr, n * L
-        b.offsets, b.entry_len, b.n_entries = None, L, n
+        b.suite, b.n2, b.payload, b.payload_bytes = a.suite, a.n2, payload_ptr, payload_bytes
+        if offsets_dev is not None:
+            b.offsets = offsets_dev.data_ptr() if device_resident else host_offs.ctypes.data
+        else:
+            b.offsets = None
+        b.entry_len, b.n_entries = L, n
         b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, n1_local
         b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(ds_buf), len(ds_bytes), D, device_resident
         return b
@@ -277,11 +329,7 @@ def main():
     call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), None, e_part)
     parts = [e_part.raw]
     if world > 1:
-        t = torch.frombuffer(bytearray(e_part.raw), dtype=torch.uint8).cuda()
-        g = torch.empty(world * 32, dtype=torch.uint8, device="cuda")
-        dist.all_gather_into_tensor(g, t)
-        gb = g.cpu().numpy().tobytes()
-        parts = [gb[32 * r:32 * r + 32] for r in range(world)]
+        parts = MG.all_gather_bytes(e_part.raw)
     e_hat = sum(int.from_bytes(p, "little") for p in parts) % L_ORDER
     y = rng.randrange(1, L_ORDER)
     r_nonce = rng.randrange(1, L_ORDER)
@@ -296,15 +344,13 @@ def main():
         call(lib.poslo_gpu_paver, ctypes.byref(b), Yb, Sb, Rb, None, ctypes.byref(verdict))
         return verdict.value
 
-    gbuf = torch.empty(world * 32, dtype=torch.uint8, device="cuda")
-
     def step_multi(b):
+        # partial e-hat of this rank's epochs -> all-gather (NCCL/NVLink) ->
+        # rank-ordered device fold mod l -> one group check on rank 0
         call(lib.poslo_gpu_agg_ekeys, ctypes.byref(b), None, e_part)
-        t = torch.frombuffer(bytearray(e_part.raw), dtype=torch.uint8).to("cuda", non_blocking=True)
-        dist.all_gather_into_tensor(gbuf, t)
+        gathered = b"".join(MG.all_gather_bytes(e_part.raw))
         ok = 1
         if rank == 0:
-            gathered = gbuf.cpu().numpy().tobytes()
             eh = ctypes.create_string_buffer(32)
             call(lib.poslo_gpu_scalar_sum, world, gathered, eh)  # rank-ordered device fold mod l
             call(lib.poslo_gpu_group_check, 1, Yb, eh, Sb, Rb, ctypes.byref(verdict))
@@ -312,6 +358,30 @@ def main():
         return ok
 
     step = step_single if world == 1 else step_multi
+
+    if a.mode == "epoch":
+        # per-epoch signatures (s_i, R_i = alpha^{r_i}, s_i = r_i - e~_i y): one
+        # verdict per epoch, no cross-rank exchange except the verdict count
+        et = ctypes.create_string_buffer(n1_local * 32)
+        call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), et, None)
+        r_list = [rng.randrange(1, L_ORDER) for _ in range(n1_local)]
+        et_raw = et.raw
+        s_bytes = b"".join(((r_list[k] - int.from_bytes(et_raw[32 * k:32 * k + 32], "little") * y) % L_ORDER)
+                           .to_bytes(32, "little") for k in range(n1_local))
+        r_enc = b"".join(v.commit_check_batch(bytes(32), [bytes(32)] * n1_local,
+                                              [r.to_bytes(32, "little") for r in r_list]))
+        s_buf = ctypes.create_string_buffer(s_bytes, len(s_bytes))
+        r_buf = ctypes.create_string_buffer(r_enc, len(r_enc))
+        verd = ctypes.create_string_buffer(n1_local)
+
+        def step_epoch(b):
+            call(lib.poslo_gpu_epoch_verify, ctypes.byref(b), Yb, s_buf, r_buf, verd, None)
+            bad = n1_local - sum(verd.raw[:n1_local])
+            if world > 1:
+                bad = sum(int.from_bytes(x, "little") for x in MG.all_gather_bytes(bad.to_bytes(4, "little")))
+            return 1 if bad == 0 else 0
+
+        step = step_epoch
 
     # ---- warm-up + correctness of the fixture
     for _ in range(a.warmup):
@@ -323,7 +393,7 @@ def main():
         saved = log[0].item()
         log[0] = saved ^ 1
         torch.cuda.synchronize()
-        assert step_single(bdev) == 0, "tampered log accepted"
+        assert step(bdev) == 0, "tampered log accepted"
         log[0] = saved
         torch.cuda.synchronize()
 
@@ -346,7 +416,7 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
         dist.barrier()
@@ -355,26 +425,36 @@ def main():
 
     # ---- e2e: same metric through the C-ABI with the log in pinned HOST memory
     v.enable_timing(False)
-    host = torch.empty(n * L, dtype=torch.uint8, pin_memory=True)
-    host.copy_(log)
-    bhost = batch(host.data_ptr(), 0)
-    step(bhost)  # warm the staging buffers
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    ev0.record(stream)
-    for _ in range(a.e2e_steps):
-        step(bhost)
-    ev1.record(stream)
-    ev1.synchronize()
-    e2e_ms = max(ev0.elapsed_time(ev1), (time.perf_counter() - t0) * 1e3) / a.e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
-    e2e_value = world * n / (e2e_ms * 1e-3)
-    del host
+    e2e = None
+    if a.e2e_steps > 0:
+        host = torch.empty(payload_bytes, dtype=torch.uint8, pin_memory=True)
+        host.copy_(log)
+        if offsets_dev is not None:
+            host_offs = offsets_dev.cpu().numpy().view(np.uint64)
+        bhost = batch(host.data_ptr(), 0)
+        step(bhost)  # warm the staging buffers
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(a.e2e_steps):
+            step(bhost)
+        ev1.record(stream)
+        ev1.synchronize()
+        e2e_ms = max(ev0.elapsed_time(ev1), (time.perf_counter() - t0) * 1e3) / a.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda" if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e_value = world * n / (e2e_ms * 1e-3)
+        del host
+        h2d = payload_bytes + (8 * (n + 1) if offsets_dev is not None else 0) + 4 * n1_local + len(ds_bytes) + 8 + (64 * n1_local if a.mode == "epoch" else 32)
+        d2h = (n1_local if a.mode == "epoch" else 1) + 8
+        e2e = {"value": round(e2e_value, 1), "unit": "entries/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
+               "path": f"poslo_gpu_{'paver' if a.mode == 'coarse' else 'epoch_verify'}(device_resident=0) "
+                       f"on a pinned host log, 64 MiB chunked H2D overlapped with hashing"}
 
     if rank != 0:
         dist.destroy_process_group()
@@ -385,12 +465,15 @@ def main():
     # (onetime_seed, H(m||x), H(0x01||m||x)) x 1376 int32 lane-ops each
     # (64 rounds x 14 + 48 schedule words x 10 with 3-input LOP3/IADD3 and
     # funnel-shift rotates; hoisting and constant folding NOT subtracted).
-    mode = int(os.environ.get("POSLO_SHA_MODE", "3"))
-    if a.n2 <= 256:
-        kname = "k_hash_s1_l32cILi128ELi2E" if mode == 3 else f"k_hash_s1_l32ILi128ELi2ELi{mode}E"
-    else:
-        kname = "k_hash_s1_l32cILi256ELi4E" if mode == 3 else f"k_hash_s1_l32ILi256ELi4ELi{mode}E"
-    ops = 3 * 1376 if a.suite == 1 else None
+    mode = int(os.environ.get("POSLO_SHA_MODE", "5"))
+    te = "ILi128ELi1E" if a.n2 <= 128 else ("ILi128ELi2E" if a.n2 <= 256 else "ILi256ELi4E")
+    kname = f"k_hash_s1_l32c{te}Li{mode - 3}E" if mode >= 3 else f"k_hash_s1_l32{te}Li{mode}E"
+    ops = 3 * 1376 if a.suite == 1 and not a.varlen else None
+    if a.suite == 1 and a.varlen:  # ceil((L+25)/64) + ceil((L+26)/64) + 1 compressions per entry
+        lens_np = synth_varlen(a.seed, rank * n, n).astype(np.int64)
+        comps = (lens_np + 25 + 63) // 64 + (lens_np + 26 + 63) // 64 + 1
+        ops = 1376 * float(comps.mean())
+        kname = "k_hash_s1_var"
     peaks = int_peak(local) or {}
     hash_avg_ms = statistics.mean(hash_ms) if hash_ms else None
     peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -401,7 +484,7 @@ def main():
     if ops and hash_avg_ms and peaks.get("alu"):
         achieved = ops * n / (hash_avg_ms * 1e-3) / 1e12
         peak = peaks["alu"] / 1e12
-        hbm_gbs = n * L / (hash_avg_ms * 1e-3) / 1e9
+        hbm_gbs = payload_bytes / (hash_avg_ms * 1e-3) / 1e9
         roof = {"bound": "int32 ALU pipe", "kernel": kname, "achieved": round(achieved, 2), "peak": round(peak, 2),
                 "unit": "Tops/s (int32 lane-ops)", "frac": round(achieved / peak, 4), "traffic": None,
                 "ops_per_entry": ops, "ops_basis": "3 SHA-256 compressions x 1376 lane-ops (algorithmic)",
@@ -418,9 +501,7 @@ def main():
         "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (counter-based log, include/poslo_synth.h)",
         "config": config_dict(a, world),
-        "e2e": {"value": round(e2e_value, 1), "unit": "entries/s", "h2d_bytes_per_step": n * L + 4 * n1_local + len(ds_bytes) + 8,
-                "d2h_bytes_per_step": 1 + 8, "ms_per_step": round(e2e_ms, 3),
-                "path": "poslo_gpu_paver(device_resident=0) on pinned host log"},
+        "e2e": e2e,
         "roofline": roof,
         "gpu_launches": launches,
         "verdict": bool(ok),

@@ -168,6 +168,12 @@ int poslo_gpu_entry_scalars(poslo_gpu_ctx* ctx, const poslo_batch* batch, uint8_
 int poslo_gpu_synth_log(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint64_t n,
                         uint32_t entry_len, void* d_out, poslo_error* err);
 
+/* Variable-length printable synthetic log ("syslog-style", BASELINE config 4):
+ * entry first + t gets bytes poslo_synth_ascii(seed, first + t, b) at
+ * d_out[d_offsets[t] .. d_offsets[t+1]) (lengths from poslo_synth_varlen). */
+int poslo_gpu_synth_varlog(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint64_t n,
+                           const uint64_t* d_offsets, void* d_out, poslo_error* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,7 @@ EXPORTS = [
     "poslo_gpu_paver", "poslo_gpu_epoch_verify", "poslo_gpu_sebver", "poslo_gpu_commit_check",
     "poslo_gpu_group_fold", "poslo_gpu_point_valid", "poslo_gpu_seed_retrieve",
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
+    "poslo_gpu_synth_varlog",
 ]
 
 _lib = None
@@ -85,6 +86,7 @@ def load():
         "poslo_gpu_group_check": ([P, c.c_uint32, P, P, P, P, P, E], c.c_int),
         "poslo_gpu_scalar_sum": ([P, c.c_uint64, P, P, E], c.c_int),
         "poslo_gpu_synth_log": ([P, c.c_uint64, c.c_uint64, c.c_uint64, c.c_uint32, P, E], c.c_int),
+        "poslo_gpu_synth_varlog": ([P, c.c_uint64, c.c_uint64, c.c_uint64, P, P, E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

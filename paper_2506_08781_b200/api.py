@@ -328,7 +328,8 @@ class Verifier:
         tot = ctypes.create_string_buffer(32)
         cb = pb.cstruct()
         self._call(self._lib.poslo_gpu_agg_ekeys, ctypes.byref(cb), out, tot)
-        return [(int(pb.epochs[k]), out.raw[32 * k:32 * k + 32]) for k in range(n)], tot.raw
+        raw = out.raw
+        return [(int(pb.epochs[k]), raw[32 * k:32 * k + 32]) for k in range(n)], tot.raw
 
     def aggregate_ekey(self, suite: SuiteConfig, batches, ds: SeedStack) -> bytes:
         return self.agg_ekeys(suite, batches, ds)[1]
@@ -371,7 +372,8 @@ class Verifier:
         cb = pb.cstruct()
         self._call(self._lib.poslo_gpu_epoch_verify, ctypes.byref(cb), _buf(pk.y), _buf(s), _buf(r),
                    out, et)
-        return [bool(out.raw[k]) for k in range(len(eps))]
+        raw = out.raw
+        return [bool(raw[k]) for k in range(len(eps))]
 
     # -- SeBVer over a coarse CCD (distiller.cpp:181-233)
     def sebver(self, y: bytes, suite: SuiteConfig, all_msgs, ds: SeedStack, epochs_distilled: int,
@@ -396,8 +398,9 @@ class Verifier:
                    _buf(valid[0]) if valid else None, _buf(valid[1]) if valid else None,
                    ctypes.byref(vbit) if valid else None, ui.ctypes.data if len(ui) else None,
                    _buf(us) if us else None, _buf(ur) if ur else None, len(umbrellas), ubits, ibits)
-        res = {"U": [bool(ubits.raw[k]) for k in range(len(umbrellas))],
-               "I": [bool(ibits.raw[k]) for k in range(len(invalid))]}
+        ub, ib = ubits.raw, ibits.raw
+        res = {"U": [bool(ub[k]) for k in range(len(umbrellas))],
+               "I": [bool(ib[k]) for k in range(len(invalid))]}
         if valid:
             res["V"] = [bool(vbit.value)]
         return res
@@ -408,7 +411,8 @@ class Verifier:
         out = ctypes.create_string_buffer(max(n, 1) * 32)
         self._call(self._lib.poslo_gpu_commit_check, n, _buf(y), _buf(b"".join(es)),
                    _buf(b"".join(ss)), out)
-        return [out.raw[32 * k:32 * k + 32] for k in range(n)]
+        raw = out.raw
+        return [raw[32 * k:32 * k + 32] for k in range(n)]
 
     def commit_check(self, y: bytes, e: bytes, s: bytes) -> bytes:
         return self.commit_check_batch(y, [e], [s])[0]
@@ -429,7 +433,8 @@ class Verifier:
         out = ctypes.create_string_buffer(max(n, 1))
         self._call(self._lib.poslo_gpu_group_check, n, _buf(y), _buf(b"".join(es)), _buf(b"".join(ss)),
                    _buf(b"".join(rs)), out)
-        return [bool(out.raw[k]) for k in range(n)]
+        raw = out.raw
+        return [bool(raw[k]) for k in range(n)]
 
     def group_fold(self, pts: Sequence[bytes]) -> bytes:
         out = ctypes.create_string_buffer(32)
@@ -444,7 +449,8 @@ class Verifier:
         n = len(pts)
         out = ctypes.create_string_buffer(max(n, 1))
         self._call(self._lib.poslo_gpu_point_valid, n, _buf(b"".join(pts)) if pts else None, out)
-        return [bool(out.raw[k]) for k in range(n)]
+        raw = out.raw
+        return [bool(raw[k]) for k in range(n)]
 
     # -- stage-level parity hooks
     def seed_retrieve(self, suite: int, ds: SeedStack, epochs: Sequence[int]) -> List[bytes]:
@@ -453,14 +459,16 @@ class Verifier:
         w = ds.serialize()
         self._call(self._lib.poslo_gpu_seed_retrieve, suite, _buf(w), len(w), ds.capacity,
                    ep.ctypes.data if len(ep) else None, len(ep), out)
-        return [out.raw[16 * k:16 * k + 16] for k in range(len(ep))]
+        raw = out.raw
+        return [raw[16 * k:16 * k + 16] for k in range(len(ep))]
 
     def entry_scalars(self, suite: SuiteConfig, batches, ds: SeedStack) -> List[bytes]:
         pb = PackedBatch(suite.suite, suite.n2, batches, ds)
         out = ctypes.create_string_buffer(max(pb.n_entries, 1) * 32)
         cb = pb.cstruct()
         self._call(self._lib.poslo_gpu_entry_scalars, ctypes.byref(cb), out)
-        return [out.raw[32 * k:32 * k + 32] for k in range(pb.n_entries)]
+        raw = out.raw
+        return [raw[32 * k:32 * k + 32] for k in range(pb.n_entries)]
 
 
 _default = None

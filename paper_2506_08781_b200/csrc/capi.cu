@@ -31,23 +31,32 @@ struct DevBuf {
 
 }  // namespace
 
+struct PinnedStage {  // pinned host landing zone for the per-call small D2H copies
+    unsigned long long err_key;
+    int flags[4];
+    uint8_t verdict;
+};
+
 struct poslo_gpu_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;  // H2D of host-resident logs, overlapped with hashing
+    cudaStream_t side = nullptr;  // e-hat-independent part of the group check, overlapped with hashing
+    cudaEvent_t ev_side[2] = {};
     std::vector<cudaEvent_t> chunk_ev;
     std::mutex mtx;
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
     void* d_pk = nullptr;
     uint8_t tabY_key[32] = {};
     bool tabY_valid = false;
+    PinnedStage* stage = nullptr;
     bool timing = false;
     cudaEvent_t ev[7] = {};
     float last_ms[6] = {};
@@ -264,6 +273,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
                 launch_hash_s1_l32(P.lay, t, d_x0, d_partial, P.d_etilde, s);
             else
                 launch_hash_s2_l32(P.lay, t, d_x0, d_partial, P.d_etilde, ctx->d_t0, s);
+        } else if (b->suite == 1) {
+            launch_hash_s1_var(P.lay, t, d_x0, d_partial, s);
         } else {
             launch_hash_generic(b->suite, P.lay, t, d_x0, d_partial, nullptr, d_err, ctx->d_t0, s);
         }
@@ -304,17 +315,20 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     return POSLO_OK;
 }
 
-// Reads the error word (synchronises) and maps it to the reference error.
-int check_hash_errors(poslo_gpu_ctx* ctx, const poslo_batch* b, poslo_error* err) {
-    unsigned long long key;
-    CU(cudaMemcpyAsync(&key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+int map_hash_error(unsigned long long key, const poslo_batch* b, poslo_error* err) {
     if (key == ~0ull) return POSLO_OK;
     uint32_t k = (uint32_t)(key >> 1);
     uint32_t epoch = k < b->n_epochs ? b->epochs[k] : 0;
     if ((key & 1) == 0)
         return set_err(err, POSLO_SEED_NOT_DISCLOSED, epoch, "seed for epoch %u not yet disclosed", epoch);
     return set_err(err, POSLO_FORMAT_ERROR, epoch, "modular-addition hash: entry too long for this suite");
+}
+
+// Reads the error word (synchronises) and maps it to the reference error.
+int check_hash_errors(poslo_gpu_ctx* ctx, const poslo_batch* b, poslo_error* err) {
+    CU(cudaMemcpyAsync(&ctx->stage->err_key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return map_hash_error(ctx->stage->err_key, b, err);
 }
 
 void finish_timing(poslo_gpu_ctx* ctx) {
@@ -448,6 +462,9 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     }
     ctx->stream = ctx->own;
     e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; i++)
+        e = cudaEventCreateWithFlags(&ctx->ev_side[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         poslo_gpu_destroy(ctx);
         return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
@@ -457,6 +474,7 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     e = cudaMalloc(&ctx->d_t0, sizeof t0);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_t0, t0, sizeof t0, cudaMemcpyHostToDevice);
     for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreate(&ctx->ev[i]);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->stage, sizeof(PinnedStage));
     if (e != cudaSuccess) {
         poslo_gpu_destroy(ctx);
         return set_err(err, POSLO_CUDA_ERROR, 0, "init: %s", cudaGetErrorString(e));
@@ -472,16 +490,20 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_scratch, &ctx->b_tiles, &ctx->b_starts, &ctx->b_tbegin, &ctx->b_err,
                       &ctx->b_flags, &ctx->b_payload, &ctx->b_offsets, &ctx->b_e, &ctx->b_s,
                       &ctx->b_r, &ctx->b_enc, &ctx->b_verdict, &ctx->b_mask, &ctx->b_seg, &ctx->b_y,
-                      &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat};
+                      &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
+    if (ctx->stage) cudaFreeHost(ctx->stage);
     for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_pk})
         if (p) cudaFree(p);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->chunk_ev) cudaEventDestroy(ev);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    for (auto& ev : ctx->ev_side)
+        if (ev) cudaEventDestroy(ev);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }
@@ -554,6 +576,7 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     ENSURE(b_rhat, 32, d_rhat);
     int* d_flags;
     ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
     if (r_hat_agg) {
         CU(cudaMemcpyAsync(d_rhat, r_hat_agg, 32, cudaMemcpyHostToDevice, ctx->stream));
     } else {
@@ -561,32 +584,52 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
         void* d_fs;
         UPLOAD(b_pts, r_hats, (size_t)b->n_epochs * 32, d_pts);
         ENSURE(b_foldscratch, 1024 * 128, d_fs);
-        CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
         launch_point_fold(d_pts, b->n_epochs, d_rhat, d_flags + 1, d_fs, ctx->stream);
         ctx->launches += 2;
     }
-    // 3. e-hat = sum of agg_ekeys (:83-85)
-    Prepared P;
-    int rc = run_hash(ctx, b, P, err);
+    // 3. the e-hat-independent half of the check (R decode, R - s*alpha) on
+    // the side stream, overlapped with hashing
+    int rc = ensure_tables(ctx, y, d_flags, err);  // syncs only when Y changed
     if (rc) return rc;
-    mark(ctx, kEvSum);
     uint32_t *d_sum, *d_scr, *d_s;
+    void* d_pre;
+    uint8_t* d_verdict;
+    UPLOAD(b_s, s_hat, 32, d_s);
+    ENSURE(b_pre, 256, d_pre);
+    ENSURE(b_verdict, 1, d_verdict);
+    CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
+    launch_check_pre(ctx->d_tabB, d_s, d_rhat, d_pre, ctx->side);
+    ctx->launches += 1;
+    CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
+    // 4. e-hat = sum of agg_ekeys (:83-85)
+    Prepared P;
+    rc = run_hash(ctx, b, P, err);
+    if (rc) {
+        cudaStreamSynchronize(ctx->side);
+        return rc;
+    }
+    mark(ctx, kEvSum);
     ENSURE(b_sum, 8, d_sum);
     ENSURE(b_scratch, 17 * 1024, d_scr);
     launch_sum_mod_l(P.d_etilde, 8, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
     ctx->launches += 2;
-    UPLOAD(b_s, s_hat, 32, d_s);
     mark(ctx, kEvGroup);
-    rc = check_hash_errors(ctx, b, err);
+    // 5. one commitment check (:86): e-hat * Y == R - s*alpha, then ONE
+    // synchronisation for the error word, the fold's counter and the verdict
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
+    launch_check_post(ctx->d_tabY, d_sum, d_pre, d_verdict, ctx->stream);
+    ctx->launches += 1;
+    CU(cudaGetLastError());
+    PinnedStage* hs = ctx->stage;
+    CU(cudaMemcpyAsync(&hs->err_key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(hs->flags, d_flags, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&hs->verdict, d_verdict, 1, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    rc = map_hash_error(hs->err_key, b, err);
     if (rc) return rc;
-    if (!r_hat_agg) {
-        int bad = 0;
-        CU(cudaMemcpy(&bad, d_flags + 1, 4, cudaMemcpyDeviceToHost));
-        if (bad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
-    }
-    // 4. one commitment check (:86)
-    rc = group_check_dev(ctx, y, 1, d_sum, d_s, d_rhat, verdict, nullptr, err);
-    if (rc) return rc;
+    if (!r_hat_agg && hs->flags[1]) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    *verdict = hs->verdict;
     finish_timing(ctx);
     return ok(err);
 }
@@ -860,6 +903,18 @@ int poslo_gpu_synth_log(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint6
     if (n && !d_out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
     Guard g(ctx);
     launch_synth_fixed(seed, first, n, entry_len, static_cast<uint8_t*>(d_out), ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
+int poslo_gpu_synth_varlog(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint64_t n,
+                           const uint64_t* d_offsets, void* d_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (n && (!d_out || !d_offsets)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    launch_synth_var(seed, first, n, d_offsets, static_cast<uint8_t*>(d_out), ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));

@@ -217,6 +217,76 @@ __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict_
     }
 }
 
+// ---- split single check: commit_check(Y, e, s) == R <=> e*Y == R - s*B ----
+// The pre part (R decode + s*B) does not depend on e-hat, so paver runs it on
+// a side stream concurrently with hashing; after hashing only e*Y (64 table
+// lookups + a 6-level tree) and a 4-multiplication equality remain.
+struct CheckPre {
+    gpt T;   // R - s*B
+    int ok;  // R decoded
+};
+
+__device__ __forceinline__ void named_sync64() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+// 64 threads each take one signed radix-16 window of the scalar from the
+// table, then a 6-level shared-memory tree (named barrier over warps 0-1).
+__device__ __forceinline__ gpt comb_tree64(const gcached* tab, const uint32_t* scal, int8_t* dig, gpt* sh) {
+    const int t = threadIdx.x;
+    if (t == 0) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = scal[k];
+        int8_t d[64];
+        sc_signed_radix16(v, d);
+        for (int k = 0; k < 64; k++) dig[k] = d[k];
+    }
+    named_sync64();
+    gpt acc = pt_identity();
+    if (dig[t]) acc = pt_add_cached(acc, table_pick(tab, t, dig[t]));
+    sh[t] = acc;
+    named_sync64();
+    for (int w = 32; w >= 1; w >>= 1) {
+        if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
+        named_sync64();
+    }
+    return sh[0];
+}
+
+__global__ void __launch_bounds__(96) k_check_pre(const gcached* __restrict__ tabB,
+                                                  const uint32_t* __restrict__ s,
+                                                  const uint8_t* __restrict__ r_enc,
+                                                  CheckPre* __restrict__ out) {
+    __shared__ int8_t dig[64];
+    __shared__ gpt sh[64];
+    __shared__ gpt R;
+    __shared__ int rok;
+    if (threadIdx.x < 64) {
+        gpt S = comb_tree64(tabB, s, dig, sh);
+        (void)S;
+    } else if (threadIdx.x == 64) {  // warp 2 decodes R concurrently
+        uint8_t b[32];
+        load32(r_enc, b);
+        gpt P;
+        rok = rist_decode(b, P) ? 1 : 0;
+        R = P;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out->ok = rok;
+        out->T = rok ? pt_add(R, pt_neg(sh[0])) : pt_identity();
+    }
+}
+
+__global__ void __launch_bounds__(64) k_check_post(const gcached* __restrict__ tabY,
+                                                   const uint32_t* __restrict__ e,
+                                                   const CheckPre* __restrict__ pre,
+                                                   uint8_t* __restrict__ verdict) {
+    __shared__ int8_t dig[64];
+    __shared__ gpt sh[64];
+    gpt E = comb_tree64(tabY, e, dig, sh);
+    if (threadIdx.x == 0) verdict[0] = (pre->ok && rist_equal(E, pre->T)) ? 1 : 0;
+}
+
 }  // namespace
 
 void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
@@ -256,6 +326,17 @@ void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n,
         k_check_cta<<<n, 128, 0, s>>>(ty, tb, d_e, d_s, d_r, d_enc, d_verdict);
     else
         k_check_thread<<<(n + 127) / 128, 128, 0, s>>>(ty, tb, n, d_e, d_s, d_r, d_enc, d_verdict);
+}
+
+void launch_check_pre(const void* d_tabB, const uint32_t* d_s, const uint8_t* d_r, void* d_pre,
+                      cudaStream_t s) {
+    k_check_pre<<<1, 96, 0, s>>>(static_cast<const gcached*>(d_tabB), d_s, d_r, static_cast<CheckPre*>(d_pre));
+}
+
+void launch_check_post(const void* d_tabY, const uint32_t* d_e, const void* d_pre, uint8_t* d_verdict,
+                       cudaStream_t s) {
+    k_check_post<<<1, 64, 0, s>>>(static_cast<const gcached*>(d_tabY), d_e, static_cast<const CheckPre*>(d_pre),
+                                  d_verdict);
 }
 
 }  // namespace poslo_gpu

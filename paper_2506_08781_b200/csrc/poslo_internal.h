@@ -60,6 +60,12 @@ void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, c
                          uint32_t* d_partial, uint32_t* d_entry_e, unsigned long long* d_err,
                          const uint32_t* d_t0, cudaStream_t s);
 
+// Suite 1 over variable-length (or any non-32-byte) entries: streamed SHA-256
+// straight from the payload, tiles length-sorted in shared memory. Writes
+// per-tile partials (tile_entries must be <= 1024).
+void launch_hash_s1_var(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0, uint32_t* d_partial,
+                        cudaStream_t s);
+
 // Per-epoch e~ from tile partials (skipped when tiles_per_epoch == 1 on the
 // fast paths, which finalise in the hashing kernel).
 void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,
@@ -82,9 +88,9 @@ void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, con
                         const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, int* d_ybad,
                         cudaStream_t s);
 
-// Fixed-base comb table (512 cached points, 64 KiB) of the point encoded at
+// Fixed-base comb table (512 affine Niels points, 48 KiB) of the point encoded at
 // d_enc, or of the generator when d_enc == nullptr. d_pk_scratch >= 64 * 128 B.
-constexpr size_t kCombTableBytes = 512 * 128;
+constexpr size_t kCombTableBytes = 512 * 96;
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s);
 // commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,
@@ -92,6 +98,13 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
 void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n, const uint32_t* d_e,
                              const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
                              cudaStream_t s);
+
+// Split single check for paver: pre (R decode, T = R - s*alpha; independent
+// of e-hat, overlappable with hashing) and post (e*Y == T). d_pre >= 256 B.
+void launch_check_pre(const void* d_tabB, const uint32_t* d_s, const uint8_t* d_r, void* d_pre,
+                      cudaStream_t s);
+void launch_check_post(const void* d_tabY, const uint32_t* d_e, const void* d_pre, uint8_t* d_verdict,
+                       cudaStream_t s);
 
 // Fold of n encoded points with the group law (group_combine); d_bad counts
 // invalid encodings. d_scratch >= 1024 * 128 bytes.
@@ -104,5 +117,9 @@ void launch_point_validate(const uint8_t* d_pts, uint32_t n, uint8_t* d_ok, cuda
 // Synthetic fixed-length log entries [first, first+n) (include/poslo_synth.h).
 void launch_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L, uint8_t* d_out,
                         cudaStream_t s);
+
+// Synthetic variable-length printable entries at device offsets (n + 1).
+void launch_synth_var(uint64_t seed, uint64_t first, uint64_t n, const uint64_t* d_offsets, uint8_t* d_out,
+                      cudaStream_t s);
 
 }  // namespace poslo_gpu

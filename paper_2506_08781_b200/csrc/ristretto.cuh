@@ -96,21 +96,51 @@ PHD fe fe_sub(const fe& a, const fe& b) {
     return r;
 }
 
+#ifdef __CUDA_ARCH__
+// 8x8-limb product with carry-flag chains (two per row: low and high
+// halves), then the 2^256 == 38 fold: ~170 instructions, about half of the
+// portable C version. Identical results (tests/native + GPU parity tests).
+__device__ __forceinline__ fe fe_mul_ptx(const fe& a, const fe& b) {
+    fe r;
+    asm("{\n\t.reg .u32 r<16>;\n\tmov.u32 r0, 0;\n\tmov.u32 r1, 0;\n\tmov.u32 r2, 0;\n\tmov.u32 r3, 0;\n\tmov.u32 r4, 0;\n\tmov.u32 r5, 0;\n\tmov.u32 r6, 0;\n\tmov.u32 r7, 0;\n\tmov.u32 r8, 0;\n\tmov.u32 r9, 0;\n\tmov.u32 r10, 0;\n\tmov.u32 r11, 0;\n\tmov.u32 r12, 0;\n\tmov.u32 r13, 0;\n\tmov.u32 r14, 0;\n\tmov.u32 r15, 0;\n\tmad.lo.cc.u32 r0, %8, %16, r0;\n\tmadc.lo.cc.u32 r1, %9, %16, r1;\n\tmadc.lo.cc.u32 r2, %10, %16, r2;\n\tmadc.lo.cc.u32 r3, %11, %16, r3;\n\tmadc.lo.cc.u32 r4, %12, %16, r4;\n\tmadc.lo.cc.u32 r5, %13, %16, r5;\n\tmadc.lo.cc.u32 r6, %14, %16, r6;\n\tmadc.lo.cc.u32 r7, %15, %16, r7;\n\taddc.u32 r8, 0, 0;\n\tmad.hi.cc.u32 r1, %8, %16, r1;\n\tmadc.hi.cc.u32 r2, %9, %16, r2;\n\tmadc.hi.cc.u32 r3, %10, %16, r3;\n\tmadc.hi.cc.u32 r4, %11, %16, r4;\n\tmadc.hi.cc.u32 r5, %12, %16, r5;\n\tmadc.hi.cc.u32 r6, %13, %16, r6;\n\tmadc.hi.cc.u32 r7, %14, %16, r7;\n\tmadc.hi.u32 r8, %15, %16, r8;\n\tmad.lo.cc.u32 r1, %8, %17, r1;\n\tmadc.lo.cc.u32 r2, %9, %17, r2;\n\tmadc.lo.cc.u32 r3, %10, %17, r3;\n\tmadc.lo.cc.u32 r4, %11, %17, r4;\n\tmadc.lo.cc.u32 r5, %12, %17, r5;\n\tmadc.lo.cc.u32 r6, %13, %17, r6;\n\tmadc.lo.cc.u32 r7, %14, %17, r7;\n\tmadc.lo.cc.u32 r8, %15, %17, r8;\n\taddc.u32 r9, 0, 0;\n\tmad.hi.cc.u32 r2, %8, %17, r2;\n\tmadc.hi.cc.u32 r3, %9, %17, r3;\n\tmadc.hi.cc.u32 r4, %10, %17, r4;\n\tmadc.hi.cc.u32 r5, %11, %17, r5;\n\tmadc.hi.cc.u32 r6, %12, %17, r6;\n\tmadc.hi.cc.u32 r7, %13, %17, r7;\n\tmadc.hi.cc.u32 r8, %14, %17, r8;\n\tmadc.hi.u32 r9, %15, %17, r9;\n\tmad.lo.cc.u32 r2, %8, %18, r2;\n\tmadc.lo.cc.u32 r3, %9, %18, r3;\n\tmadc.lo.cc.u32 r4, %10, %18, r4;\n\tmadc.lo.cc.u32 r5, %11, %18, r5;\n\tmadc.lo.cc.u32 r6, %12, %18, r6;\n\tmadc.lo.cc.u32 r7, %13, %18, r7;\n\tmadc.lo.cc.u32 r8, %14, %18, r8;\n\tmadc.lo.cc.u32 r9, %15, %18, r9;\n\taddc.u32 r10, 0, 0;\n\tmad.hi.cc.u32 r3, %8, %18, r3;\n\tmadc.hi.cc.u32 r4, %9, %18, r4;\n\tmadc.hi.cc.u32 r5, %10, %18, r5;\n\tmadc.hi.cc.u32 r6, %11, %18, r6;\n\tmadc.hi.cc.u32 r7, %12, %18, r7;\n\tmadc.hi.cc.u32 r8, %13, %18, r8;\n\tmadc.hi.cc.u32 r9, %14, %18, r9;\n\tmadc.hi.u32 r10, %15, %18, r10;\n\tmad.lo.cc.u32 r3, %8, %19, r3;\n\tmadc.lo.cc.u32 r4, %9, %19, r4;\n\tmadc.lo.cc.u32 r5, %10, %19, r5;\n\tmadc.lo.cc.u32 r6, %11, %19, r6;\n\tmadc.lo.cc.u32 r7, %12, %19, r7;\n\tmadc.lo.cc.u32 r8, %13, %19, r8;\n\tmadc.lo.cc.u32 r9, %14, %19, r9;\n\tmadc.lo.cc.u32 r10, %15, %19, r10;\n\taddc.u32 r11, 0, 0;\n\tmad.hi.cc.u32 r4, %8, %19, r4;\n\tmadc.hi.cc.u32 r5, %9, %19, r5;\n\tmadc.hi.cc.u32 r6, %10, %19, r6;\n\tmadc.hi.cc.u32 r7, %11, %19, r7;\n\tmadc.hi.cc.u32 r8, %12, %19, r8;\n\tmadc.hi.cc.u32 r9, %13, %19, r9;\n\tmadc.hi.cc.u32 r10, %14, %19, r10;\n\tmadc.hi.u32 r11, %15, %19, r11;\n\tmad.lo.cc.u32 r4, %8, %20, r4;\n\tmadc.lo.cc.u32 r5, %9, %20, r5;\n\tmadc.lo.cc.u32 r6, %10, %20, r6;\n\tmadc.lo.cc.u32 r7, %11, %20, r7;\n\tmadc.lo.cc.u32 r8, %12, %20, r8;\n\tmadc.lo.cc.u32 r9, %13, %20, r9;\n\tmadc.lo.cc.u32 r10, %14, %20, r10;\n\tmadc.lo.cc.u32 r11, %15, %20, r11;\n\taddc.u32 r12, 0, 0;\n\tmad.hi.cc.u32 r5, %8, %20, r5;\n\tmadc.hi.cc.u32 r6, %9, %20, r6;\n\tmadc.hi.cc.u32 r7, %10, %20, r7;\n\tmadc.hi.cc.u32 r8, %11, %20, r8;\n\tmadc.hi.cc.u32 r9, %12, %20, r9;\n\tmadc.hi.cc.u32 r10, %13, %20, r10;\n\tmadc.hi.cc.u32 r11, %14, %20, r11;\n\tmadc.hi.u32 r12, %15, %20, r12;\n\tmad.lo.cc.u32 r5, %8, %21, r5;\n\tmadc.lo.cc.u32 r6, %9, %21, r6;\n\tmadc.lo.cc.u32 r7, %10, %21, r7;\n\tmadc.lo.cc.u32 r8, %11, %21, r8;\n\tmadc.lo.cc.u32 r9, %12, %21, r9;\n\tmadc.lo.cc.u32 r10, %13, %21, r10;\n\tmadc.lo.cc.u32 r11, %14, %21, r11;\n\tmadc.lo.cc.u32 r12, %15, %21, r12;\n\taddc.u32 r13, 0, 0;\n\tmad.hi.cc.u32 r6, %8, %21, r6;\n\tmadc.hi.cc.u32 r7, %9, %21, r7;\n\tmadc.hi.cc.u32 r8, %10, %21, r8;\n\tmadc.hi.cc.u32 r9, %11, %21, r9;\n\tmadc.hi.cc.u32 r10, %12, %21, r10;\n\tmadc.hi.cc.u32 r11, %13, %21, r11;\n\tmadc.hi.cc.u32 r12, %14, %21, r12;\n\tmadc.hi.u32 r13, %15, %21, r13;\n\tmad.lo.cc.u32 r6, %8, %22, r6;\n\tmadc.lo.cc.u32 r7, %9, %22, r7;\n\tmadc.lo.cc.u32 r8, %10, %22, r8;\n\tmadc.lo.cc.u32 r9, %11, %22, r9;\n\tmadc.lo.cc.u32 r10, %12, %22, r10;\n\tmadc.lo.cc.u32 r11, %13, %22, r11;\n\tmadc.lo.cc.u32 r12, %14, %22, r12;\n\tmadc.lo.cc.u32 r13, %15, %22, r13;\n\taddc.u32 r14, 0, 0;\n\tmad.hi.cc.u32 r7, %8, %22, r7;\n\tmadc.hi.cc.u32 r8, %9, %22, r8;\n\tmadc.hi.cc.u32 r9, %10, %22, r9;\n\tmadc.hi.cc.u32 r10, %11, %22, r10;\n\tmadc.hi.cc.u32 r11, %12, %22, r11;\n\tmadc.hi.cc.u32 r12, %13, %22, r12;\n\tmadc.hi.cc.u32 r13, %14, %22, r13;\n\tmadc.hi.u32 r14, %15, %22, r14;\n\tmad.lo.cc.u32 r7, %8, %23, r7;\n\tmadc.lo.cc.u32 r8, %9, %23, r8;\n\tmadc.lo.cc.u32 r9, %10, %23, r9;\n\tmadc.lo.cc.u32 r10, %11, %23, r10;\n\tmadc.lo.cc.u32 r11, %12, %23, r11;\n\tmadc.lo.cc.u32 r12, %13, %23, r12;\n\tmadc.lo.cc.u32 r13, %14, %23, r13;\n\tmadc.lo.cc.u32 r14, %15, %23, r14;\n\taddc.u32 r15, 0, 0;\n\tmad.hi.cc.u32 r8, %8, %23, r8;\n\tmadc.hi.cc.u32 r9, %9, %23, r9;\n\tmadc.hi.cc.u32 r10, %10, %23, r10;\n\tmadc.hi.cc.u32 r11, %11, %23, r11;\n\tmadc.hi.cc.u32 r12, %12, %23, r12;\n\tmadc.hi.cc.u32 r13, %13, %23, r13;\n\tmadc.hi.cc.u32 r14, %14, %23, r14;\n\tmadc.hi.u32 r15, %15, %23, r15;\n\t.reg .u32 t8, c38;\n\tmov.u32 c38, 38;\n\tmad.lo.cc.u32 r0, r8, c38, r0;\n\tmadc.lo.cc.u32 r1, r9, c38, r1;\n\tmadc.lo.cc.u32 r2, r10, c38, r2;\n\tmadc.lo.cc.u32 r3, r11, c38, r3;\n\tmadc.lo.cc.u32 r4, r12, c38, r4;\n\tmadc.lo.cc.u32 r5, r13, c38, r5;\n\tmadc.lo.cc.u32 r6, r14, c38, r6;\n\tmadc.lo.cc.u32 r7, r15, c38, r7;\n\taddc.u32 t8, 0, 0;\n\tmad.hi.cc.u32 r1, r8, c38, r1;\n\tmadc.hi.cc.u32 r2, r9, c38, r2;\n\tmadc.hi.cc.u32 r3, r10, c38, r3;\n\tmadc.hi.cc.u32 r4, r11, c38, r4;\n\tmadc.hi.cc.u32 r5, r12, c38, r5;\n\tmadc.hi.cc.u32 r6, r13, c38, r6;\n\tmadc.hi.cc.u32 r7, r14, c38, r7;\n\tmadc.hi.u32 t8, r15, c38, t8;\n\tmul.lo.u32 t8, t8, c38;\n\tadd.cc.u32 r0, r0, t8;\n\taddc.cc.u32 r1, r1, 0;\n\taddc.cc.u32 r2, r2, 0;\n\taddc.cc.u32 r3, r3, 0;\n\taddc.cc.u32 r4, r4, 0;\n\taddc.cc.u32 r5, r5, 0;\n\taddc.cc.u32 r6, r6, 0;\n\taddc.cc.u32 r7, r7, 0;\n\taddc.u32 t8, 0, 0;\n\tmul.lo.u32 t8, t8, c38;\n\tadd.cc.u32 r0, r0, t8;\n\taddc.cc.u32 r1, r1, 0;\n\taddc.cc.u32 r2, r2, 0;\n\taddc.cc.u32 r3, r3, 0;\n\taddc.cc.u32 r4, r4, 0;\n\taddc.cc.u32 r5, r5, 0;\n\taddc.cc.u32 r6, r6, 0;\n\taddc.cc.u32 r7, r7, 0;\n\taddc.u32 t8, 0, 0;\n\tmov.u32 %0, r0;\n\tmov.u32 %1, r1;\n\tmov.u32 %2, r2;\n\tmov.u32 %3, r3;\n\tmov.u32 %4, r4;\n\tmov.u32 %5, r5;\n\tmov.u32 %6, r6;\n\tmov.u32 %7, r7;\n\t}"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+          "=r"(r.v[6]), "=r"(r.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]),
+          "r"(a.v[7]), "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]),
+          "r"(b.v[6]), "r"(b.v[7]));
+    return r;
+}
+#endif
+
+// Product scanning: the 64 32x32 products are independent and every column
+// is summed on its own (96-bit column accumulators), so only the final carry
+// sweep is serial — short dependency chains for the latency-bound single-
+// check path, where the old row-by-row carry chain dominated.
 PHD fe fe_mul(const fe& a, const fe& b) {
+#ifdef __CUDA_ARCH__
+    return fe_mul_ptx(a, b);
+#endif
     uint32_t t[16];
+    uint64_t carry = 0;  // < 2^36
 #pragma unroll
-    for (int i = 0; i < 16; i++) t[i] = 0;
+    for (int k = 0; k < 15; k++) {
+        uint64_t lo = 0;
+        uint32_t hi = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        uint64_t carry = 0;
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            uint64_t p = (uint64_t)a.v[i] * b.v[j] + t[i + j] + carry;
-            t[i + j] = (uint32_t)p;
-            carry = p >> 32;
+        for (int i = 0; i < 8; i++) {
+            const int j = k - i;
+            if (j < 0 || j > 7) continue;
+            const uint64_t p = (uint64_t)a.v[i] * b.v[j];
+            lo += p;
+            hi += lo < p;
         }
-        t[i + 8] = (uint32_t)carry;
+        lo += carry;
+        hi += lo < carry;
+        t[k] = (uint32_t)lo;
+        carry = (lo >> 32) | ((uint64_t)hi << 32);
     }
+    t[15] = (uint32_t)carry;
+    // 2^256 == 38 (mod p): r = t_lo + 38 * t_hi, folded twice
     fe r;
     uint64_t c = 0;
 #pragma unroll
@@ -365,23 +395,40 @@ PHD void commit_check_enc(const gpt& Y, const uint32_t e[8], const uint32_t s[8]
 }
 
 // ---- fixed-base comb tables (stage 3 v2) ---------------------------------
-// For a base P: tab[8k + i] = (i+1) * 16^k * P, k = 0..63, i = 0..7, in the
-// "cached" form (Y+X, Y-X, 2Z, 2dT) so one table addition costs 8 muls. With
-// signed radix-16 digits s = sum d_k 16^k, d_k in [-8, 8), a scalar
-// multiplication is 64 table additions and NO doublings. Y is fixed per
-// public key and alpha is fixed forever, so both exponentiations of
-// commit_check become fixed-base.
+// For a base P: tab[8k + i] = (i+1) * 16^k * P, k = 0..63, i = 0..7, in
+// affine Niels form (y+x, y-x, 2dxy) with Z = 1, so one table addition (a
+// mixed addition) costs 7 multiplications. With signed radix-16 digits
+// s = sum d_k 16^k, d_k in [-8, 8), a scalar multiplication is 64 table
+// additions and NO doublings. Y is fixed per public key and alpha forever,
+// so both exponentiations of commit_check are fixed-base (SURVEY.md §7.5).
 struct gcached {
-    fe YpX, YmX, Z2, T2d;
+    fe YpX, YmX, T2d;
 };
+
+// z^(p-2) = z^(2^255 - 21)
+PHD fe fe_invert(const fe& z) {
+    fe z2 = fe_sq(z);
+    fe z9 = fe_mul(fe_sqn(z2, 2), z);            // z^9
+    fe z11 = fe_mul(z9, z2);                     // z^11
+    fe z5 = fe_mul(fe_sq(z11), z9);              // 2^5 - 1
+    fe z10 = fe_mul(fe_sqn(z5, 5), z5);          // 2^10 - 1
+    fe z20 = fe_mul(fe_sqn(z10, 10), z10);       // 2^20 - 1
+    fe z40 = fe_mul(fe_sqn(z20, 20), z20);       // 2^40 - 1
+    fe z50 = fe_mul(fe_sqn(z40, 10), z10);       // 2^50 - 1
+    fe z100 = fe_mul(fe_sqn(z50, 50), z50);      // 2^100 - 1
+    fe z200 = fe_mul(fe_sqn(z100, 100), z100);   // 2^200 - 1
+    fe z250 = fe_mul(fe_sqn(z200, 50), z50);     // 2^250 - 1
+    return fe_mul(fe_sqn(z250, 5), z11);         // 2^255 - 21
+}
 
 PHD gcached pt_to_cached(const gpt& p) {
     const fe d2 = FE_CONST(FE_D2_LIMBS);
+    fe zi = fe_invert(p.Z);
+    fe x = fe_mul(p.X, zi), y = fe_mul(p.Y, zi);
     gcached c;
-    c.YpX = fe_add(p.Y, p.X);
-    c.YmX = fe_sub(p.Y, p.X);
-    c.Z2 = fe_add(p.Z, p.Z);
-    c.T2d = fe_mul(p.T, d2);
+    c.YpX = fe_add(y, x);
+    c.YmX = fe_sub(y, x);
+    c.T2d = fe_mul(fe_mul(x, y), d2);
     return c;
 }
 
@@ -389,16 +436,16 @@ PHD gcached cached_neg(const gcached& c) {
     gcached r;
     r.YpX = c.YmX;
     r.YmX = c.YpX;
-    r.Z2 = c.Z2;
     r.T2d = fe_neg(c.T2d);
     return r;
 }
 
+// mixed addition p + q (q affine Niels): add-2008-hwcd-3 with Z2 = 1
 PHD gpt pt_add_cached(const gpt& p, const gcached& q) {
     fe A = fe_mul(fe_sub(p.Y, p.X), q.YmX);
     fe B = fe_mul(fe_add(p.Y, p.X), q.YpX);
     fe C = fe_mul(p.T, q.T2d);
-    fe D = fe_mul(p.Z, q.Z2);
+    fe D = fe_add(p.Z, p.Z);
     fe E = fe_sub(B, A), F = fe_sub(D, C), G = fe_add(D, C), H = fe_add(B, A);
     gpt r;
     r.X = fe_mul(E, F);
@@ -430,4 +477,11 @@ PHD gpt comb_mul_add(gpt acc, const gcached* tab, const int8_t d[64]) {
     for (int k = 0; k < 64; k++)
         if (d[k]) acc = pt_add_cached(acc, table_pick(tab, k, d[k]));
     return acc;
+}
+
+// Ristretto equality of classes (RFC 9496 §4.3.3): X1*Y2 == Y1*X2 or
+// Y1*Y2 == X1*X2. Equal classes <=> equal canonical encodings, so comparing
+// against a decoded R replaces encoding P (the reference's byte compare).
+PHD bool rist_equal(const gpt& p, const gpt& q) {
+    return fe_eq(fe_mul(p.X, q.Y), fe_mul(p.Y, q.X)) || fe_eq(fe_mul(p.Y, q.Y), fe_mul(p.X, q.X));
 }

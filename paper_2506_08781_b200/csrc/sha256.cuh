@@ -295,6 +295,17 @@ PHD uint32_t sha_kc(int t) {
         (h) = fadd(sha_maj((a), (b), (c)), fadd(sha_S0(a), t1_, one), one);           \
     } while (0)
 
+// FMA >= 3: also h + (K + w) on the FMA pipe (K as the IMAD multiplicand, so
+// it can stay an immediate / constant-bank operand): the ALU pipe carries
+// only the six rotations and four LOP3s of a round.
+#define SHA_RND_F3(a, b, c, d, e, f, g, h, w, k)                                      \
+    do {                                                                              \
+        uint32_t t1_ = fadd(sha_ch((e), (f), (g)),                                    \
+                            fadd(sha_S1(e), fadd((h), fadd((k), (w), one), one), one), one); \
+        (d) = fadd((d), t1_, one);                                                    \
+        (h) = fadd(sha_maj((a), (b), (c)), fadd(sha_S0(a), t1_, one), one);           \
+    } while (0)
+
 #define SHA_SCHED(i)                                                                   \
     W[i] += sha_s0(W[((i) + 1) & 15]) + W[((i) + 9) & 15] + sha_s1(W[((i) + 14) & 15])
 #define SHA_SCHED_F(i)                                                                 \
@@ -305,7 +316,12 @@ PHD uint32_t sha_kc(int t) {
 // through round 63 over message words W (destroyed).
 template <int FMA = 0>
 PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, uint32_t one = 1) {
-#define RND(...) do { if (FMA) SHA_RND_F(__VA_ARGS__); else SHA_RND(__VA_ARGS__); } while (0)
+#define RND(...)                                      \
+    do {                                              \
+        if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);        \
+        else if (FMA) SHA_RND_F(__VA_ARGS__);         \
+        else SHA_RND(__VA_ARGS__);                    \
+    } while (0)
     uint32_t a, b, c, d, e, f, g, h;
     if (r0 == 0) {
         a = st[0]; b = st[1]; c = st[2]; d = st[3]; e = st[4]; f = st[5]; g = st[6]; h = st[7];

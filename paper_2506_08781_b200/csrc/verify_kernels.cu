@@ -268,6 +268,16 @@ __global__ void k_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_
     }
 }
 
+// Variable-length printable entries at caller-provided offsets (lengths from
+// poslo_synth_varlen), byte-identical to the CPU generator.
+__global__ void k_synth_var(uint64_t seed, uint64_t first, uint64_t n, const uint64_t* __restrict__ offsets,
+                            uint8_t* __restrict__ out) {
+    uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t o0 = offsets[t], o1 = offsets[t + 1];
+    for (uint64_t b = 0; b < o1 - o0; b++) out[o0 + b] = poslo_synth_ascii(seed, first + t, (uint32_t)b);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
@@ -315,6 +325,12 @@ void launch_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L, u
                         cudaStream_t s) {
     if (!n) return;
     k_synth_fixed<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, first, n, L, d_out);
+}
+
+void launch_synth_var(uint64_t seed, uint64_t first, uint64_t n, const uint64_t* d_offsets, uint8_t* d_out,
+                      cudaStream_t s) {
+    if (!n) return;
+    k_synth_var<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(seed, first, n, d_offsets, d_out);
 }
 
 }  // namespace poslo_gpu

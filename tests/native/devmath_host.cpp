@@ -86,8 +86,10 @@ void dm_entry_s1_mode(int mode, const uint8_t m[32], const uint8_t x0[16], uint3
     for (int k = 0; k < 8; k++) mw[k] = bswap32(mm[k]);
     ots_pre(x0w, pre);
     if (mode >= 3)
-        (mode == 3 ? entry_limbs_s1_l32_compact<0> : mode == 4 ? entry_limbs_s1_l32_compact<1>
-                                                               : entry_limbs_s1_l32_compact<2>)(
+        (mode == 3 ? entry_limbs_s1_l32_compact<0>
+         : mode == 4 ? entry_limbs_s1_l32_compact<1>
+         : mode == 5 ? entry_limbs_s1_l32_compact<2>
+                     : entry_limbs_s1_l32_compact<3>)(
             x0w, pre, j, mw, limbs_out, 1u);
     else if (mode == 1)
         entry_limbs_s1_l32<1>(x0w, pre, j, mw, limbs_out, 1u);
@@ -169,6 +171,26 @@ int dm_commit_check_comb(const uint8_t y[32], const uint8_t e[32], const uint8_t
     acc = comb_mul_add(acc, tb.data(), d);
     rist_encode(acc, out);
     return 0;
+}
+
+// split check used by paver: e*Y == R - s*B, compared with rist_equal
+int dm_check_split(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32], const uint8_t r[32]) {
+    gpt Y, R;
+    if (!rist_decode(y, Y)) return -1;
+    if (!rist_decode(r, R)) return 0;
+    std::vector<gcached> ty, tb;
+    host_table(Y, ty);
+    host_table(pt_base(), tb);
+    uint32_t ee[8], ss[8];
+    words_le(e, ee, 8);
+    words_le(s, ss, 8);
+    int8_t d[64];
+    sc_signed_radix16(ss, d);
+    gpt S = comb_mul_add(pt_identity(), tb.data(), d);
+    gpt T = pt_add(R, pt_neg(S));
+    sc_signed_radix16(ee, d);
+    gpt E = comb_mul_add(pt_identity(), ty.data(), d);
+    return rist_equal(E, T) ? 1 : 0;
 }
 
 int dm_fold(uint32_t n, const uint8_t* pts, uint8_t out[32]) {

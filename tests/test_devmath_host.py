@@ -73,7 +73,7 @@ def test_entry_fast32_and_deferred_sum(dm, suite):
     assert o.raw == ref  # sum of raw digests reduced once == sum of reductions
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5, 6])
 def test_sha_pipe_balance_modes(dm, mode):
     rng = random.Random(20 + mode)
     for t in range(64):
@@ -118,6 +118,14 @@ def test_group_ops(dm, kat):
         assert o.raw.hex() == P
     for p, v in kat["point_valid"]:
         assert dm.dm_point_valid(bytes.fromhex(p)) == v
+    # split check (paver): e*Y == R - s*B  <=>  encode(e*Y + s*B) == R
+    rows = kat["commit_check"][:12]
+    for i, (Y, e, s, P) in enumerate(rows):
+        Yb, eb, sb, Pb = (bytes.fromhex(x) for x in (Y, e, s, P))
+        assert dm.dm_check_split(Yb, eb, sb, Pb) == 1
+        other = bytes.fromhex(rows[(i + 1) % len(rows)][3])
+        assert dm.dm_check_split(Yb, eb, sb, other) == int(other == Pb)
+        assert dm.dm_check_split(Yb, eb, sb, b"\xff" * 32) == 0  # invalid R never verifies
     for a, b, c in kat["group_combine"]:
         o = out(32)
         assert dm.dm_fold(2, bytes.fromhex(a) + bytes.fromhex(b), o) == 0

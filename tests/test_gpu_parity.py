@@ -305,3 +305,14 @@ def test_chunked_host_path_matches_device_resident(verifier):
         ents = [bytes(host[(k * n2 + j) * L:(k * n2 + j + 1) * L].numpy()) for j in range(n2)]
         ref = _oracle_etilde(1, {k: ents}, ds)
         assert et_h[32 * k:32 * k + 32] == ref[0]
+
+
+@pytest.mark.parametrize("n2", [65, 100, 128, 129, 200, 256])
+def test_multi_epoch_tiles_match_oracle(verifier, n2):
+    """Small epochs (n2 <= 256) run several epochs per CTA (k_hash_s1_l32m),
+    including a partial last CTA."""
+    cfg, batches, ds = _synthetic(1, 37, n2, 32, seed=n2)
+    parts, e_hat = verifier.agg_ekeys(cfg, batches, ds, 1)
+    ref = _oracle_etilde(1, batches, ds)
+    assert [p[1] for p in parts] == ref
+    assert e_hat == O.sum_scalars(ref)
