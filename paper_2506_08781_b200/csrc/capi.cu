@@ -231,7 +231,9 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     P.fast = P.uniform && !b->offsets && b->entry_len == 32 && (b->suite == 1 || b->suite == 2) && aligned;
     uint32_t* d_partial = nullptr;
     if (P.uniform) {
-        if (P.fast)
+        if (P.fast && b->suite == 1 && b->n2 <= kLeanMaxN2)
+            tm.tile_entries = std::max<uint32_t>(b->n2, 1);  // one tile per epoch (lean kernel)
+        else if (P.fast)
             tm.tile_entries = b->n2 <= 128 ? 128 : (b->n2 <= 256 ? 256 : 1024);
         else
             tm.tile_entries = 1024;

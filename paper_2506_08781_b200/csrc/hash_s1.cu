@@ -10,42 +10,9 @@ namespace {
 
 using namespace tilec;
 
-// ---------------------------------------------------------------- K1+K2, suite 1, L = 32
-// MODE selects the ALU/FMA pipe balance of the SHA-256 rounds (sha256.cuh);
-// `one` is 1 at run time but opaque to the compiler so additions stay IMADs.
-template <int T, int E, int MODE>
-__global__ void __launch_bounds__(T) k_hash_s1_l32(const uint4* __restrict__ pay, uint32_t n2,
-                                                   uint32_t tpe, const uint4* __restrict__ x0,
-                                                   uint32_t* __restrict__ partial,
-                                                   uint32_t* __restrict__ etilde, uint32_t one,
-                                                   uint32_t tile0) {
-    __shared__ uint32_t red[(T / 32) * 17];
-    const uint32_t tile = tile0 + blockIdx.x;
-    const uint32_t ep = tile / tpe, sub = tile - ep * tpe;
-    const uint4 xr = __ldg(x0 + ep);
-    const uint32_t x0w[4] = {bswap32(xr.x), bswap32(xr.y), bswap32(xr.z), bswap32(xr.w)};
-    uint32_t pre[8];
-    ots_pre(x0w, pre);
-    uint32_t acc[17];
-    acc17_zero(acc);
-    const uint32_t jbase = sub * (T * E) + threadIdx.x;
-#pragma unroll
-    for (int i = 0; i < E; i++) {
-        const uint32_t j = jbase + i * T;
-        if (j < n2) {
-            const uint64_t ent = (uint64_t)ep * n2 + j;
-            const uint4 a = __ldg(pay + 2 * ent), b = __ldg(pay + 2 * ent + 1);
-            const uint32_t m[8] = {bswap32(a.x), bswap32(a.y), bswap32(a.z), bswap32(a.w),
-                                   bswap32(b.x), bswap32(b.y), bswap32(b.z), bswap32(b.w)};
-            uint32_t limbs[16];
-            entry_limbs_s1_l32<MODE>(x0w, pre, j, m, limbs, one);
-            acc17_add16(acc, limbs);
-        }
-    }
-    block_reduce_acc17(acc, red);
-    if (threadIdx.x == 0) store_tile(acc, tpe == 1, ep, tile, partial, etilde);
-}
+constexpr int kLeanStride = 256;  // threads per CTA of the register-lean kernel
 
+// ---------------------------------------------------------------- K1+K2, suite 1, L = 32
 // Compact variant (default): E entries per thread in a rolled loop, the
 // three compressions of an entry in one rolled loop over shared round code.
 template <int T, int E, int FMA>
@@ -53,7 +20,7 @@ __global__ void __launch_bounds__(T) k_hash_s1_l32c(const uint4* __restrict__ pa
                                                     uint32_t tpe, const uint4* __restrict__ x0,
                                                     uint32_t* __restrict__ partial,
                                                     uint32_t* __restrict__ etilde, uint32_t tile0,
-                                                    uint32_t one) {
+                                                    const PipeK pk) {
     __shared__ uint32_t red[(T / 32) * 17];
     const uint32_t tile = tile0 + blockIdx.x;
     const uint32_t ep = tile / tpe, sub = tile - ep * tpe;
@@ -73,7 +40,7 @@ __global__ void __launch_bounds__(T) k_hash_s1_l32c(const uint4* __restrict__ pa
             const uint32_t m[8] = {bswap32(a.x), bswap32(a.y), bswap32(a.z), bswap32(a.w),
                                    bswap32(b.x), bswap32(b.y), bswap32(b.z), bswap32(b.w)};
             uint32_t limbs[16];
-            entry_limbs_s1_l32_compact<FMA>(x0w, pre, j, m, limbs, one);
+            entry_limbs_s1_l32_compact<FMA>(x0w, pre, j, m, limbs, pk);
             acc17_add16(acc, limbs);
         }
     }
@@ -81,54 +48,153 @@ __global__ void __launch_bounds__(T) k_hash_s1_l32c(const uint4* __restrict__ pa
     if (threadIdx.x == 0) store_tile(acc, tpe == 1, ep, tile, partial, etilde);
 }
 
-// Multi-epoch tiles for small epochs (n2 <= T/EPC * E, e.g. the n2 = 256 of
-// the coarse configs): EPC epochs per CTA, T/EPC threads per epoch, so the
-// CTA-wide fixed costs (hoisted OTS rounds, the 17-limb reduction) are paid
-// once per 4 entries per thread instead of once per 2. Reduction: warp
-// shuffles, then the first thread of each epoch folds its warps' partials.
-template <int T, int E, int FMA, int EPC, int MINB>
-__global__ void __launch_bounds__(T, MINB) k_hash_s1_l32m(const uint4* __restrict__ pay, uint32_t n2,
-                                                    uint32_t n_epochs, uint32_t epoch0,
-                                                    const uint4* __restrict__ x0,
-                                                    uint32_t* __restrict__ etilde, uint32_t one) {
+// Register-lean multi-epoch kernel. The three compressions of an entry are
+// a dependency chain with little instruction-level parallelism, so the
+// hash rate is set by how many warps each scheduler can choose from. Here
+// only the compression state (16 schedule words + 8 working words), the
+// one-time seed x and loop indices stay in registers: the per-epoch seed
+// words and hoisted onetime_seed mid-state live in shared memory, the entry
+// is re-read from L1 for each of its two hashes, and the running sums live
+// in shared memory as two 9-limb accumulators (H0 and H1 halves, one column
+// per thread: conflict-free). That allows MINB CTAs of T threads per SM.
+PD void smem_acc9_add8(uint32_t* s, const uint32_t v[8]) {
+    uint32_t a[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) a[k] = s[k * kLeanStride];
+    asm("add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.cc.u32 %2, %2, %11;\n\t"
+        "addc.cc.u32 %3, %3, %12;\n\t"
+        "addc.cc.u32 %4, %4, %13;\n\t"
+        "addc.cc.u32 %5, %5, %14;\n\t"
+        "addc.cc.u32 %6, %6, %15;\n\t"
+        "addc.cc.u32 %7, %7, %16;\n\t"
+        "addc.u32 %8, %8, 0;\n\t"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+          "+r"(a[8])
+        : "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+#pragma unroll
+    for (int k = 0; k < 9; k++) s[k * kLeanStride] = a[k];
+}
+
+template <int T, int EPC, int FMA, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restrict__ pay, uint32_t n2,
+                                                          uint32_t n_epochs, uint32_t epoch0,
+                                                          const uint4* __restrict__ x0,
+                                                          uint32_t* __restrict__ etilde, const PipeK pk) {
+    static_assert(T == kLeanStride, "accumulator column stride");
     constexpr int TPE = T / EPC;  // threads per epoch (multiple of 32)
+    __shared__ uint32_t s_pre[EPC][8], s_x0w[EPC][4];
+    __shared__ uint32_t s_acc[18 * T];  // rows 0..8: sum of H1 words, rows 9..17: sum of H0 words
     __shared__ uint32_t red[(T / 32) * 17];
-    const uint32_t ep = epoch0 + blockIdx.x * EPC + threadIdx.x / TPE;
-    const uint32_t lt = threadIdx.x % TPE;
+    const uint32_t le = threadIdx.x / TPE, lt = threadIdx.x % TPE;
+    const uint32_t ep = epoch0 + blockIdx.x * EPC + le;
     const bool live = ep < n_epochs;
-    uint32_t acc[17];
-    acc17_zero(acc);
-    if (live) {
+    if (lt == 0 && live) {
         const uint4 xr = __ldg(x0 + ep);
         const uint32_t x0w[4] = {bswap32(xr.x), bswap32(xr.y), bswap32(xr.z), bswap32(xr.w)};
         uint32_t pre[8];
         ots_pre(x0w, pre);
+#pragma unroll
+        for (int k = 0; k < 8; k++) s_pre[le][k] = pre[k];
+#pragma unroll
+        for (int k = 0; k < 4; k++) s_x0w[le][k] = x0w[k];
+    }
+    uint32_t* acc = s_acc + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 18; k++) acc[k * T] = 0;
+    __syncthreads();
+    if (live) {
 #pragma unroll 1
-        for (int i = 0; i < E; i++) {
-            const uint32_t j = lt + i * TPE;
-            if (j < n2) {
-                const uint64_t ent = (uint64_t)ep * n2 + j;
-                const uint4 a = __ldg(pay + 2 * ent), b = __ldg(pay + 2 * ent + 1);
-                const uint32_t m[8] = {bswap32(a.x), bswap32(a.y), bswap32(a.z), bswap32(a.w),
-                                       bswap32(b.x), bswap32(b.y), bswap32(b.z), bswap32(b.w)};
-                uint32_t limbs[16];
-                entry_limbs_s1_l32_compact<FMA>(x0w, pre, j, m, limbs, one);
-                acc17_add16(acc, limbs);
+        for (uint32_t j = lt; j < n2; j += TPE) {
+            const uint4* pe = pay + 2 * ((uint64_t)ep * n2 + j);
+            uint32_t x[4] = {0, 0, 0, 0};
+#pragma unroll 1
+            for (int c = 0; c < 3; c++) {
+                uint32_t W[16], st[8];
+                int r0 = 0;
+                if (c == 0) {  // x = onetime_seed(x0, j), resumed at round 4
+#pragma unroll
+                    for (int k = 0; k < 4; k++) W[k] = s_x0w[le][k];
+                    W[4] = j;
+                    W[5] = 0x80000000u;
+#pragma unroll
+                    for (int k = 6; k < 15; k++) W[k] = 0;
+                    W[15] = 160u;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) st[k] = s_pre[le][k];
+                    r0 = 4;
+                } else {
+                    const uint4 a = __ldg(pe), b = __ldg(pe + 1);
+                    const uint32_t m[8] = {bswap32(a.x), bswap32(a.y), bswap32(a.z), bswap32(a.w),
+                                           bswap32(b.x), bswap32(b.y), bswap32(b.z), bswap32(b.w)};
+                    if (c == 1) {  // m || x
+#pragma unroll
+                        for (int k = 0; k < 8; k++) W[k] = m[k];
+                        W[8] = x[0]; W[9] = x[1]; W[10] = x[2]; W[11] = x[3];
+                        W[12] = 0x80000000u; W[13] = 0; W[14] = 0; W[15] = 384u;
+                    } else {  // 0x01 || m || x
+                        W[0] = 0x01000000u | (m[0] >> 8);
+#pragma unroll
+                        for (int k = 1; k < 8; k++) W[k] = fshr32(m[k], m[k - 1], 8);
+                        W[8] = fshr32(x[0], m[7], 8);
+                        W[9] = fshr32(x[1], x[0], 8);
+                        W[10] = fshr32(x[2], x[1], 8);
+                        W[11] = fshr32(x[3], x[2], 8);
+                        W[12] = (x[3] << 24) | 0x00800000u;
+                        W[13] = 0; W[14] = 0; W[15] = 392u;
+                    }
+                    sha256_init(st);
+                }
+                sha256_rounds_compact<FMA>(st, W, r0, pk);
+                const uint32_t iv[8] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3, SHA_IV4, SHA_IV5, SHA_IV6, SHA_IV7};
+                if (c == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) x[k] = st[k] + iv[k];
+                } else {
+                    // digest word k is limb 7 - k of its half (H0 = high half, H1 = low half)
+                    uint32_t v[8];
+#pragma unroll
+                    for (int k = 0; k < 8; k++) v[7 - k] = st[k] + iv[k];
+                    smem_acc9_add8(acc + (c == 1 ? 9 * T : 0), v);
+                }
             }
         }
+    }
+    // acc17 = lo9 + hi9 * 2^256
+    uint32_t a17[17];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a17[k] = acc[k * T];
+    {
+        uint32_t lo8 = acc[8 * T], hi[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) hi[k] = acc[(9 + k) * T];
+        asm("add.cc.u32 %0, %9, %10;\n\t"
+            "addc.cc.u32 %1, %11, 0;\n\t"
+            "addc.cc.u32 %2, %12, 0;\n\t"
+            "addc.cc.u32 %3, %13, 0;\n\t"
+            "addc.cc.u32 %4, %14, 0;\n\t"
+            "addc.cc.u32 %5, %15, 0;\n\t"
+            "addc.cc.u32 %6, %16, 0;\n\t"
+            "addc.cc.u32 %7, %17, 0;\n\t"
+            "addc.u32 %8, %18, 0;\n\t"
+            : "=r"(a17[8]), "=r"(a17[9]), "=r"(a17[10]), "=r"(a17[11]), "=r"(a17[12]), "=r"(a17[13]),
+              "=r"(a17[14]), "=r"(a17[15]), "=r"(a17[16])
+            : "r"(lo8), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]),
+              "r"(hi[7]), "r"(hi[8]));
     }
     const unsigned full = 0xffffffffu;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
         uint32_t v[17];
 #pragma unroll
-        for (int k = 0; k < 17; k++) v[k] = __shfl_down_sync(full, acc[k], off);
-        acc17_add17(acc, v);
+        for (int k = 0; k < 17; k++) v[k] = __shfl_down_sync(full, a17[k], off);
+        acc17_add17(a17, v);
     }
     const int warp = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0)
 #pragma unroll
-        for (int k = 0; k < 17; k++) red[warp * 17 + k] = acc[k];
+        for (int k = 0; k < 17; k++) red[warp * 17 + k] = a17[k];
     __syncthreads();
     if (lt == 0 && live) {
 #pragma unroll 1
@@ -136,10 +202,10 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32m(const uint4* __restric
             uint32_t v[17];
 #pragma unroll
             for (int k = 0; k < 17; k++) v[k] = red[(warp + w) * 17 + k];
-            acc17_add17(acc, v);
+            acc17_add17(a17, v);
         }
         uint32_t e[8];
-        sc_reduce_limbs(acc, 17, e);
+        sc_reduce_limbs(a17, 17, e);
 #pragma unroll
         for (int k = 0; k < 8; k++) etilde[(size_t)ep * 8 + k] = e[k];
     }
@@ -147,34 +213,15 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32m(const uint4* __restric
 
 }  // namespace
 
-static int sha_mode() {
-    static int mode = [] {
-        const char* e = std::getenv("POSLO_SHA_MODE");
-        // 3-6 = compact (3 plain, 4 IMAD rounds, 5 + IMAD schedule, 6 + IMAD K+w),
-        // 0-2 = fully unrolled variants (instruction-cache bound; kept for comparison)
-        int m = e ? std::atoi(e) : 5;  // measured best on B200: 13.0 ms / 2^26 entries
-        return (m < 0 || m > 6) ? 5 : m;
-    }();
-    return mode;
-}
+static PipeK pipek_host() { return pipek_make(); }
 
+// Large epochs (n2 > kLeanMaxN2): tiles of T * E entries, partial sums
+// finalised per epoch by launch_epoch_finalize.
 template <int T, int E>
-static void launch_cfg(int mode, uint32_t n_tiles, const uint4* pay, const TileMap& tm, const uint4* d_x0,
-                uint32_t* d_partial, uint32_t* d_etilde, cudaStream_t s) {
-    if (mode == 3)
-        k_hash_s1_l32c<T, E, 0><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, tm.tile_begin, 1u);
-    else if (mode == 4)
-        k_hash_s1_l32c<T, E, 1><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, tm.tile_begin, 1u);
-    else if (mode == 5)
-        k_hash_s1_l32c<T, E, 2><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, tm.tile_begin, 1u);
-    else if (mode == 6)
-        k_hash_s1_l32c<T, E, 3><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, tm.tile_begin, 1u);
-    else if (mode == 0)
-        k_hash_s1_l32<T, E, 0><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, 1u, tm.tile_begin);
-    else if (mode == 1)
-        k_hash_s1_l32<T, E, 1><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, 1u, tm.tile_begin);
-    else
-        k_hash_s1_l32<T, E, 2><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde, 1u, tm.tile_begin);
+static void launch_tiled(uint32_t n_tiles, const uint4* pay, const TileMap& tm, const uint4* d_x0,
+                         uint32_t* d_partial, uint32_t* d_etilde, cudaStream_t s) {
+    k_hash_s1_l32c<T, E, 2><<<n_tiles, T, 0, s>>>(pay, tm.n2, tm.tiles_per_epoch, d_x0, d_partial, d_etilde,
+                                                  tm.tile_begin, pipek_host());
 }
 
 void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
@@ -182,30 +229,22 @@ void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
     uint32_t n_tiles = tm.tile_count ? tm.tile_count : tm.n_epochs * tm.tiles_per_epoch;
     if (!n_tiles) return;
     const uint4* pay = reinterpret_cast<const uint4*>(lay.payload);
-    const int mode = sha_mode();
-    // small epochs (one tile each): multi-epoch CTAs, 4 entries per thread
-    if (mode == 5 && tm.tiles_per_epoch == 1 && tm.n2 > 64 && tm.n2 <= 256) {
-        const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;  // tile == epoch here
-        const uint32_t epc = tm.n2 <= 128 ? 8 : 4;
-        const uint32_t grid = (n_tiles + epc - 1) / epc;
-        static const int minb = [] {
-            const char* e = std::getenv("POSLO_S1M_MINB");
-            return e ? std::atoi(e) : 3;
-        }();
-        if (epc == 4 && minb == 2)
-            k_hash_s1_l32m<256, 4, 2, 4, 2><<<grid, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, 1u);
-        else if (epc == 4)
-            k_hash_s1_l32m<256, 4, 2, 4, 3><<<grid, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, 1u);
+    if (tm.tiles_per_epoch == 1 && tm.n2 <= kLeanMaxN2) {
+        // whole epochs per CTA (tile == epoch): register-lean kernel, e~ written directly
+        const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;
+        const PipeK pk = pipek_host();
+        if (tm.n2 <= 128)
+            k_hash_s1_l32r<256, 8, 2, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, pk);
         else
-            k_hash_s1_l32m<256, 4, 2, 8, 3><<<grid, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, 1u);
+            k_hash_s1_l32r<256, 4, 2, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, pk);
         return;
     }
     if (tm.tile_entries == 256 * 4)
-        launch_cfg<256, 4>(mode, n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
+        launch_tiled<256, 4>(n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
     else if (tm.tile_entries == 128 * 2)
-        launch_cfg<128, 2>(mode, n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
+        launch_tiled<128, 2>(n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
     else
-        launch_cfg<128, 1>(mode, n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
+        launch_tiled<128, 1>(n_tiles, pay, tm, d_x0, d_partial, d_etilde, s);
 }
 
 }  // namespace poslo_gpu

@@ -81,7 +81,7 @@ __device__ __forceinline__ void sha256_var(const VarStream& s, uint32_t H[8]) {
         uint32_t st[8];
 #pragma unroll
         for (int i = 0; i < 8; i++) st[i] = H[i];
-        sha256_rounds_compact<2>(st, W, 0, 1u);
+        sha256_rounds_compact<2>(st, W, 0, pipek_make());
 #pragma unroll
         for (int i = 0; i < 8; i++) H[i] += st[i];
     }

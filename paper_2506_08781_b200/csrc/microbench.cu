@@ -5,6 +5,9 @@
 //   0  ALU pipe only  (LOP3 chains)
 //   1  FMA pipe only  (IMAD chains, multiplier opaque to the compiler)
 //   2  both pipes     (interleaved LOP3 + IMAD, the dual-issue ceiling)
+//   3  IMAD with an immediate multiplier      4  LOP3 + immediate IMAD
+//   5  SHF.R.W funnel rotate (ALU pipe)       6  IMAD.HI immediate
+//   7  LOP3 + IMAD.HI immediate
 // Every thread runs 8 independent chains; lane-ops = threads * iters * 8 (16 for mode 2).
 // Not part of the verifier ABI (separate library libposlo_microbench.so).
 #include <cuda_runtime.h>
@@ -16,15 +19,21 @@ __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uin
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         x[k] = threadIdx.x * (k + 1) ^ a;
-        y[k] = blockIdx.x + k * b;
+        y[k] = blockIdx.x + k * b + threadIdx.x * 0x10001u;  // per-lane: keeps IMADs off the uniform datapath
     }
     for (int i = 0; i < iters; i++) {
 #pragma unroll
         for (int k = 0; k < 8; k++) {
-            if (MODE == 0 || MODE == 2)
+            if (MODE == 0 || MODE == 2 || MODE == 4 || MODE == 7)
                 asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(x[(k + 1) & 7]));
             if (MODE == 1 || MODE == 2)
                 asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(a), "r"(y[(k + 3) & 7]));
+            if (MODE == 3 || MODE == 4)  // IMAD, immediate multiplier
+                asm volatile("mad.lo.u32 %0, %0, 0x9e3779b9, %1;" : "+r"(y[k]) : "r"(y[(k + 3) & 7]));
+            if (MODE == 5)  // SHF funnel rotate
+                asm volatile("shf.r.wrap.b32 %0, %0, %0, 13;" : "+r"(x[k]));
+            if (MODE == 6 || MODE == 7)  // IMAD.HI, immediate multiplier
+                asm volatile("mad.hi.u32 %0, %0, 0x9e3779b9, %1;" : "+r"(y[k]) : "r"(y[(k + 3) & 7]));
         }
     }
     uint32_t r = 0;
@@ -45,9 +54,17 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     auto launch = [&]() {
-        if (mode == 0) k_int_peak<0><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
-        else if (mode == 1) k_int_peak<1><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
-        else k_int_peak<2><<<blocks, 256>>>(out, 0x9e3779b9u, 0x7f4a7c15u, iters);
+        const uint32_t a = 0x9e3779b9u, b = 0x7f4a7c15u;
+        switch (mode) {
+            case 0: k_int_peak<0><<<blocks, 256>>>(out, a, b, iters); break;
+            case 1: k_int_peak<1><<<blocks, 256>>>(out, a, b, iters); break;
+            case 2: k_int_peak<2><<<blocks, 256>>>(out, a, b, iters); break;
+            case 3: k_int_peak<3><<<blocks, 256>>>(out, a, b, iters); break;
+            case 4: k_int_peak<4><<<blocks, 256>>>(out, a, b, iters); break;
+            case 5: k_int_peak<5><<<blocks, 256>>>(out, a, b, iters); break;
+            case 6: k_int_peak<6><<<blocks, 256>>>(out, a, b, iters); break;
+            default: k_int_peak<7><<<blocks, 256>>>(out, a, b, iters); break;
+        }
     };
     launch();  // warm-up (clock ramp)
     launch();
@@ -58,7 +75,7 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    double per_iter = mode == 2 ? 16.0 : 8.0;
+    double per_iter = (mode == 2 || mode == 4 || mode == 7) ? 16.0 : 8.0;
     double ops = (double)blocks * 256 * iters * per_iter * reps;
     *ops_per_s = ops / (ms * 1e-3);
     if (ms_out) *ms_out = ms / reps;

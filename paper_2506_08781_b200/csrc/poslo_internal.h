@@ -47,6 +47,9 @@ void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, 
 
 // Fast path: suite 1, 32-byte entries, uniform epochs. Writes per-tile
 // 17-limb partial sums, or e_tilde directly when one tile covers an epoch.
+// Suite-1, 32-byte uniform epochs of at most kLeanMaxN2 entries are hashed one
+// epoch per CTA slice (tile == epoch); larger epochs are tiled.
+constexpr uint32_t kLeanMaxN2 = 4096;
 void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
                         uint32_t* d_partial, uint32_t* d_etilde, cudaStream_t s);
 

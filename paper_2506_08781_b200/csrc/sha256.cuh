@@ -73,6 +73,50 @@ PHD uint32_t shr_via(uint32_t w, int n, uint32_t one) {
     return w >> n;
 }
 
+// Opaque multipliers for moving rotations and shifts to the FMA pipe.
+// rotr(x, n) = lo(x * 2^(32-n)) + hi(x * 2^(32-n)) (the two halves have
+// disjoint bits), i.e. one IMAD.HI + one IMAD, no ALU instruction; x >> n =
+// hi(x * 2^(32-n)) is one IMAD.HI. The multipliers arrive as kernel
+// parameters so ptxas cannot strength-reduce them back into SHF/LEA (ALU).
+struct PipeK {
+    uint32_t one;       // 1
+    uint32_t r22, r25;  // 2^(32-22), 2^(32-25): rotr 22 (Sigma0), rotr 25 (Sigma1)
+    uint32_t s3, s10;   // 2^29, 2^22: >> 3 (sigma0), >> 10 (sigma1)
+};
+
+PHD PipeK pipek_make() {
+    PipeK k;
+    k.one = 1u;
+    k.r22 = 1u << 10;
+    k.r25 = 1u << 7;
+    k.s3 = 1u << 29;
+    k.s10 = 1u << 22;
+    return k;
+}
+
+// rotr(x, n) with p = 2^(32-n), on the FMA pipe
+PHD uint32_t rotr_fma(uint32_t x, uint32_t p) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi, r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(x), "r"(p));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(p), "r"(hi));
+    return r;
+#else
+    return (uint32_t)(((uint64_t)x * p) >> 32) + x * p;
+#endif
+}
+
+// x >> n with p = 2^(32-n), on the FMA pipe
+PHD uint32_t shr_fma(uint32_t x, uint32_t p) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(x), "r"(p));
+    return hi;
+#else
+    return (uint32_t)(((uint64_t)x * p) >> 32);
+#endif
+}
+
 // Constness of all 64 schedule words, evaluated at compile time: W[t] is a
 // constant iff all four words it is derived from are.
 template <uint32_t CM>
@@ -306,6 +350,60 @@ PHD uint32_t sha_kc(int t) {
         (h) = fadd(sha_maj((a), (b), (c)), fadd(sha_S0(a), t1_, one), one);           \
     } while (0)
 
+// FMA == 4, balanced: one rotation of each Sigma on the FMA pipe
+// (rotr_fma) plus the additions of SHA_RND_F. Per round 4 SHF + 4 LOP3 +
+// 1 IADD3 on the ALU pipe and 9 IMAD-class on the FMA pipe; per schedule word
+// 4 SHF + 2 LOP3 (ALU) and 2 IMAD.HI + 3 IMAD (FMA). Per compression
+// ALU 864 / FMA 816 instructions, against ALU 1088 / FMA 464 for FMA == 2:
+// the two pipes (16 lanes/clk each per SMSP) are then nearly equally loaded
+// and the bound moves to the issue slot (1 instruction/clk/SMSP).
+#define SHA_RND_B(a, b, c, d, e, f, g, h, w, k)                                       \
+    do {                                                                              \
+        const uint32_t s1_ = rotr32((e), 6) ^ rotr32((e), 11) ^ rotr_fma((e), pk.r25); \
+        const uint32_t s0_ = rotr32((a), 2) ^ rotr32((a), 13) ^ rotr_fma((a), pk.r22); \
+        uint32_t t1_ = fadd(sha_ch((e), (f), (g)), fadd(s1_, (h) + (w) + (k), one), one); \
+        (d) = fadd((d), t1_, one);                                                    \
+        (h) = fadd(sha_maj((a), (b), (c)), fadd(s0_, t1_, one), one);                 \
+    } while (0)
+#define SHA_SCHED_B(i)                                                                 \
+    do {                                                                              \
+        const uint32_t x15_ = W[((i) + 1) & 15], x2_ = W[((i) + 14) & 15];            \
+        const uint32_t s0_ = rotr32(x15_, 7) ^ rotr32(x15_, 18) ^ shr_fma(x15_, pk.s3); \
+        const uint32_t s1_ = rotr32(x2_, 17) ^ rotr32(x2_, 19) ^ shr_fma(x2_, pk.s10); \
+        W[i] = fadd(s0_, fadd(s1_, fadd(W[((i) + 9) & 15], W[i], one), one), one);    \
+    } while (0)
+
+// Pipe-assignment sweep (FMA >= 16: P = FMA - 16 is a bit set). Each bit moves
+// one class of work of a round / schedule word between the ALU pipe (IADD3,
+// LOP3, SHF) and the FMA pipe (IMAD; IMAD.HI is half rate, measured):
+//   P&1  sigma shifts on IMAD.HI          P&2  h + w + K on IMADs
+//   P&4  Sigma1 rotr 25 on IMAD.HI+IMAD   P&8  Sigma0 rotr 22 on IMAD.HI+IMAD
+//   P&16 T1 = IADD3(hwk, S1, Ch)          P&32 schedule sum as 2 IADD3
+//   P&64 e' = d + T1 on the ALU           P&128 a' = IADD3(T1, S0, Maj)
+template <int P>
+PHD void sha_rnd_p(uint32_t a, uint32_t b, uint32_t c, uint32_t& d, uint32_t e, uint32_t f, uint32_t g,
+                   uint32_t& h, uint32_t w, uint32_t k, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    const uint32_t r25 = (P & 4) ? rotr_fma(e, pk.r25) : rotr32(e, 25);
+    const uint32_t r22 = (P & 8) ? rotr_fma(a, pk.r22) : rotr32(a, 22);
+    const uint32_t s1 = rotr32(e, 6) ^ rotr32(e, 11) ^ r25;
+    const uint32_t s0 = rotr32(a, 2) ^ rotr32(a, 13) ^ r22;
+    const uint32_t hwk = (P & 2) ? fadd(h, fadd(k, w, one), one) : h + w + k;
+    const uint32_t t1 = (P & 16) ? hwk + s1 + sha_ch(e, f, g) : fadd(sha_ch(e, f, g), fadd(s1, hwk, one), one);
+    d = (P & 64) ? d + t1 : fadd(d, t1, one);
+    h = (P & 128) ? t1 + s0 + sha_maj(a, b, c) : fadd(sha_maj(a, b, c), fadd(s0, t1, one), one);
+}
+
+template <int P>
+PHD uint32_t sha_sched_p(uint32_t w16, uint32_t w15, uint32_t w7, uint32_t w2, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    const uint32_t sh3 = (P & 1) ? shr_fma(w15, pk.s3) : w15 >> 3;
+    const uint32_t sh10 = (P & 1) ? shr_fma(w2, pk.s10) : w2 >> 10;
+    const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ sh3;
+    const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ sh10;
+    return (P & 32) ? w16 + s0 + w7 + s1 : fadd(s0, fadd(s1, fadd(w7, w16, one), one), one);
+}
+
 #define SHA_SCHED(i)                                                                   \
     W[i] += sha_s0(W[((i) + 1) & 15]) + W[((i) + 9) & 15] + sha_s1(W[((i) + 14) & 15])
 #define SHA_SCHED_F(i)                                                                 \
@@ -315,10 +413,13 @@ PHD uint32_t sha_kc(int t) {
 // Working state st (a..h) from round r0 (0 or 4; rounds < r0 already applied)
 // through round 63 over message words W (destroyed).
 template <int FMA = 0>
-PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, uint32_t one = 1) {
+PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const PipeK& pk) {
+    const uint32_t one = pk.one;
 #define RND(...)                                      \
     do {                                              \
-        if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);        \
+        if (FMA >= 16) sha_rnd_p<FMA - 16>(__VA_ARGS__, pk); \
+        else if (FMA >= 4) SHA_RND_B(__VA_ARGS__);    \
+        else if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);   \
         else if (FMA) SHA_RND_F(__VA_ARGS__);         \
         else SHA_RND(__VA_ARGS__);                    \
     } while (0)
@@ -348,7 +449,10 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, uint32_t 
     for (int blk = 16; blk < 64; blk += 16) {
 #pragma unroll
         for (int i = 0; i < 16; i++) {
-            if (FMA >= 2) SHA_SCHED_F(i); else SHA_SCHED(i);
+            if (FMA >= 16) W[i] = sha_sched_p<FMA - 16>(W[i], W[(i + 1) & 15], W[(i + 9) & 15], W[(i + 14) & 15], pk);
+            else if (FMA >= 4) SHA_SCHED_B(i);
+            else if (FMA >= 2) SHA_SCHED_F(i);
+            else SHA_SCHED(i);
         }
         RND(a, b, c, d, e, f, g, h, W[0], sha_kc(blk + 0));
         RND(h, a, b, c, d, e, f, g, W[1], sha_kc(blk + 1));
@@ -377,7 +481,7 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, uint32_t 
 // the round code. Output as in h2s_sha256_len32.
 template <int FMA = 0>
 PHD void entry_limbs_s1_l32_compact(const uint32_t x0w[4], const uint32_t pre[8], uint32_t j,
-                                    const uint32_t m[8], uint32_t limbs[16], uint32_t one = 1) {
+                                    const uint32_t m[8], uint32_t limbs[16], const PipeK& pk) {
     uint32_t x[4] = {0, 0, 0, 0};
 #pragma unroll 1
     for (int c = 0; c < 3; c++) {
@@ -410,7 +514,7 @@ PHD void entry_limbs_s1_l32_compact(const uint32_t x0w[4], const uint32_t pre[8]
             W[13] = 0; W[14] = 0; W[15] = 392u;
             sha256_init(st);
         }
-        sha256_rounds_compact<FMA>(st, W, r0, one);
+        sha256_rounds_compact<FMA>(st, W, r0, pk);
         const uint32_t iv[8] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3, SHA_IV4, SHA_IV5, SHA_IV6, SHA_IV7};
         if (c == 0) {
 #pragma unroll

@@ -89,8 +89,9 @@ void dm_entry_s1_mode(int mode, const uint8_t m[32], const uint8_t x0[16], uint3
         (mode == 3 ? entry_limbs_s1_l32_compact<0>
          : mode == 4 ? entry_limbs_s1_l32_compact<1>
          : mode == 5 ? entry_limbs_s1_l32_compact<2>
-                     : entry_limbs_s1_l32_compact<3>)(
-            x0w, pre, j, mw, limbs_out, 1u);
+         : mode == 6 ? entry_limbs_s1_l32_compact<3>
+                     : entry_limbs_s1_l32_compact<4>)(
+            x0w, pre, j, mw, limbs_out, pipek_make());
     else if (mode == 1)
         entry_limbs_s1_l32<1>(x0w, pre, j, mw, limbs_out, 1u);
     else if (mode == 2)

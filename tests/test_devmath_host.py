@@ -73,7 +73,7 @@ def test_entry_fast32_and_deferred_sum(dm, suite):
     assert o.raw == ref  # sum of raw digests reduced once == sum of reductions
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_sha_pipe_balance_modes(dm, mode):
     rng = random.Random(20 + mode)
     for t in range(64):
