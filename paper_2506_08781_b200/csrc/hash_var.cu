@@ -2,11 +2,10 @@
 // syslog-style 64..1024-byte records), uniform or ragged epochs.
 //
 // onetime_seed (primitives.cpp:209-223) then H(m||x) and H(0x01||m||x)
-// (primitives.cpp:162-176) streamed block by block straight from the packed
-// payload: each message word is one funnel-shifted pair of aligned 32-bit
-// loads (the entry can start at any byte), so no staging copy is needed;
-// only the last one or two blocks (x, 0x80 padding, bit length) take a
-// byte-assembled slow path. Work per entry grows with L
+// (primitives.cpp:162-176), the two hash streams advanced block by block in
+// lockstep from one staged 72-byte window per block step (see stage_window):
+// 16-byte vector loads instead of per-word gathers, so the L1 sees 6 wide
+// requests per block pair rather than 64 narrow ones. Work per entry grows with L
 // (ceil((L+25)/64) + ceil((L+26)/64) + 1 compressions), so each CTA first
 // counting-sorts its tile by block count in shared memory: threads of a warp
 // then hash entries of similar length and the warp does not idle on the
@@ -20,82 +19,111 @@ namespace {
 
 using namespace tilec;
 
-constexpr int kVarT = 256;        // threads per CTA
+constexpr int kVarT = 128;        // threads per CTA
 constexpr int kVarTile = 1024;    // entries per tile
 constexpr int kVarBuckets = 32;   // block-count buckets (clamped)
 
-// Big-endian word at byte offset p of the logical stream
-//   [0x01 if tagged] || m (L bytes) || x (16 bytes) || 0x80 || 0.. || bitlen
-// where total = message length (L + 16 [+1]) and nb = number of 64-byte blocks.
-struct VarStream {
-    const uint8_t* m;
-    uint32_t L;
-    uint32_t tag;       // 0 or 1 (bytes of prefix)
-    uint32_t x[4];      // x as big-endian words
-    uint64_t total;     // L + 16 + tag
-    uint64_t nb;        // blocks
-
-    __device__ __forceinline__ uint32_t m_word_fast(uint32_t q) const {  // bytes m[q..q+3], q+3 < L
-        const uintptr_t a = (uintptr_t)(m + q);
-        const uint32_t* base = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-        const uint32_t sh = (uint32_t)(a & 3) * 8;
-        uint32_t lo = __ldg(base);
-        uint32_t v = sh ? __funnelshift_r(lo, __ldg(base + 1), sh) : lo;
-        return bswap32(v);
-    }
-    __device__ __forceinline__ uint32_t byte_at(uint64_t p) const {
-        if (p < tag) return 0x01u;
-        uint64_t q = p - tag;
-        if (q < L) return m[q];
-        q -= L;
-        if (q < 16) return (x[q >> 2] >> (24 - 8 * (q & 3))) & 0xffu;
-        if (p == total) return 0x80u;
-        return 0u;
-    }
-    __device__ __forceinline__ uint32_t word(uint64_t p) const {
-        if (p >= tag && p - tag + 3 < L) return m_word_fast((uint32_t)(p - tag));
-        uint32_t w = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++) w = (w << 8) | byte_at(p + i);
-        return w;
-    }
-};
-
-__device__ __forceinline__ void sha256_var(const VarStream& s, uint32_t H[8]) {
-    sha256_init(H);
-    for (uint64_t b = 0; b < s.nb; b++) {
-        uint32_t W[16];
-        const uint64_t p0 = 64 * b;
-        const bool fast = p0 + 64 <= s.tag + s.L && p0 >= s.tag;
-        if (fast) {
-#pragma unroll
-            for (int k = 0; k < 16; k++) W[k] = s.m_word_fast((uint32_t)(p0 - s.tag + 4 * k));
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; k++) W[k] = s.word(p0 + 4 * k);
-        }
-        if (b == s.nb - 1) {
-            W[14] = (uint32_t)((s.total * 8) >> 32);
-            W[15] = (uint32_t)(s.total * 8);
-        }
-        uint32_t st[8];
-#pragma unroll
-        for (int i = 0; i < 8; i++) st[i] = H[i];
-        sha256_rounds_compact<2>(st, W, 0, pipek_make());
-#pragma unroll
-        for (int i = 0; i < 8; i++) H[i] += st[i];
-    }
-}
+constexpr int kSlotWords = 28;    // per-thread staging slot: 24-word window + x (4 words)
+constexpr uint32_t kNoEntry = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t nblocks(uint64_t msg_len) { return (uint32_t)((msg_len + 9 + 63) / 64); }
 
-__global__ void __launch_bounds__(kVarT) k_hash_s1_var(EntryLayout lay, TileMap tm,
-                                                       const uint4* __restrict__ x0,
-                                                       uint32_t* __restrict__ partial) {
+// Staging of one 64-byte block step. Both hash streams of an entry read the
+// same bytes: H(m || x) at stream offset p reads m[p], H(0x01 || m || x)
+// reads m[p - 1], and x || 0x80 || 0.. follows m in both. For block b a
+// thread stages the window of m positions [64b - 4, 64b + 68) in its private
+// shared-memory slot: six 16-byte aligned vector loads (only chunks that hold
+// bytes of this entry are read), then the bytes at positions >= L are
+// overwritten with x || 0x80 || 0.. and, for b = 0, position -1 with the
+// 0x01 tag. Message words are then one LDS + one PRMT each (the PRMT does
+// both the byte-misaligned funnel and the big-endian swap).
+struct VarEntry {
+    const uint8_t* m;  // entry bytes
+    uint32_t L;
+    uint32_t* slot;    // kSlotWords words of shared memory
+    uintptr_t base;    // 16-byte aligned global address of slot word 0 (window start)
+};
+
+__device__ __forceinline__ void stage_window(VarEntry& v, uint32_t b) {
+    const uintptr_t a = (uintptr_t)v.m;
+    const uintptr_t lo = a + 64ull * b - 4;
+    v.base = lo & ~(uintptr_t)15;
+    uint4* s4 = reinterpret_cast<uint4*>(v.slot);
+#pragma unroll
+    for (int c = 0; c < 6; c++) {
+        const uintptr_t cs = v.base + 16 * c;
+        uint4 q = make_uint4(0, 0, 0, 0);
+        if (cs < a + v.L && cs + 16 > a) q = __ldg(reinterpret_cast<const uint4*>(cs));
+        s4[c] = q;
+    }
+    uint8_t* sb = reinterpret_cast<uint8_t*>(v.slot);
+    const int64_t w0 = (int64_t)64 * b - 4;  // m position of the first window byte we need
+    const int64_t off = (int64_t)(a - v.base);  // slot byte of m position 0
+    if (b == 0) sb[off - 1] = 0x01;  // tag byte of the second stream
+    const int64_t wend = (int64_t)64 * b + 68;
+    if (wend > (int64_t)v.L) {
+        const uint8_t* xs = reinterpret_cast<const uint8_t*>(v.slot + 24);
+        for (int64_t q = max(w0, (int64_t)v.L); q < wend; q++) {
+            const int64_t r = q - (int64_t)v.L;
+            sb[off + q] = r < 16 ? xs[r] : (r == 16 ? 0x80 : 0);
+        }
+    }
+}
+
+// Message words of block b of one stream (tag = 0 or 1 prefix bytes).
+__device__ __forceinline__ void load_block(const VarEntry& v, uint32_t b, uint32_t tag, uint32_t W[16]) {
+    const uint32_t d = (uint32_t)((uintptr_t)v.m + 64ull * b - tag - v.base);  // slot byte of word 0
+    const uint32_t r = d & 3;
+    const uint32_t sel = (r + 3) | (r + 2) << 4 | (r + 1) << 8 | r << 12;
+    const uint32_t* s = v.slot + (d >> 2);
+    uint32_t lo = s[0];
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const uint32_t hi = s[k + 1];
+        W[k] = __byte_perm(lo, hi, sel);
+        lo = hi;
+    }
+}
+
+__device__ __forceinline__ void compress_into(uint32_t H[8], uint32_t W[16], const PipeK& pk) {
+    uint32_t st[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) st[i] = H[i];
+    sha256_rounds_compact<2>(st, W, 0, pk);
+#pragma unroll
+    for (int i = 0; i < 8; i++) H[i] += st[i];
+}
+
+PD void smem_acc9_add8v(uint32_t* s, int stride, const uint32_t v[8]) {
+    uint32_t a[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) a[k] = s[k * stride];
+    asm("add.cc.u32 %0, %0, %9;\n\t"
+        "addc.cc.u32 %1, %1, %10;\n\t"
+        "addc.cc.u32 %2, %2, %11;\n\t"
+        "addc.cc.u32 %3, %3, %12;\n\t"
+        "addc.cc.u32 %4, %4, %13;\n\t"
+        "addc.cc.u32 %5, %5, %14;\n\t"
+        "addc.cc.u32 %6, %6, %15;\n\t"
+        "addc.cc.u32 %7, %7, %16;\n\t"
+        "addc.u32 %8, %8, 0;\n\t"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+          "+r"(a[8])
+        : "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+#pragma unroll
+    for (int k = 0; k < 9; k++) s[k * stride] = a[k];
+}
+
+__global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileMap tm,
+                                                          const uint4* __restrict__ x0,
+                                                          uint32_t* __restrict__ partial, const PipeK pk) {
     __shared__ uint32_t red[(kVarT / 32) * 17];
     __shared__ uint16_t order[kVarTile];
     __shared__ uint32_t bucket_count[kVarBuckets];
     __shared__ uint32_t bucket_base[kVarBuckets];
+    __shared__ __align__(16) uint32_t slots[kVarT * kSlotWords];
+    __shared__ uint32_t s_acc[18 * kVarT];  // rows 0..8: sum of H1 digests, 9..17: sum of H0 digests
+    __shared__ uint32_t s_pre[8], s_x0w[4];
     const uint32_t tile = tm.tile_begin + blockIdx.x;
     uint32_t ep, j0, count;
     uint64_t ebase;
@@ -110,8 +138,22 @@ __global__ void __launch_bounds__(kVarT) k_hash_s1_var(EntryLayout lay, TileMap 
         count = min(tm.tile_entries, tm.n2 - j0);
         ebase = (uint64_t)ep * tm.n2;
     }
-    // counting sort of the tile by block count (longest first)
+    // counting sort of the tile by block count (longest first): the lanes of
+    // a warp then run the same number of block steps
     if (threadIdx.x < kVarBuckets) bucket_count[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        const uint4 xr = __ldg(x0 + ep);
+        const uint32_t x0w[4] = {bswap32(xr.x), bswap32(xr.y), bswap32(xr.z), bswap32(xr.w)};
+        uint32_t pre[8];
+        ots_pre(x0w, pre);
+#pragma unroll
+        for (int k = 0; k < 8; k++) s_pre[k] = pre[k];
+#pragma unroll
+        for (int k = 0; k < 4; k++) s_x0w[k] = x0w[k];
+    }
+    uint32_t* acc = s_acc + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 18; k++) acc[k * kVarT] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
         const uint64_t ent = ebase + j0 + i;
@@ -120,10 +162,10 @@ __global__ void __launch_bounds__(kVarT) k_hash_s1_var(EntryLayout lay, TileMap 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t acc = 0;
+        uint32_t a = 0;
         for (int k = kVarBuckets - 1; k >= 0; k--) {
-            bucket_base[k] = acc;
-            acc += bucket_count[k];
+            bucket_base[k] = a;
+            a += bucket_count[k];
         }
     }
     __syncthreads();
@@ -135,43 +177,95 @@ __global__ void __launch_bounds__(kVarT) k_hash_s1_var(EntryLayout lay, TileMap 
     }
     __syncthreads();
 
-    const uint4 xr = __ldg(x0 + ep);
-    const uint32_t x0w[4] = {bswap32(xr.x), bswap32(xr.y), bswap32(xr.z), bswap32(xr.w)};
-    uint32_t pre[8];
-    ots_pre(x0w, pre);
-    uint32_t acc[17];
-    acc17_zero(acc);
+    VarEntry v;
+    v.slot = slots + threadIdx.x * kSlotWords;
+#pragma unroll 1
     for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
-        const uint32_t idx = order[i];
-        const uint32_t j = j0 + idx;
+        const uint32_t j = j0 + order[i];
         const uint64_t ent = ebase + j;
-        const uint8_t* m;
         uint64_t L;
         if (lay.offsets) {
             const uint64_t o0 = lay.offsets[ent];
-            m = lay.payload + o0;
+            v.m = lay.payload + o0;
             L = lay.offsets[ent + 1] - o0;
         } else {
-            m = lay.payload + ent * lay.entry_len;
+            v.m = lay.payload + ent * lay.entry_len;
             L = lay.entry_len;
         }
-        uint32_t xw[4];
-        ots_finish(x0w, pre, j, xw);
-        uint32_t limbs[16], H[8];
-        VarStream s1{m, (uint32_t)L, 0u, {xw[0], xw[1], xw[2], xw[3]}, L + 16, nblocks(L + 16)};
-        sha256_var(s1, H);
+        v.L = (uint32_t)L;
+        {  // x = onetime_seed(x0, j), resumed at round 4; kept in the slot tail (bytes, stream order)
+            uint32_t W[16], st[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) limbs[15 - k] = H[k];
-        VarStream s2{m, (uint32_t)L, 1u, {xw[0], xw[1], xw[2], xw[3]}, L + 17, nblocks(L + 17)};
-        sha256_var(s2, H);
+            for (int k = 0; k < 4; k++) W[k] = s_x0w[k];
+            W[4] = j;
+            W[5] = 0x80000000u;
 #pragma unroll
-        for (int k = 0; k < 8; k++) limbs[7 - k] = H[k];
-        acc17_add16(acc, limbs);
+            for (int k = 6; k < 15; k++) W[k] = 0;
+            W[15] = 160u;
+#pragma unroll
+            for (int k = 0; k < 8; k++) st[k] = s_pre[k];
+            sha256_rounds_compact<2>(st, W, 4, pk);
+            const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
+#pragma unroll
+            for (int k = 0; k < 4; k++) v.slot[24 + k] = bswap32(st[k] + iv[k]);
+        }
+        const uint32_t nb0 = nblocks(L + 16), nb1 = nblocks(L + 17);
+        uint32_t H0[8], H1[8];
+        sha256_init(H0);
+        sha256_init(H1);
+#pragma unroll 1
+        for (uint32_t b = 0; b < nb1; b++) {
+            stage_window(v, b);
+            uint32_t W[16];
+            if (b < nb0) {
+                load_block(v, b, 0, W);
+                if (b == nb0 - 1) {
+                    W[14] = (uint32_t)(((L + 16) * 8) >> 32);
+                    W[15] = (uint32_t)((L + 16) * 8);
+                }
+                compress_into(H0, W, pk);
+            }
+            load_block(v, b, 1, W);
+            if (b == nb1 - 1) {
+                W[14] = (uint32_t)(((L + 17) * 8) >> 32);
+                W[15] = (uint32_t)((L + 17) * 8);
+            }
+            compress_into(H1, W, pk);
+        }
+        // H0 is the high half of the 512-bit wide value: digest word k is limb 7 - k of its half
+        uint32_t d[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) d[7 - k] = H0[k];
+        smem_acc9_add8v(acc + 9 * kVarT, kVarT, d);
+#pragma unroll
+        for (int k = 0; k < 8; k++) d[7 - k] = H1[k];
+        smem_acc9_add8v(acc, kVarT, d);
     }
-    block_reduce_acc17(acc, red);
+    uint32_t a17[17];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a17[k] = acc[k * kVarT];
+    {
+        uint32_t lo8 = acc[8 * kVarT], hi[9];
+#pragma unroll
+        for (int k = 0; k < 9; k++) hi[k] = acc[(9 + k) * kVarT];
+        asm("add.cc.u32 %0, %9, %10;\n\t"
+            "addc.cc.u32 %1, %11, 0;\n\t"
+            "addc.cc.u32 %2, %12, 0;\n\t"
+            "addc.cc.u32 %3, %13, 0;\n\t"
+            "addc.cc.u32 %4, %14, 0;\n\t"
+            "addc.cc.u32 %5, %15, 0;\n\t"
+            "addc.cc.u32 %6, %16, 0;\n\t"
+            "addc.cc.u32 %7, %17, 0;\n\t"
+            "addc.u32 %8, %18, 0;\n\t"
+            : "=r"(a17[8]), "=r"(a17[9]), "=r"(a17[10]), "=r"(a17[11]), "=r"(a17[12]), "=r"(a17[13]),
+              "=r"(a17[14]), "=r"(a17[15]), "=r"(a17[16])
+            : "r"(lo8), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]),
+              "r"(hi[7]), "r"(hi[8]));
+    }
+    block_reduce_acc17(a17, red);
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < 17; k++) partial[(size_t)tile * 17 + k] = acc[k];
+        for (int k = 0; k < 17; k++) partial[(size_t)tile * 17 + k] = a17[k];
 }
 
 }  // namespace
@@ -180,7 +274,7 @@ void launch_hash_s1_var(const EntryLayout& lay, const TileMap& tm, const uint4* 
                         cudaStream_t s) {
     uint32_t n_tiles = tm.tile_count ? tm.tile_count : (tm.tiles ? tm.n_tiles : tm.n_epochs * tm.tiles_per_epoch);
     if (!n_tiles) return;
-    k_hash_s1_var<<<n_tiles, kVarT, 0, s>>>(lay, tm, d_x0, d_partial);
+    k_hash_s1_var<<<n_tiles, kVarT, 0, s>>>(lay, tm, d_x0, d_partial, pipek_make());
 }
 
 }  // namespace poslo_gpu
