@@ -149,7 +149,10 @@ struct Prepared {
     TileMap tm{};
     bool fast = false;
     bool uniform = false;
-    uint32_t* d_etilde = nullptr;
+    bool want_etilde = true;        // false: only e-hat is needed (paver, agg_ekeys without e~ out)
+    uint32_t* d_etilde = nullptr;   // per-epoch e~ (8 limbs), valid when want_etilde
+    const uint32_t* sum_src = nullptr;  // what e-hat sums: e~ (8 limbs) or raw epoch sums (17 limbs)
+    int sum_limbs = 8;
 };
 
 bool is_uniform(const poslo_batch* b) {
@@ -268,7 +271,19 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         tm.n_tiles = (uint32_t)tiles.size();
     }
     ENSURE(b_partial, (size_t)std::max<uint32_t>(tm.n_tiles, 1) * 17, d_partial);
-    bool need_finalize = P.fast ? tm.tiles_per_epoch != 1 : true;
+    // The lean suite-1 kernel leaves each epoch's raw 544-bit digest sum in
+    // d_partial; the mod-l reduction to e~ is a separate full-warp kernel, and
+    // is skipped when only e-hat is wanted (sum of raw sums, reduced once;
+    // exact while the batch has < 2^32 entries, so 17 limbs cannot overflow).
+    const bool lean = P.fast && b->suite == 1 && tm.tiles_per_epoch == 1 && b->n2 <= kLeanMaxN2;
+    bool need_finalize = P.fast ? (tm.tiles_per_epoch != 1 || lean) : true;
+    P.sum_src = P.d_etilde;
+    P.sum_limbs = 8;
+    if (lean && !P.want_etilde && n_entries < (1ull << 32)) {
+        need_finalize = false;
+        P.sum_src = d_partial;
+        P.sum_limbs = 17;
+    }
     auto launch_hash = [&](const TileMap& t) {
         if (P.fast) {
             if (b->suite == 1)
@@ -536,6 +551,7 @@ int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_til
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     Guard g(ctx);
     Prepared P;
+    P.want_etilde = e_tilde_out != nullptr;
     int rc = run_hash(ctx, b, P, err);
     if (rc) return rc;
     mark(ctx, kEvSum);
@@ -544,7 +560,7 @@ int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_til
         uint32_t* d_scr;
         ENSURE(b_sum, 8, d_sum);
         ENSURE(b_scratch, 17 * 1024, d_scr);
-        launch_sum_mod_l(P.d_etilde, 8, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
+        launch_sum_mod_l(P.sum_src, P.sum_limbs, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
         ctx->launches += 2;
     }
     mark(ctx, kEvGroup);
@@ -606,6 +622,7 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
     // 4. e-hat = sum of agg_ekeys (:83-85)
     Prepared P;
+    P.want_etilde = false;
     rc = run_hash(ctx, b, P, err);
     if (rc) {
         cudaStreamSynchronize(ctx->side);
@@ -614,7 +631,7 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     mark(ctx, kEvSum);
     ENSURE(b_sum, 8, d_sum);
     ENSURE(b_scratch, 17 * 1024, d_scr);
-    launch_sum_mod_l(P.d_etilde, 8, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
+    launch_sum_mod_l(P.sum_src, P.sum_limbs, b->n_epochs, nullptr, d_sum, d_scr, ctx->stream);
     ctx->launches += 2;
     mark(ctx, kEvGroup);
     // 5. one commitment check (:86): e-hat * Y == R - s*alpha, then ONE

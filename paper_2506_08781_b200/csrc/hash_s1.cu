@@ -81,7 +81,7 @@ template <int T, int EPC, int FMA, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restrict__ pay, uint32_t n2,
                                                           uint32_t n_epochs, uint32_t epoch0,
                                                           const uint4* __restrict__ x0,
-                                                          uint32_t* __restrict__ etilde, const PipeK pk) {
+                                                          uint32_t* __restrict__ epoch_sum, const PipeK pk) {
     static_assert(T == kLeanStride, "accumulator column stride");
     constexpr int TPE = T / EPC;  // threads per epoch (multiple of 32)
     __shared__ uint32_t s_pre[EPC][8], s_x0w[EPC][4];
@@ -204,10 +204,10 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
             for (int k = 0; k < 17; k++) v[k] = red[(warp + w) * 17 + k];
             acc17_add17(a17, v);
         }
-        uint32_t e[8];
-        sc_reduce_limbs(a17, 17, e);
+        // raw 544-bit epoch sum; the mod-l reduction runs in a full-warp kernel
+        // (k_epoch_finalize) or not at all when only e-hat is needed
 #pragma unroll
-        for (int k = 0; k < 8; k++) etilde[(size_t)ep * 8 + k] = e[k];
+        for (int k = 0; k < 17; k++) epoch_sum[(size_t)ep * 17 + k] = a17[k];
     }
 }
 
@@ -230,13 +230,13 @@ void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
     if (!n_tiles) return;
     const uint4* pay = reinterpret_cast<const uint4*>(lay.payload);
     if (tm.tiles_per_epoch == 1 && tm.n2 <= kLeanMaxN2) {
-        // whole epochs per CTA (tile == epoch): register-lean kernel, e~ written directly
+        // whole epochs per CTA (tile == epoch): register-lean kernel, raw epoch sums
         const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;
         const PipeK pk = pipek_host();
         if (tm.n2 <= 128)
-            k_hash_s1_l32r<256, 8, 2, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, pk);
+            k_hash_s1_l32r<256, 8, 2, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         else
-            k_hash_s1_l32r<256, 4, 2, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_etilde, pk);
+            k_hash_s1_l32r<256, 4, 2, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         return;
     }
     if (tm.tile_entries == 256 * 4)

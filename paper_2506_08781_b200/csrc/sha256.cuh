@@ -410,19 +410,44 @@ PHD uint32_t sha_sched_p(uint32_t w16, uint32_t w15, uint32_t w7, uint32_t w2, c
     W[i] = fadd(sha_s0(W[((i) + 1) & 15]), fadd(sha_s1(W[((i) + 14) & 15]),            \
                 fadd(W[((i) + 9) & 15], W[i], one), one), one)
 
-// Working state st (a..h) from round r0 (0 or 4; rounds < r0 already applied)
-// through round 63 over message words W (destroyed).
-template <int FMA = 0>
-PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const PipeK& pk) {
-    const uint32_t one = pk.one;
-#define RND(...)                                      \
-    do {                                              \
-        if (FMA >= 16) sha_rnd_p<FMA - 16>(__VA_ARGS__, pk); \
-        else if (FMA >= 4) SHA_RND_B(__VA_ARGS__);    \
-        else if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);   \
-        else if (FMA) SHA_RND_F(__VA_ARGS__);         \
-        else SHA_RND(__VA_ARGS__);                    \
+#define SHA_RND_SEL(...)                                        \
+    do {                                                        \
+        if (FMA >= 16) sha_rnd_p<FMA - 16>(__VA_ARGS__, pk);    \
+        else if (FMA >= 4) SHA_RND_B(__VA_ARGS__);              \
+        else if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);             \
+        else if (FMA) SHA_RND_F(__VA_ARGS__);                   \
+        else SHA_RND(__VA_ARGS__);                              \
     } while (0)
+
+// 16 rounds starting at round t0 + 0 whose message words are W[0..15]
+// (after the schedule update): the body shared by all compressions.
+#define SHA_16_ROUNDS(KF, t0)                                                  \
+    do {                                                                       \
+        SHA_RND_SEL(a, b, c, d, e, f, g, h, W[0], KF((t0) + 0));               \
+        SHA_RND_SEL(h, a, b, c, d, e, f, g, W[1], KF((t0) + 1));               \
+        SHA_RND_SEL(g, h, a, b, c, d, e, f, W[2], KF((t0) + 2));               \
+        SHA_RND_SEL(f, g, h, a, b, c, d, e, W[3], KF((t0) + 3));               \
+        SHA_RND_SEL(e, f, g, h, a, b, c, d, W[4], KF((t0) + 4));               \
+        SHA_RND_SEL(d, e, f, g, h, a, b, c, W[5], KF((t0) + 5));               \
+        SHA_RND_SEL(c, d, e, f, g, h, a, b, W[6], KF((t0) + 6));               \
+        SHA_RND_SEL(b, c, d, e, f, g, h, a, W[7], KF((t0) + 7));               \
+        SHA_RND_SEL(a, b, c, d, e, f, g, h, W[8], KF((t0) + 8));               \
+        SHA_RND_SEL(h, a, b, c, d, e, f, g, W[9], KF((t0) + 9));               \
+        SHA_RND_SEL(g, h, a, b, c, d, e, f, W[10], KF((t0) + 10));             \
+        SHA_RND_SEL(f, g, h, a, b, c, d, e, W[11], KF((t0) + 11));             \
+        SHA_RND_SEL(e, f, g, h, a, b, c, d, W[12], KF((t0) + 12));             \
+        SHA_RND_SEL(d, e, f, g, h, a, b, c, W[13], KF((t0) + 13));             \
+        SHA_RND_SEL(c, d, e, f, g, h, a, b, W[14], KF((t0) + 14));             \
+        SHA_RND_SEL(b, c, d, e, f, g, h, a, W[15], KF((t0) + 15));             \
+    } while (0)
+
+// Rounds r0..15 (r0 = 0, or 4 resuming after a hoisted round 3) over W[0..15].
+// st is a..h in the usual order on entry and exit.
+template <int FMA = 0>
+PHD void sha256_rounds_head(uint32_t st[8], const uint32_t W[16], int r0, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    (void)one;
+#define RND SHA_RND_SEL
     uint32_t a, b, c, d, e, f, g, h;
     if (r0 == 0) {
         a = st[0]; b = st[1]; c = st[2]; d = st[3]; e = st[4]; f = st[5]; g = st[6]; h = st[7];
@@ -445,8 +470,20 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const Pip
     RND(d, e, f, g, h, a, b, c, W[13], sha_k(13));
     RND(c, d, e, f, g, h, a, b, W[14], sha_k(14));
     RND(b, c, d, e, f, g, h, a, W[15], sha_k(15));
+#undef RND
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
+// Rounds blk0..63 (blk0 = 16 or 32) as a rolled loop over one 16-round body:
+// schedule update of the rolling window W (W[i] = W_{blk-16+i} on entry),
+// then 16 rounds with K from constant memory.
+template <int FMA = 0>
+PHD void sha256_rounds_loop(uint32_t st[8], uint32_t W[16], int blk0, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    (void)one;
+    uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
 #pragma unroll 1
-    for (int blk = 16; blk < 64; blk += 16) {
+    for (int blk = blk0; blk < 64; blk += 16) {
 #pragma unroll
         for (int i = 0; i < 16; i++) {
             if (FMA >= 16) W[i] = sha_sched_p<FMA - 16>(W[i], W[(i + 1) & 15], W[(i + 9) & 15], W[(i + 14) & 15], pk);
@@ -454,24 +491,71 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const Pip
             else if (FMA >= 2) SHA_SCHED_F(i);
             else SHA_SCHED(i);
         }
-        RND(a, b, c, d, e, f, g, h, W[0], sha_kc(blk + 0));
-        RND(h, a, b, c, d, e, f, g, W[1], sha_kc(blk + 1));
-        RND(g, h, a, b, c, d, e, f, W[2], sha_kc(blk + 2));
-        RND(f, g, h, a, b, c, d, e, W[3], sha_kc(blk + 3));
-        RND(e, f, g, h, a, b, c, d, W[4], sha_kc(blk + 4));
-        RND(d, e, f, g, h, a, b, c, W[5], sha_kc(blk + 5));
-        RND(c, d, e, f, g, h, a, b, W[6], sha_kc(blk + 6));
-        RND(b, c, d, e, f, g, h, a, W[7], sha_kc(blk + 7));
-        RND(a, b, c, d, e, f, g, h, W[8], sha_kc(blk + 8));
-        RND(h, a, b, c, d, e, f, g, W[9], sha_kc(blk + 9));
-        RND(g, h, a, b, c, d, e, f, W[10], sha_kc(blk + 10));
-        RND(f, g, h, a, b, c, d, e, W[11], sha_kc(blk + 11));
-        RND(e, f, g, h, a, b, c, d, W[12], sha_kc(blk + 12));
-        RND(d, e, f, g, h, a, b, c, W[13], sha_kc(blk + 13));
-        RND(c, d, e, f, g, h, a, b, W[14], sha_kc(blk + 14));
-        RND(b, c, d, e, f, g, h, a, W[15], sha_kc(blk + 15));
+        SHA_16_ROUNDS(sha_kc, blk);
     }
-#undef RND
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
+// Working state st (a..h) from round r0 (0 or 4; rounds < r0 already applied)
+// through round 63 over message words W (destroyed).
+template <int FMA = 0>
+PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const PipeK& pk) {
+    sha256_rounds_head<FMA>(st, W, r0, pk);
+    sha256_rounds_loop<FMA>(st, W, 16, pk);
+}
+
+// ---- onetime_seed specialisation: F(x0 || be32 j) for all j of an epoch ----
+// The message is x0 (4 words, per epoch), W4 = j and the constants
+// W5 = 0x80000000, W6..W14 = 0, W15 = 160. Hence W16..W18 are per-epoch
+// constants, and in W19..W31 every sigma0 term and the W_{t-16} / W_{t-7}
+// terms drawn from W5..W15 are compile-time or per-epoch constants. OtsEpoch
+// holds the per-epoch values; ots_head_rounds runs rounds 4..31 with the
+// reduced schedule (13 sigma1 evaluations and one sigma0 instead of 16 of
+// each) and leaves W = W16..W31 for sha256_rounds_loop(.., 32, ..).
+struct OtsEpoch {
+    uint32_t w16, w17, w18;
+    uint32_t c19;  // sigma1(W17) + W3
+    uint32_t c20;  // sigma1(W18) + sigma0(0x80000000)
+    uint32_t c31;  // sigma0(W16) + 160
+};
+
+PHD OtsEpoch ots_epoch_consts(const uint32_t x0w[4]) {
+    OtsEpoch E;
+    E.w16 = sha_s0(x0w[1]) + x0w[0];
+    E.w17 = sha_s1(160u) + sha_s0(x0w[2]) + x0w[1];
+    E.w18 = sha_s1(E.w16) + sha_s0(x0w[3]) + x0w[2];
+    E.c19 = sha_s1(E.w17) + x0w[3];
+    E.c20 = sha_s1(E.w18) + sha_s0(0x80000000u);
+    E.c31 = sha_s0(E.w16) + 160u;
+    return E;
+}
+
+template <int FMA = 2>
+PHD void ots_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t j, const OtsEpoch& E, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    (void)one;
+    // rounds 4..15: W4 = j, the rest compile-time constants
+    const uint32_t Wm[16] = {0, 0, 0, 0, j, 0x80000000u, 0, 0, 0, 0, 0, 0, 0, 0, 0, 160u};
+    sha256_rounds_head<FMA>(st, Wm, 4, pk);
+    // schedule words 16..31
+    W[0] = E.w16;
+    W[1] = E.w17;
+    W[2] = E.w18;
+    W[3] = fadd(sha_s0(j), E.c19, one);
+    W[4] = fadd(j, E.c20, one);
+    W[5] = sha_s1(W[3]) + 0x80000000u;
+    W[6] = sha_s1(W[4]) + 160u;
+    W[7] = fadd(sha_s1(W[5]), W[0], one);
+    W[8] = fadd(sha_s1(W[6]), W[1], one);
+    W[9] = fadd(sha_s1(W[7]), W[2], one);
+    W[10] = fadd(sha_s1(W[8]), W[3], one);
+    W[11] = fadd(sha_s1(W[9]), W[4], one);
+    W[12] = fadd(sha_s1(W[10]), W[5], one);
+    W[13] = fadd(sha_s1(W[11]), W[6], one);
+    W[14] = fadd(sha_s1(W[12]), W[7] + sha_s0(160u), one);
+    W[15] = fadd(sha_s1(W[13]), fadd(W[8], E.c31, one), one);
+    uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+    SHA_16_ROUNDS(sha_k, 16);
     st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
 }
 

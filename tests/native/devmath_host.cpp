@@ -100,6 +100,24 @@ void dm_entry_s1_mode(int mode, const uint8_t m[32], const uint8_t x0[16], uint3
         entry_limbs_s1_l32<0>(x0w, pre, j, mw, limbs_out, 1u);
 }
 
+// onetime_seed through the specialised schedule of the lean kernel
+// (ots_epoch_consts + ots_head_rounds + sha256_rounds_loop from round 32)
+void dm_ots_spec(const uint8_t x0[16], uint32_t j, uint8_t out[16]) {
+    uint32_t x0m[4], x0w[4], st[8], W[16];
+    words_le(x0, x0m, 4);
+    for (int k = 0; k < 4; k++) x0w[k] = bswap32(x0m[k]);
+    ots_pre(x0w, st);
+    const OtsEpoch E = ots_epoch_consts(x0w);
+    const PipeK pk = pipek_make();
+    ots_head_rounds<2>(st, W, j, E, pk);
+    sha256_rounds_loop<2>(st, W, 32, pk);
+    const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
+    for (int k = 0; k < 4; k++) {
+        uint32_t v = st[k] + iv[k];
+        out[4 * k] = v >> 24; out[4 * k + 1] = v >> 16; out[4 * k + 2] = v >> 8; out[4 * k + 3] = v;
+    }
+}
+
 // sum of n 16-limb values via the 17-limb accumulator, reduced mod l
 void dm_sum_reduce(const uint32_t* limbs16, uint32_t n, uint8_t e_out[32]) {
     uint32_t acc[17];

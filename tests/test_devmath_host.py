@@ -87,6 +87,17 @@ def test_sha_pipe_balance_modes(dm, mode):
         assert o.raw == O.hash_to_scalar(1, m, O.onetime_seed(1, x0, j))
 
 
+def test_ots_specialised_schedule(dm):
+    # the lean kernel's onetime_seed: per-epoch constants + reduced schedule W16..W31
+    rng = random.Random(77)
+    for t in range(200):
+        x0 = bytes(rng.getrandbits(8) for _ in range(16))
+        j = [0, 1, 255, 1023, 0xFFFFFFFF][t] if t < 5 else rng.getrandbits(32)
+        o = out(16)
+        dm.dm_ots_spec(x0, j, o)
+        assert o.raw == O.onetime_seed(1, x0, j)
+
+
 def test_deferred_sum_worst_case(dm):
     # all-ones digests maximise carries through the 17-limb accumulator
     n = 4096

@@ -44,10 +44,10 @@ int main() {
     uint32_t *et, *et0;
     cudaMalloc(&pay, (size_t)n * 32);
     cudaMalloc(&x0, (size_t)n_ep * 16);
-    cudaMalloc(&et, (size_t)n_ep * 32);
+    cudaMalloc(&et, (size_t)n_ep * 68);
     fill<<<1184, 256>>>((uint32_t*)pay, (size_t)n * 8);
     fill<<<1184, 256>>>((uint32_t*)x0, (size_t)n_ep * 4);
-    std::vector<uint32_t> ref(n_ep * 8), got(n_ep * 8);
+    std::vector<uint32_t> ref(n_ep * 17), got(n_ep * 17);
     const int reps = 5;
     auto check = [&](int P, float ms) {
         cudaMemcpy(got.data(), et, got.size() * 4, cudaMemcpyDeviceToHost);
