@@ -53,9 +53,13 @@ struct poslo_gpu_ctx {
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
+    void* d_tabB256 = nullptr;  // radix-256 combs for batched checks (built on first use)
+    void* d_tabY256 = nullptr;
     void* d_pk = nullptr;
     uint8_t tabY_key[32] = {};
     bool tabY_valid = false;
+    uint8_t tabY256_key[32] = {};
+    bool tabY256_valid = false;
     PinnedStage* stage = nullptr;
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -388,7 +392,7 @@ int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void*
 
 // Comb tables of alpha (once per context) and of Y (cached per Y value).
 // Y validation (GroupElement::from_bytes) happens in the table build.
-int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err) {
+int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false) {
     if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * 128));
     if (!ctx->d_tabB) {
         CU(cudaMalloc(&ctx->d_tabB, kCombTableBytes));
@@ -411,6 +415,22 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
         std::memcpy(ctx->tabY_key, y, 32);
         ctx->tabY_valid = true;
     }
+    if (wide) {
+        if (!ctx->d_tabB256) {
+            CU(cudaMalloc(&ctx->d_tabB256, kComb256TableBytes));
+            launch_build_table256(nullptr, ctx->d_pk, ctx->d_tabB256, d_flags, ctx->stream);
+            ctx->launches += 2;
+        }
+        if (!ctx->d_tabY256) CU(cudaMalloc(&ctx->d_tabY256, kComb256TableBytes));
+        if (!ctx->tabY256_valid || std::memcmp(ctx->tabY256_key, y, 32) != 0) {
+            uint8_t* d_y;
+            UPLOAD(b_y, y, 32, d_y);  // Y already validated by the radix-16 build above
+            launch_build_table256(d_y, ctx->d_pk, ctx->d_tabY256, d_flags, ctx->stream);
+            ctx->launches += 2;
+            std::memcpy(ctx->tabY256_key, y, 32);
+            ctx->tabY256_valid = true;
+        }
+    }
     return POSLO_OK;
 }
 
@@ -423,11 +443,12 @@ int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const u
     uint8_t* d_enc = nullptr;
     ENSURE(b_flags, 4, d_flags);
     CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
-    int rc = ensure_tables(ctx, y, d_flags, err);
+    int rc = ensure_tables(ctx, y, d_flags, err, n > kCtaCheckMax);
     if (rc) return rc;
     if (h_verdict) ENSURE(b_verdict, n, d_verdict);
     if (h_enc) ENSURE(b_enc, (size_t)n * 32, d_enc);
-    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, n, d_e, d_s, d_r, d_enc, d_verdict, ctx->stream);
+    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_r, d_enc,
+                            d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     int ybad = 0;
@@ -512,7 +533,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
     if (ctx->stage) cudaFreeHost(ctx->stage);
-    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_pk})
+    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_tabB256, ctx->d_tabY256, ctx->d_pk})
         if (p) cudaFree(p);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);

@@ -106,7 +106,9 @@ __global__ void k_validate(const uint8_t* __restrict__ pts, uint32_t n, uint8_t*
 // Builds the fixed-base table of P (decoded from `enc`, or the ristretto255
 // generator when enc == nullptr). Stage A (one thread): P_k = 16^k P. Stage B
 // (one thread per entry): (i+1) P_k in cached form.
-__global__ void k_table_pow16(const uint8_t* __restrict__ enc, gpt* __restrict__ pk, int* bad) {
+// W = 4: 64 powers 16^k P; W = 8: 32 powers 256^k P.
+template <int W>
+__global__ void k_table_pow(const uint8_t* __restrict__ enc, gpt* __restrict__ pk, int* bad) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     gpt P;
     if (enc) {
@@ -119,10 +121,25 @@ __global__ void k_table_pow16(const uint8_t* __restrict__ enc, gpt* __restrict__
     } else {
         P = pt_base();
     }
-    for (int k = 0; k < 64; k++) {
+    for (int k = 0; k < 256 / W; k++) {
         pk[k] = P;
-        P = pt_dbl(pt_dbl(pt_dbl(pt_dbl(P))));
+        for (int i = 0; i < W; i++) P = pt_dbl(P);
     }
+}
+
+// Radix-256 fill: thread t = 128 k + i writes (i + 1) 256^k P, by
+// double-and-add on the bits of i + 1 (<= 8 doublings + 8 additions).
+__global__ void k_table_fill256(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 32 * 128) return;
+    const int k = t >> 7, m = (t & 127) + 1;
+    const gpt base = pk[k];
+    gpt q = pt_identity();
+    for (int b = 7; b >= 0; b--) {
+        q = pt_dbl(q);
+        if ((m >> b) & 1) q = pt_add(q, base);
+    }
+    tab[t] = pt_to_cached(q);
 }
 
 __global__ void k_table_fill(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
@@ -183,7 +200,8 @@ __global__ void __launch_bounds__(128) k_check_cta(const gcached* __restrict__ t
     }
 }
 
-// One thread per check (throughput mode, e.g. 2^20 per-epoch checks).
+// One thread per check (throughput mode, e.g. 2^20 per-epoch checks), on
+// the radix-256 combs: 64 mixed additions + one encode per check.
 __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict__ tabY,
                                                       const gcached* __restrict__ tabB, uint32_t n,
                                                       const uint32_t* __restrict__ e,
@@ -194,16 +212,13 @@ __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict_
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint32_t v[8];
-    int8_t d[64];
     gpt acc = pt_identity();
 #pragma unroll
     for (int k = 0; k < 8; k++) v[k] = e[(size_t)i * 8 + k];
-    sc_signed_radix16(v, d);
-    acc = comb_mul_add(acc, tabY, d);
+    acc = comb256_mul_add(acc, tabY, v);
 #pragma unroll
     for (int k = 0; k < 8; k++) v[k] = s[(size_t)i * 8 + k];
-    sc_signed_radix16(v, d);
-    acc = comb_mul_add(acc, tabB, d);
+    acc = comb256_mul_add(acc, tabB, v);
     uint8_t out[32];
     rist_encode(acc, out);
     if (enc)
@@ -312,20 +327,26 @@ void launch_point_validate(const uint8_t* d_pts, uint32_t n, uint8_t* d_ok, cuda
 
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s) {
-    k_table_pow16<<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
+    k_table_pow<4><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
     k_table_fill<<<4, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
 }
 
-void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n, const uint32_t* d_e,
-                             const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
-                             cudaStream_t s) {
+void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s) {
+    k_table_pow<8><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
+    k_table_fill256<<<32, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
+}
+
+void launch_group_check_comb(const void* d_tabY, const void* d_tabB, const void* d_tabY256,
+                             const void* d_tabB256, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
+                             const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, cudaStream_t s) {
     if (!n) return;
-    const gcached* ty = static_cast<const gcached*>(d_tabY);
-    const gcached* tb = static_cast<const gcached*>(d_tabB);
-    if (n <= 1024)
-        k_check_cta<<<n, 128, 0, s>>>(ty, tb, d_e, d_s, d_r, d_enc, d_verdict);
+    if (n <= kCtaCheckMax)
+        k_check_cta<<<n, 128, 0, s>>>(static_cast<const gcached*>(d_tabY), static_cast<const gcached*>(d_tabB),
+                                      d_e, d_s, d_r, d_enc, d_verdict);
     else
-        k_check_thread<<<(n + 127) / 128, 128, 0, s>>>(ty, tb, n, d_e, d_s, d_r, d_enc, d_verdict);
+        k_check_thread<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY256),
+                                                       static_cast<const gcached*>(d_tabB256), n, d_e, d_s,
+                                                       d_r, d_enc, d_verdict);
 }
 
 void launch_check_pre(const void* d_tabB, const uint32_t* d_s, const uint8_t* d_r, void* d_pre,

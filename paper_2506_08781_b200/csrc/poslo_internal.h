@@ -93,14 +93,18 @@ void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, con
 
 // Fixed-base comb table (512 affine Niels points, 48 KiB) of the point encoded at
 // d_enc, or of the generator when d_enc == nullptr. d_pk_scratch >= 64 * 128 B.
-constexpr size_t kCombTableBytes = 512 * 96;
+constexpr size_t kCombTableBytes = 512 * 96;       // radix 16: 64 x 8 affine Niels points
+constexpr size_t kComb256TableBytes = 4096 * 96;  // radix 256: 32 x 128 points
+constexpr uint32_t kCtaCheckMax = 1024;          // larger batches use one thread per check (radix-256 combs)
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s);
 // commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,
 // thread-per-check above).
-void launch_group_check_comb(const void* d_tabY, const void* d_tabB, uint32_t n, const uint32_t* d_e,
-                             const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
-                             cudaStream_t s);
+// Radix-256 tables (kComb256TableBytes) for the thread-per-check path.
+void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s);
+void launch_group_check_comb(const void* d_tabY, const void* d_tabB, const void* d_tabY256,
+                             const void* d_tabB256, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
+                             const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, cudaStream_t s);
 
 // Split single check for paver: pre (R decode, T = R - s*alpha; independent
 // of e-hat, overlappable with hashing) and post (e*Y == T). d_pre >= 256 B.

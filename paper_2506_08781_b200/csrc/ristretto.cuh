@@ -479,6 +479,32 @@ PHD gpt comb_mul_add(gpt acc, const gcached* tab, const int8_t d[64]) {
     return acc;
 }
 
+// Signed radix-256 recoding (throughput-mode combs): d[k] in [-128, 128),
+// sum d[k] 256^k = s; s < 2^253 so the top digit never carries out.
+PHD void sc_signed_radix256(const uint32_t s[8], int16_t d[32]) {
+    int carry = 0;
+    for (int k = 0; k < 32; k++) {
+        int v = (int)((s[k >> 2] >> (8 * (k & 3))) & 255u) + carry;
+        carry = (v + 128) >> 8;
+        d[k] = (int16_t)(v - (carry << 8));
+    }
+}
+
+// acc + s * P via the radix-256 comb table of P (tab[128 k + |d| - 1] =
+// |d| 256^k P): 32 mixed additions instead of the radix-16 table's 64.
+PHD gpt comb256_mul_add(gpt acc, const gcached* tab, const uint32_t s[8]) {
+    int16_t d[32];
+    sc_signed_radix256(s, d);
+    for (int k = 0; k < 32; k++) {
+        const int dig = d[k];
+        if (!dig) continue;
+        const int a = dig < 0 ? -dig : dig;
+        const gcached c = tab[128 * k + a - 1];
+        acc = pt_add_cached(acc, dig < 0 ? cached_neg(c) : c);
+    }
+    return acc;
+}
+
 // Ristretto equality of classes (RFC 9496 §4.3.3): X1*Y2 == Y1*X2 or
 // Y1*Y2 == X1*X2. Equal classes <=> equal canonical encodings, so comparing
 // against a decoded R replaces encoding P (the reference's byte compare).

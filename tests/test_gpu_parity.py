@@ -119,6 +119,29 @@ def test_commit_check_batched(verifier, kat):
         assert g == R.commit_check(Y, e, s)
 
 
+def test_commit_check_radix256_path(verifier, kat):
+    """n > 1024 checks run thread-per-check on the radix-256 combs; they must
+    agree with the CTA path (radix-16 combs, n <= 1024) and the oracle,
+    including edge scalars (0, 1, l - 1, digits that carry)."""
+    import random
+    from oracle import ristretto as R
+    rng = random.Random(256)
+    Y = bytes.fromhex(kat["commit_check"][5][0])
+    L = R.L if hasattr(R, "L") else 2**252 + 27742317777372353535851937790883648493
+    edge = [0, 1, 2, 127, 128, 255, 256, 0x80 * 0x0101010101, L - 1, L - 128, 2**252]
+    vals = edge + [rng.randrange(L) for _ in range(1100 - len(edge))]
+    es = [v.to_bytes(32, "little") for v in vals]
+    ss = [rng.randrange(L).to_bytes(32, "little") for _ in vals]
+    ss[0] = bytes(32)
+    wide = verifier.commit_check_batch(Y, es, ss)          # 1100 > 1024: radix-256 path
+    narrow = []
+    for k in range(0, len(es), 1000):                        # <= 1024: radix-16 CTA path
+        narrow += verifier.commit_check_batch(Y, es[k:k + 1000], ss[k:k + 1000])
+    assert wide == narrow
+    for k in list(range(len(edge))) + [500, 1099]:
+        assert wide[k] == R.commit_check(Y, es[k], ss[k])
+
+
 # ------------------------------------------------------------------ synthetic scale parity
 def _synthetic(suite, n1, n2, L, seed, ragged=False):
     api = A()
