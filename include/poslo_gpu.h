@@ -77,6 +77,10 @@ typedef struct poslo_batch {
     uint32_t ds_len;
     uint32_t ds_capacity;          /* D = log2(n1) */
     int32_t device_resident;       /* payload/offsets live in device memory */
+    const uint64_t* ds_offsets;    /* optional (host): n_epochs + 1 byte offsets into `ds`; epoch k
+                                      is then derived from its OWN stack ds[ds_offsets[k] ..
+                                      ds_offsets[k+1]) (EpochSignature::ds, the distill_epoch
+                                      semantics). NULL: one stack `ds` for every epoch. */
 } poslo_batch;
 
 /* ---- context -------------------------------------------------------------- */
@@ -130,6 +134,30 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t
                      const uint8_t* v_r, uint8_t* v_bit, const uint32_t* umb_index,
                      const uint8_t* umb_s, const uint8_t* umb_r, uint32_t n_umb, uint8_t* u_bits,
                      uint8_t* i_bits, poslo_error* err);
+
+/* ---- coarse distillation (ColdCryptoData::distill_epoch, distiller.cpp:60-89) ---
+ * Batched: the batch holds consecutive epochs in stream order (n2 entries
+ * each), usually with per-epoch seed stacks (batch->ds_offsets: each epoch
+ * verified with its own signature's ds, as aver(pk, {i: msgs}, sig.s_hat,
+ * nullopt, sig.ds) does). verdicts[k] = epoch k valid. The batch is cut
+ * into n_seg segments [seg[g], seg[g+1]) of batch positions (the pieces of
+ * umbrellas, distiller.cpp:82-88); per segment, over its VALID epochs only:
+ * seg_s[g] = sum of s_hats mod l (Scalar::add fold, :48) and seg_r[g] = the
+ * group_combine fold of r_hats (:49, identity = 32 zero bytes when none).
+ * The running CCD state (valid/umbrella accumulators, invalid list, ds) is
+ * the caller's; see paper_2506_08781_b200/distill.py. */
+int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                             const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg,
+                             uint32_t n_seg, uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r,
+                             poslo_error* err);
+
+/* Masked segmented folds on the device: for g < n_seg, over items k in
+ * [seg[g], seg[g+1]) with mask[k] != 0 (mask NULL = all): out_s[g] = sum of
+ * scalars mod l and out_r[g] = group_combine fold of points. Either of
+ * scalars/out_s or points/out_r may be NULL. */
+int poslo_gpu_segfold(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* scalars, const uint8_t* points,
+                      const uint8_t* mask, const uint32_t* seg, uint32_t n_seg, uint8_t* out_s,
+                      uint8_t* out_r, poslo_error* err);
 
 /* ---- group primitives (group.cpp), batched on the device ----------------------
  * commit_check: out[i] = encode(Y^e[i] * alpha^s[i]) (group.cpp:144-167).

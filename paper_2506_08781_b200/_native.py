@@ -35,6 +35,7 @@ class PosloBatch(ctypes.Structure):
         ("ds_len", ctypes.c_uint32),
         ("ds_capacity", ctypes.c_uint32),
         ("device_resident", ctypes.c_int32),
+        ("ds_offsets", ctypes.c_void_p),
     ]
 
 
@@ -44,7 +45,7 @@ EXPORTS = [
     "poslo_gpu_paver", "poslo_gpu_epoch_verify", "poslo_gpu_sebver", "poslo_gpu_commit_check",
     "poslo_gpu_group_fold", "poslo_gpu_point_valid", "poslo_gpu_seed_retrieve",
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
-    "poslo_gpu_synth_varlog",
+    "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold",
 ]
 
 _lib = None
@@ -87,6 +88,8 @@ def load():
         "poslo_gpu_scalar_sum": ([P, c.c_uint64, P, P, E], c.c_int),
         "poslo_gpu_synth_log": ([P, c.c_uint64, c.c_uint64, c.c_uint64, c.c_uint32, P, E], c.c_int),
         "poslo_gpu_synth_varlog": ([P, c.c_uint64, c.c_uint64, c.c_uint64, P, P, E], c.c_int),
+        "poslo_gpu_distill_coarse": ([P, B, P, P, P, P, c.c_uint32, P, P, P, E], c.c_int),
+        "poslo_gpu_segfold": ([P, c.c_uint32, P, P, P, P, c.c_uint32, P, P, E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

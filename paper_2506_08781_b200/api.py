@@ -48,9 +48,13 @@ class DeviceError(RuntimeError):
 def _raise(rc: int, err: N.PosloError):
     msg = err.message.decode(errors="replace")
     if rc == N.FORMAT_ERROR:
-        raise FormatError(msg)
+        e = FormatError(msg)
+        e.epoch = err.epoch
+        raise e
     if rc == N.STATE_ERROR:
-        raise StateError(msg)
+        e = StateError(msg)
+        e.epoch = err.epoch
+        raise e
     if rc == N.SEED_NOT_DISCLOSED:
         raise SeedNotDisclosed(err.epoch)
     if rc == N.INVALID_ARGUMENT:
@@ -218,7 +222,10 @@ class PackedBatch:
     """The map<u32, vector<Bytes>> of the reference packed into one payload
     buffer + offsets (or a fixed stride) + epoch ranges (include/poslo_gpu.h)."""
 
-    def __init__(self, suite: int, n2: int, batches: Dict[int, Sequence[bytes]], ds: SeedStack):
+    def __init__(self, suite: int, n2: int, batches: Dict[int, Sequence[bytes]], ds: SeedStack,
+                 epoch_ds: Optional[Dict[int, SeedStack]] = None):
+        """epoch_ds: optional per-epoch seed stacks (EpochSignature::ds): epoch i is
+        then derived from epoch_ds[i] instead of ds (poslo_batch.ds_offsets)."""
         self.suite = suite
         self.n2 = n2
         self.epochs = np.array(sorted(batches), dtype=np.uint32)
@@ -242,6 +249,12 @@ class PackedBatch:
             np.cumsum(counts, out=self.starts[1:])
         self.ds_bytes = ds.serialize()
         self.ds_capacity = ds.capacity
+        self.ds_offsets = None
+        if epoch_ds is not None:
+            blobs = [epoch_ds[int(e)].serialize() for e in self.epochs]
+            self.ds_offsets = np.zeros(len(blobs) + 1, dtype=np.uint64)
+            np.cumsum([len(x) for x in blobs], out=self.ds_offsets[1:])
+            self.ds_bytes = b"".join(blobs) or b"\x00"
         self._keep = []
 
     def cstruct(self) -> N.PosloBatch:
@@ -263,6 +276,7 @@ class PackedBatch:
         b.ds_len = len(self.ds_bytes)
         b.ds_capacity = self.ds_capacity
         b.device_resident = 0
+        b.ds_offsets = self.ds_offsets.ctypes.data if self.ds_offsets is not None else None
         return b
 
 
@@ -374,6 +388,45 @@ class Verifier:
                    out, et)
         raw = out.raw
         return [bool(raw[k]) for k in range(len(eps))]
+
+    # -- batched coarse distillation (distiller.cpp:60-89): verdicts + masked umbrella folds
+    def distill_coarse(self, pk: PoslocPublicKey, batches, sigs: Dict[int, "EpochSignature"],
+                       seg: Sequence[int]):
+        """Epochs of `batches` (consecutive, n2 entries each) verified against
+        their own signatures (s_hat, pk.r_hats[i], sig.ds). seg: batch-position
+        boundaries (len n_seg + 1). Returns (verdicts, [(s_le, r)] per segment)."""
+        ds_any = next(iter(sigs.values())).ds if sigs else SeedStack(pk.suite.depth())
+        pb = PackedBatch(pk.suite.suite, pk.suite.n2, batches, ds_any,
+                         epoch_ds={i: sigs[i].ds for i in batches})
+        eps = [int(e) for e in pb.epochs]
+        s = b"".join(sigs[e].s_hat for e in eps)
+        r = b"".join(pk.r_hats[e] for e in eps)
+        segs = np.array(seg, dtype=np.uint32)
+        ng = max(len(segs) - 1, 0)
+        verd = ctypes.create_string_buffer(max(len(eps), 1))
+        out_s = ctypes.create_string_buffer(max(ng, 1) * 32)
+        out_r = ctypes.create_string_buffer(max(ng, 1) * 32)
+        cb = pb.cstruct()
+        self._call(self._lib.poslo_gpu_distill_coarse, ctypes.byref(cb), _buf(pk.y), _buf(s) if s else None,
+                   _buf(r) if r else None, segs.ctypes.data if ng else None, ng, verd, out_s, out_r)
+        vr, sr_, rr = verd.raw, out_s.raw, out_r.raw
+        return ([bool(vr[k]) for k in range(len(eps))],
+                [(sr_[32 * g:32 * g + 32], rr[32 * g:32 * g + 32]) for g in range(ng)])
+
+    def segfold(self, scalars: Sequence[bytes], points: Sequence[bytes], mask: Optional[Sequence[bool]],
+                seg: Sequence[int]):
+        """Masked segmented (sum mod l, group_combine fold) on the device."""
+        n = max(len(scalars), len(points))
+        segs = np.array(seg, dtype=np.uint32)
+        ng = max(len(segs) - 1, 0)
+        m = bytes(int(bool(x)) for x in mask) if mask is not None else None
+        out_s = ctypes.create_string_buffer(max(ng, 1) * 32)
+        out_r = ctypes.create_string_buffer(max(ng, 1) * 32)
+        self._call(self._lib.poslo_gpu_segfold, n, _buf(b"".join(scalars)) if scalars else None,
+                   _buf(b"".join(points)) if points else None, _buf(m) if m else None,
+                   segs.ctypes.data if ng else None, ng, out_s if scalars else None,
+                   out_r if points else None)
+        return [(out_s.raw[32 * g:32 * g + 32], out_r.raw[32 * g:32 * g + 32]) for g in range(ng)]
 
     # -- SeBVer over a coarse CCD (distiller.cpp:181-233)
     def sebver(self, y: bytes, suite: SuiteConfig, all_msgs, ds: SeedStack, epochs_distilled: int,

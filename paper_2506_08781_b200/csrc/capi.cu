@@ -33,6 +33,7 @@ struct DevBuf {
 
 struct PinnedStage {  // pinned host landing zone for the per-call small D2H copies
     unsigned long long err_key;
+    unsigned long long err_init;  // H2D: error word seeded with host-detected seed failures
     int flags[4];
     uint8_t verdict;
 };
@@ -49,7 +50,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
@@ -176,8 +177,46 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         if (b->epochs[k] <= b->epochs[k - 1])
             return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epochs must be strictly ascending");
     DsParam ds;
-    int rc = parse_ds(b->ds, b->ds_len, b->ds_capacity, ds, err);
-    if (rc) return rc;
+    int rc = POSLO_OK;
+    std::vector<SeedStart> starts;  // per-epoch stacks: resolved covering nodes
+    unsigned long long host_err = ~0ull;
+    if (b->ds_offsets) {
+        starts.resize(b->n_epochs);
+        for (uint32_t k = 0; k < b->n_epochs; k++) {
+            const uint64_t o0 = b->ds_offsets[k], o1 = b->ds_offsets[k + 1];
+            if (o1 < o0 || o1 > b->ds_len)
+                return set_err(err, POSLO_INVALID_ARGUMENT, b->epochs[k], "bad ds_offsets");
+            rc = parse_ds(b->ds + o0, (uint32_t)(o1 - o0), b->ds_capacity, ds, err);
+            if (rc) {
+                if (err) err->epoch = b->epochs[k];
+                return rc;
+            }
+            // sr (seed_manager.cpp:71-85): top of the stack down
+            const uint32_t q = b->epochs[k];
+            int c = -1;
+            for (int i = ds.count - 1; i >= 0; i--) {
+                const uint64_t lo = (uint64_t)ds.nodes[i].index << ds.nodes[i].depth;
+                const uint64_t hi = (uint64_t)(uint32_t)(ds.nodes[i].index + 1u) << ds.nodes[i].depth;
+                if (q >= hi && i == ds.count - 1) break;
+                if (q >= lo && q < hi) {
+                    c = i;
+                    break;
+                }
+            }
+            SeedStart& st = starts[k];
+            if (c < 0) {  // SeedNotDisclosed for this epoch, ordered before its hashing errors
+                std::memset(&st, 0, sizeof st);
+                host_err = std::min<unsigned long long>(host_err, (unsigned long long)k << 1);
+                continue;
+            }
+            std::memcpy(st.value, ds.nodes[c].value, 16);
+            st.rel = q - (uint32_t)((uint64_t)ds.nodes[c].index << ds.nodes[c].depth);
+            st.depth = ds.nodes[c].depth;
+        }
+    } else {
+        rc = parse_ds(b->ds, b->ds_len, b->ds_capacity, ds, err);
+        if (rc) return rc;
+    }
     P.uniform = is_uniform(b);
     uint64_t n_entries = P.uniform ? (uint64_t)b->n_epochs * b->n2 : b->epoch_starts[b->n_epochs];
     if (b->epoch_starts && b->epoch_starts[0] != 0)
@@ -223,10 +262,19 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     }
 
     mark(ctx, kEvSeed);
-    unsigned long long init = ~0ull;
-    CU(cudaMemcpyAsync(d_err, &init, 8, cudaMemcpyHostToDevice, s));
+    ctx->stage->err_init = host_err;
+    CU(cudaMemcpyAsync(d_err, &ctx->stage->err_init, 8, cudaMemcpyHostToDevice, s));
     if (n_ep) CU(cudaMemcpyAsync(d_epochs, b->epochs, (size_t)n_ep * 4, cudaMemcpyHostToDevice, s));
-    launch_seed_derive(b->suite, ds, d_epochs, n_ep, d_x0, d_err, ctx->d_t0, s);
+    if (b->ds_offsets) {
+        SeedStart* d_starts;
+        ENSURE(b_starts_ds, std::max<size_t>(starts.size(), 1), d_starts);
+        if (n_ep) CU(cudaMemcpyAsync(d_starts, starts.data(), starts.size() * sizeof(SeedStart),
+                                     cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));  // `starts` is a host vector
+        launch_seed_walk(b->suite, d_starts, n_ep, d_x0, ctx->d_t0, s);
+    } else {
+        launch_seed_derive(b->suite, ds, d_epochs, n_ep, d_x0, d_err, ctx->d_t0, s);
+    }
     ctx->launches += n_ep ? 1 : 0;
     mark(ctx, kEvHash);
 
@@ -528,7 +576,8 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_scratch, &ctx->b_tiles, &ctx->b_starts, &ctx->b_tbegin, &ctx->b_err,
                       &ctx->b_flags, &ctx->b_payload, &ctx->b_offsets, &ctx->b_e, &ctx->b_s,
                       &ctx->b_r, &ctx->b_enc, &ctx->b_verdict, &ctx->b_mask, &ctx->b_seg, &ctx->b_y,
-                      &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre};
+                      &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
+                      &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
@@ -699,6 +748,103 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     if (rc) return rc;
     if (e_tilde_out && b->n_epochs)
         CU(cudaMemcpy(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost));
+    finish_timing(ctx);
+    return ok(err);
+}
+
+// Masked segmented folds on device buffers (scalars: n x 8 limbs; points:
+// n x 32 B encodings); results to host. mask: keep item k iff mask[k] != 0.
+static int segfold_dev(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_s, const uint8_t* d_r, const uint8_t* d_mask,
+                const uint32_t* seg, uint32_t n_seg, uint8_t* out_s, uint8_t* out_r, poslo_error* err) {
+    if (!n_seg) return POSLO_OK;
+    for (uint32_t g = 0; g < n_seg; g++)
+        if (seg[g] > seg[g + 1] || seg[g + 1] > n)
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "segments must be non-decreasing within [0, n]");
+    cudaStream_t s = ctx->stream;
+    if (d_s && out_s) {
+        std::vector<uint64_t> seg64(seg, seg + n_seg + 1);
+        uint64_t* d_seg;
+        uint32_t* d_out;
+        UPLOAD(b_seg, seg64.data(), seg64.size() * 8, d_seg);
+        ENSURE(b_out_s, (size_t)n_seg * 8, d_out);
+        launch_segsum_mod_l(d_s, d_seg, n_seg, d_mask, d_out, s, /*skip_val=*/0);
+        ctx->launches += 1;
+        CU(cudaMemcpyAsync(out_s, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, s));
+    }
+    if (d_r && out_r) {
+        uint32_t* d_seg;
+        uint8_t* d_out;
+        int* d_bad;
+        UPLOAD(b_seg32, seg, (size_t)(n_seg + 1) * 4, d_seg);
+        ENSURE(b_out_r, (size_t)n_seg * 32, d_out);
+        ENSURE(b_flags, 4, d_bad);
+        CU(cudaMemsetAsync(d_bad, 0, 4, s));
+        launch_segfold_points(d_r, d_seg, n_seg, d_mask, d_out, d_bad, s);
+        ctx->launches += 1;
+        CU(cudaMemcpyAsync(out_r, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(ctx->stage->flags, d_bad, 4, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (ctx->stage->flags[0]) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    }
+    CU(cudaStreamSynchronize(s));
+    return POSLO_OK;
+}
+
+int poslo_gpu_segfold(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* scalars, const uint8_t* points,
+                      const uint8_t* mask, const uint32_t* seg, uint32_t n_seg, uint8_t* out_s, uint8_t* out_r,
+                      poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (n_seg && !seg) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null segments");
+    Guard g(ctx);
+    uint32_t* d_s = nullptr;
+    uint8_t* d_r = nullptr;
+    uint8_t* d_mask = nullptr;
+    if (scalars && out_s) UPLOAD(b_s, scalars, (size_t)std::max<uint32_t>(n, 1) * 32, d_s);
+    if (points && out_r) UPLOAD(b_r, points, (size_t)std::max<uint32_t>(n, 1) * 32, d_r);
+    if (mask) UPLOAD(b_mask, mask, std::max<uint32_t>(n, 1), d_mask);
+    int rc = segfold_dev(ctx, n, d_s, d_r, d_mask, seg, n_seg, out_s, out_r, err);
+    if (rc) return rc;
+    return ok(err);
+}
+
+int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
+                             const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg, uint32_t n_seg,
+                             uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !y || (b->n_epochs && (!s_hats || !r_hats || !verdicts)) || (n_seg && !seg))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    Guard g(ctx);
+    // aver (poslo_c.cpp:195-197): every epoch must hold exactly n2 entries
+    if (b->epoch_starts)
+        for (uint32_t k = 0; k < b->n_epochs; k++)
+            if (b->epoch_starts[k + 1] - b->epoch_starts[k] != b->n2)
+                return set_err(err, POSLO_STATE_ERROR, b->epochs[k], "every batch must hold exactly n2 entries");
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    const uint32_t n = b->n_epochs;
+    if (!n) return ok(err);
+    uint32_t* d_s;
+    uint8_t* d_r;
+    UPLOAD(b_s, s_hats, (size_t)n * 32, d_s);
+    UPLOAD(b_r, r_hats, (size_t)n * 32, d_r);
+    mark(ctx, kEvGroup);
+    // per-epoch verdicts stay on the device as the fold mask
+    int* d_flags;
+    uint8_t* d_verdict;
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    rc = ensure_tables(ctx, y, d_flags, err, n > kCtaCheckMax);
+    if (rc) return rc;
+    ENSURE(b_verdict, n, d_verdict);
+    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s, d_r,
+                            nullptr, d_verdict, ctx->stream);
+    ctx->launches += 1;
+    CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = segfold_dev(ctx, n, d_s, d_r, d_verdict, seg, n_seg, seg_s, seg_r, err);
+    if (rc) return rc;
     finish_timing(ctx);
     return ok(err);
 }

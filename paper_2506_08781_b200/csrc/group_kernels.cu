@@ -302,7 +302,41 @@ __global__ void __launch_bounds__(64) k_check_post(const gcached* __restrict__ t
     if (threadIdx.x == 0) verdict[0] = (pre->ok && rist_equal(E, pre->T)) ? 1 : 0;
 }
 
+// Masked segmented fold: CTA g folds the valid points of [seg[g], seg[g+1]).
+__global__ void __launch_bounds__(128) k_segfold_points(const uint8_t* __restrict__ pts,
+                                                        const uint32_t* __restrict__ seg,
+                                                        const uint8_t* __restrict__ mask,
+                                                        uint8_t* __restrict__ out, int* bad) {
+    __shared__ gpt sh[128];
+    const uint32_t g = blockIdx.x, lo = seg[g], hi = seg[g + 1];
+    gpt acc = pt_identity();
+    for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+        if (mask && !mask[k]) continue;
+        uint8_t b[32];
+        load32(pts + (size_t)k * 32, b);
+        gpt P;
+        if (!rist_decode(b, P)) {
+            atomicOr(bad, 1);
+            continue;
+        }
+        acc = pt_add(acc, P);
+    }
+    block_reduce_pt(acc, sh);
+    if (threadIdx.x == 0) {
+        uint8_t o[32];
+        rist_encode(acc, o);
+#pragma unroll
+        for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
+    }
+}
+
 }  // namespace
+
+void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
+                           uint8_t* d_out, int* d_bad, cudaStream_t s) {
+    if (!n_seg) return;
+    k_segfold_points<<<n_seg, 128, 0, s>>>(d_pts, d_seg, d_mask, d_out, d_bad);
+}
 
 void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
                         const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict, int* d_ybad,

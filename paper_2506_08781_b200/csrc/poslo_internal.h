@@ -42,6 +42,15 @@ struct TileMap {
     uint32_t tile_count;  // 0 = all tiles
 };
 
+// Per-epoch seed stacks (poslo_batch.ds_offsets): walk `depth` levels from
+// the covering node's value along the low bits of rel.
+struct SeedStart {
+    uint32_t value[4];
+    uint32_t rel;
+    uint32_t depth;
+};
+void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d_x0, const uint32_t* d_t0,
+                      cudaStream_t s);
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s);
 
@@ -82,7 +91,8 @@ void launch_sum_mod_l(const uint32_t* d_items, int limbs, uint64_t n, const uint
 
 // Segmented variant: out[g] = sum of items [seg[g], seg[g+1]) (mask honoured).
 void launch_segsum_mod_l(const uint32_t* d_items, const uint64_t* d_seg, uint32_t n_groups,
-                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s);
+                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s,
+                         uint8_t skip_val = 1);
 
 // Batched commit_check: enc[i] = encode(Y^e_i * alpha^s_i); verdict[i] =
 // (enc[i] == r[i]) when r != nullptr. Y is decoded once (d_ybad set when Y
@@ -100,6 +110,10 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
                         cudaStream_t s);
 // commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,
 // thread-per-check above).
+// Masked segmented group_combine fold: one CTA per segment; out = encodings
+// (identity = zeros). *d_bad set when a point fails to decode.
+void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
+                           uint8_t* d_out, int* d_bad, cudaStream_t s);
 // Radix-256 tables (kComb256TableBytes) for the thread-per-check path.
 void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s);
 void launch_group_check_comb(const void* d_tabY, const void* d_tabB, const void* d_tabY256,

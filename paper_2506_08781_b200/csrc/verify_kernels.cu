@@ -97,6 +97,21 @@ __global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict_
     }
 }
 
+// K0 with per-epoch seed stacks: the host resolved each epoch's covering
+// node (value, offset below it, depth); one thread walks one epoch.
+__global__ void k_seed_walk(int suite, const SeedStart* __restrict__ starts, uint32_t n, uint4* __restrict__ x0,
+                            const uint32_t* __restrict__ t0g) {
+    extern __shared__ uint32_t sT0[];
+    if (suite != 1) load_t0(sT0, t0g);
+    SmemT0 t0{sT0, threadIdx.x & 31u};
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const SeedStart st = starts[k];
+    uint32_t x[4] = {st.value[0], st.value[1], st.value[2], st.value[3]};
+    ds_walk(suite, t0, x, st.rel, (int)st.depth);
+    x0[k] = make_uint4(x[0], x[1], x[2], x[3]);
+}
+
 // ---------------------------------------------------------------- generic K1+K2
 __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay, TileMap tm,
                                                       const uint4* __restrict__ x0,
@@ -231,14 +246,14 @@ __global__ void __launch_bounds__(256) k_sum_stage2(const uint32_t* __restrict__
 
 __global__ void __launch_bounds__(256) k_segsum(const uint32_t* __restrict__ items,
                                                 const uint64_t* __restrict__ seg,
-                                                const uint8_t* __restrict__ mask,
+                                                const uint8_t* __restrict__ mask, uint8_t skip_val,
                                                 uint32_t* __restrict__ out) {
     __shared__ uint32_t red[8 * 17];
     const uint32_t g = blockIdx.x;
     uint32_t acc[17];
     acc17_zero(acc);
     for (uint64_t i = seg[g] + threadIdx.x; i < seg[g + 1]; i += blockDim.x) {
-        if (mask && mask[i]) continue;
+        if (mask && mask[i] == skip_val) continue;
         uint32_t v[17];
         load_item(items, 8, i, v);
         acc17_add17(acc, v);
@@ -291,6 +306,15 @@ void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, 
     k_seed_derive<<<(groups + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, n_epochs, d_x0, d_err, d_t0);
 }
 
+void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d_x0, const uint32_t* d_t0,
+                      cudaStream_t s) {
+    if (!n) return;
+    int T = 64;
+    size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
+    if (smem) cudaFuncSetAttribute(k_seed_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_seed_walk<<<(n + T - 1) / T, T, smem, s>>>(suite, d_starts, n, d_x0, d_t0);
+}
+
 void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
                          uint32_t* d_partial, uint32_t* d_entry_e, unsigned long long* d_err,
                          const uint32_t* d_t0, cudaStream_t s) {
@@ -316,9 +340,9 @@ void launch_sum_mod_l(const uint32_t* d_items, int limbs, uint64_t n, const uint
 }
 
 void launch_segsum_mod_l(const uint32_t* d_items, const uint64_t* d_seg, uint32_t n_groups,
-                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s) {
+                         const uint8_t* d_mask, uint32_t* d_out, cudaStream_t s, uint8_t skip_val) {
     if (!n_groups) return;
-    k_segsum<<<n_groups, 256, 0, s>>>(d_items, d_seg, d_mask, d_out);
+    k_segsum<<<n_groups, 256, 0, s>>>(d_items, d_seg, d_mask, skip_val, d_out);
 }
 
 void launch_synth_fixed(uint64_t seed, uint64_t first, uint64_t n, uint32_t L, uint8_t* d_out,
