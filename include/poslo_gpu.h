@@ -83,6 +83,31 @@ typedef struct poslo_batch {
                                       semantics). NULL: one stack `ds` for every epoch. */
 } poslo_batch;
 
+/* Scheme F (POSLO-F, include/poslo/poslo_f.hpp) entries: each entry t has a
+ * one-time seed x_t, either the FineSignature seed tail (seeds[t], 16 B) or,
+ * where derive_slot[t] != UINT32_MAX, onetime_seed(sr(stack, slot_epochs[s]),
+ * j[t]) with s = derive_slot[t] and the slot's stack ds (ds_offsets: one
+ * stack per slot, else the one stack for all slots). Entry bytes as in
+ * poslo_batch (payload/offsets/entry_len). */
+typedef struct poslo_fine_batch {
+    uint8_t suite;
+    const uint8_t* payload;
+    uint64_t payload_bytes;
+    const uint64_t* offsets;       /* n_entries + 1, or NULL (fixed entry_len) */
+    uint32_t entry_len;
+    uint64_t n_entries;
+    int32_t device_resident;       /* payload/offsets in device memory */
+    const uint8_t* seeds;          /* n_entries x 16 B (host); may be NULL when every entry is derived */
+    const uint32_t* derive_slot;   /* n_entries (host) or NULL (all from seeds) */
+    const uint32_t* j;             /* n_entries (host): position in the epoch, for derived entries */
+    const uint32_t* slot_epochs;   /* n_slots epoch indices (host) */
+    uint32_t n_slots;
+    const uint8_t* ds;             /* SeedStack wire bytes (host) */
+    uint32_t ds_len;
+    uint32_t ds_capacity;
+    const uint64_t* ds_offsets;    /* n_slots + 1 (host) or NULL */
+} poslo_fine_batch;
+
 /* ---- context -------------------------------------------------------------- */
 int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);
 void poslo_gpu_destroy(poslo_gpu_ctx* ctx);
@@ -158,6 +183,23 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* batch, const
 int poslo_gpu_segfold(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* scalars, const uint8_t* points,
                       const uint8_t* mask, const uint32_t* seg, uint32_t n_seg, uint8_t* out_s,
                       uint8_t* out_r, poslo_error* err);
+
+/* ---- scheme F (poslo_f.cpp:223-246, distiller.cpp:91-129) --------------------
+ * Errors in entry order (the reference loops entries ascending): for entry t,
+ * SeedNotDisclosed (err->epoch = its epoch) when its derived seed's stack
+ * does not cover the epoch, then FormatError (suite 3, L > 31; err->epoch =
+ * t). fine_scalars: e_out n x 32 B LE (hash_to_scalar(m_t, x_t)), e_sum the
+ * sum mod l; either may be NULL. fine_verify: verdicts[t] =
+ * (commit_check(Y, e_t, s[t]) == r[t]) — aver_f_single per entry / the
+ * per-entry checks of distill_epoch_fine. aver_f_batch: *verdict =
+ * (commit_check(Y, sum e_t, s) == r) with every seed derived (x_t =
+ * onetime_seed(sr(ds, t / n2), t % n2)). */
+int poslo_gpu_fine_scalars(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint8_t* e_out, uint8_t* e_sum,
+                           poslo_error* err);
+int poslo_gpu_fine_verify(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const uint8_t y[32],
+                          const uint8_t* s, const uint8_t* r, uint8_t* verdicts, poslo_error* err);
+int poslo_gpu_aver_f_batch(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const uint8_t y[32],
+                           const uint8_t s[32], const uint8_t r[32], uint8_t* verdict, poslo_error* err);
 
 /* ---- group primitives (group.cpp), batched on the device ----------------------
  * commit_check: out[i] = encode(Y^e[i] * alpha^s[i]) (group.cpp:144-167).

@@ -9,6 +9,12 @@
 //                                      signer (kg/sig_epoch) with deterministic
 //                                      randombytes, plus every verifier output
 //                                      the GPU path must reproduce, JSON
+//   ref_tool golden_f S N1 N2 NU LEN SEED BPV_V BPV_K [TAMPER...]
+//                                      one signed fine-grained (POSLO-F) stream from
+//                                      the real signer (kg/sig_one) with every
+//                                      scheme-F verifier output: aver_f_single per
+//                                      entry, aver_f_batch (all / a subset), fine
+//                                      distillation CCD + SeBVer V/U/I, JSON
 //   ref_tool bench S LOG2N N2 LEN WORKERS SEED REPS [MODE]
 //                                      times reference paver (MODE=coarse) or
 //                                      the per-epoch aver loop sharded over
@@ -29,6 +35,7 @@
 #include "../../include/poslo_synth.h"
 #include "poslo/batch_verify.hpp"
 #include "poslo/distiller.hpp"
+#include "poslo/poslo_f.hpp"
 
 using namespace poslo;
 
@@ -313,6 +320,99 @@ int cmd_golden(int argc, char** argv) {
     return 0;
 }
 
+// ---- golden_f (scheme F) ---------------------------------------------------
+int cmd_golden_f(int argc, char** argv) {
+    if (argc < 10) return 2;
+    SuiteConfig suite{static_cast<SuiteId>(std::atoi(argv[2])), uint32_t(std::atoi(argv[3])),
+                      uint32_t(std::atoi(argv[4])), uint32_t(std::atoi(argv[5]))};
+    int len = std::atoi(argv[6]);
+    uint64_t seed = std::strtoull(argv[7], nullptr, 0);
+    uint32_t bv = uint32_t(std::atoi(argv[8])), bk = uint32_t(std::atoi(argv[9]));
+    std::vector<uint64_t> tampers;
+    for (int a = 10; a < argc; a++) tampers.push_back(std::strtoull(argv[a], nullptr, 0));
+    g_rb_state = seed;
+    std::mt19937_64 rng(seed ^ 0xf1f1ULL);
+    auto [sk, pk] = PoslofSecretKey::kg(suite, bv, bk);
+    std::map<uint32_t, std::vector<Bytes>> msgs;
+    std::vector<FineSignature> sigs;
+    for (uint32_t i = 0; i < suite.n1; i++) {
+        std::vector<Bytes> epoch;
+        for (uint32_t j = 0; j < suite.n2; j++) {
+            size_t l = len > 0 ? size_t(len) : 1 + rng() % (suite.suite == SuiteId::MmoAddQ ? 31 : 64);
+            Bytes b(l);
+            for (auto& x : b) x = uint8_t(rng());
+            sigs.push_back(sk.sig_one(b));
+            epoch.push_back(std::move(b));
+        }
+        msgs.emplace(i, std::move(epoch));
+    }
+    for (uint64_t t : tampers) msgs.at(uint32_t(t / suite.n2))[t % suite.n2][0] ^= 0x01;
+    std::printf("{\n\"scheme\": \"F\", \"suite\": %d, \"n1\": %u, \"n2\": %u, \"n_u\": %u, \"seed\": %llu,\n",
+                int(suite.suite), suite.n1, suite.n2, suite.n_u, (unsigned long long)seed);
+    std::printf("\"bpv\": [%u, %u], \"tampered_entries\": [", bv, bk);
+    for (size_t k = 0; k < tampers.size(); k++)
+        std::printf("%s%llu", k ? "," : "", (unsigned long long)tampers[k]);
+    std::printf("],\n\"pk\": \"%s\",\n\"sigs\": [", hexv(pk.serialize()).c_str());
+    for (size_t t = 0; t < sigs.size(); t++) std::printf("%s\"%s\"", t ? "," : "", hexv(sigs[t].serialize()).c_str());
+    std::printf("],\n\"entries\": [");
+    bool first = true;
+    for (auto& [i, v] : msgs)
+        for (auto& m : v) { std::printf("%s\"%s\"", first ? "" : ",", hexv(m).c_str()); first = false; }
+    std::printf("],\n");
+    // aver_f_single per entry (entries carrying ds raise FormatError: -1)
+    std::printf("\"single\": [");
+    for (size_t t = 0; t < sigs.size(); t++) {
+        int v;
+        try {
+            v = aver_f_single(pk, msgs.at(uint32_t(t / suite.n2))[t % suite.n2], sigs[t]) ? 1 : 0;
+        } catch (const FormatError&) {
+            v = -1;
+        }
+        std::printf("%s%d", t ? "," : "", v);
+    }
+    // aver_f_batch over every entry and over every third entry, final ds
+    const SeedStack& ds = std::get<SeedStack>(sigs.back().tail);
+    Bytes dsw;
+    ds.serialize(dsw);
+    auto batch = [&](uint32_t stride, uint32_t off) {
+        std::map<uint32_t, Bytes> ents;
+        Scalar s;
+        GroupElement r;
+        for (uint32_t t = off; t < sigs.size(); t += stride) {
+            ents.emplace(t, msgs.at(t / suite.n2)[t % suite.n2]);
+            s = s.add(sigs[t].s);
+            r = group_combine(r, sigs[t].r);
+        }
+        bool ok = aver_f_batch(pk, ents, s, r, ds);
+        std::printf("{\"stride\": %u, \"offset\": %u, \"s\": \"%s\", \"r\": \"%s\", \"ok\": %d}", stride, off,
+                    hexv(s.le_bytes()).c_str(), hexv(r.bytes()).c_str(), ok ? 1 : 0);
+    };
+    std::printf("],\n\"ds\": \"%s\",\n\"batch\": [", hexv(dsw).c_str());
+    batch(1, 0);
+    std::printf(", ");
+    batch(3, 1);
+    std::printf("],\n");
+    // fine distillation + SeBVer
+    ColdCryptoData ccd(CcdScheme::Fine, suite);
+    for (uint32_t i = 0; i < suite.n1; i++) {
+        std::vector<FineSignature> es(sigs.begin() + i * suite.n2, sigs.begin() + (i + 1) * suite.n2);
+        ccd.distill_epoch_fine(pk, msgs.at(i), es);
+    }
+    ccd.finalize();
+    std::printf("\"invalid_entries\": [");
+    for (size_t k = 0; k < ccd.invalid().size(); k++) std::printf("%s%u", k ? "," : "", ccd.invalid()[k].index);
+    std::printf("],\n\"ccd\": \"%s\",\n", hexv(ccd.serialize()).c_str());
+    if (ccd.has_valid()) {
+        print_bits("sebver_V", ccd.sebver(pk.y, msgs, SebverMode::V));
+        std::printf(",\n");
+    }
+    print_bits("sebver_U", ccd.sebver(pk.y, msgs, SebverMode::U));
+    std::printf(",\n");
+    print_bits("sebver_I", ccd.sebver(pk.y, msgs, SebverMode::I));
+    std::printf("\n}\n");
+    return 0;
+}
+
 // ---- bench ---------------------------------------------------------------
 int cmd_bench(int argc, char** argv) {
     if (argc < 9) return 2;
@@ -431,6 +531,7 @@ int main(int argc, char** argv) {
     try {
         if (cmd == "kat") return cmd_kat();
         if (cmd == "golden") return cmd_golden(argc, argv);
+        if (cmd == "golden_f") return cmd_golden_f(argc, argv);
         if (cmd == "bench") return cmd_bench(argc, argv);
     } catch (std::exception& e) {
         std::fprintf(stderr, "ref_tool: %s\n", e.what());

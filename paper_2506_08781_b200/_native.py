@@ -39,13 +39,35 @@ class PosloBatch(ctypes.Structure):
     ]
 
 
+class PosloFineBatch(ctypes.Structure):
+    _fields_ = [
+        ("suite", ctypes.c_uint8),
+        ("payload", ctypes.c_void_p),
+        ("payload_bytes", ctypes.c_uint64),
+        ("offsets", ctypes.c_void_p),
+        ("entry_len", ctypes.c_uint32),
+        ("n_entries", ctypes.c_uint64),
+        ("device_resident", ctypes.c_int32),
+        ("seeds", ctypes.c_void_p),
+        ("derive_slot", ctypes.c_void_p),
+        ("j", ctypes.c_void_p),
+        ("slot_epochs", ctypes.c_void_p),
+        ("n_slots", ctypes.c_uint32),
+        ("ds", ctypes.c_void_p),
+        ("ds_len", ctypes.c_uint32),
+        ("ds_capacity", ctypes.c_uint32),
+        ("ds_offsets", ctypes.c_void_p),
+    ]
+
+
 EXPORTS = [
     "poslo_gpu_create", "poslo_gpu_destroy", "poslo_gpu_set_stream", "poslo_gpu_enable_timing",
     "poslo_gpu_last_timings", "poslo_gpu_last_launches", "poslo_gpu_version", "poslo_gpu_agg_ekeys",
     "poslo_gpu_paver", "poslo_gpu_epoch_verify", "poslo_gpu_sebver", "poslo_gpu_commit_check",
     "poslo_gpu_group_fold", "poslo_gpu_point_valid", "poslo_gpu_seed_retrieve",
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
-    "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold",
+    "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold", "poslo_gpu_fine_scalars",
+    "poslo_gpu_fine_verify", "poslo_gpu_aver_f_batch",
 ]
 
 _lib = None
@@ -65,6 +87,7 @@ def load():
     P = c.c_void_p
     E = c.POINTER(PosloError)
     B = c.POINTER(PosloBatch)
+    F = c.POINTER(PosloFineBatch)
     sig = {
         "poslo_gpu_create": ([c.c_int, c.POINTER(c.c_void_p), E], c.c_int),
         "poslo_gpu_destroy": ([P], None),
@@ -90,6 +113,9 @@ def load():
         "poslo_gpu_synth_varlog": ([P, c.c_uint64, c.c_uint64, c.c_uint64, P, P, E], c.c_int),
         "poslo_gpu_distill_coarse": ([P, B, P, P, P, P, c.c_uint32, P, P, P, E], c.c_int),
         "poslo_gpu_segfold": ([P, c.c_uint32, P, P, P, P, c.c_uint32, P, P, E], c.c_int),
+        "poslo_gpu_fine_scalars": ([P, F, P, P, E], c.c_int),
+        "poslo_gpu_fine_verify": ([P, F, P, P, P, P, E], c.c_int),
+        "poslo_gpu_aver_f_batch": ([P, F, P, P, P, P, E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -149,6 +149,54 @@ int parse_ds(const uint8_t* w, uint32_t n, uint32_t cap, DsParam& ds, poslo_erro
     return POSLO_OK;
 }
 
+// sr (seed_manager.cpp:71-85) resolved on the host for per-epoch stacks:
+// for every queried epoch, its covering node in its own stack (ds_offsets,
+// or the one stack `ds` when ds_offsets == NULL). Undisclosed epochs get a
+// zero start and lower *host_err to (k << 1) (or (first_entry[k] << 1)).
+int resolve_seed_starts(const uint8_t* ds_w, uint32_t ds_len, const uint64_t* ds_offsets, uint32_t cap,
+                        const uint32_t* epochs, uint32_t n, std::vector<SeedStart>& starts,
+                        const uint64_t* first_entry, unsigned long long* host_err, poslo_error* err) {
+    starts.resize(n);
+    DsParam ds;
+    if (!ds_offsets) {
+        int rc = parse_ds(ds_w, ds_len, cap, ds, err);
+        if (rc) return rc;
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        if (ds_offsets) {
+            const uint64_t o0 = ds_offsets[k], o1 = ds_offsets[k + 1];
+            if (o1 < o0 || o1 > ds_len) return set_err(err, POSLO_INVALID_ARGUMENT, epochs[k], "bad ds_offsets");
+            int rc = parse_ds(ds_w + o0, (uint32_t)(o1 - o0), cap, ds, err);
+            if (rc) {
+                if (err) err->epoch = epochs[k];
+                return rc;
+            }
+        }
+        const uint32_t q = epochs[k];
+        int c = -1;
+        for (int i = ds.count - 1; i >= 0; i--) {
+            const uint64_t lo = (uint64_t)ds.nodes[i].index << ds.nodes[i].depth;
+            const uint64_t hi = (uint64_t)(uint32_t)(ds.nodes[i].index + 1u) << ds.nodes[i].depth;
+            if (q >= hi && i == ds.count - 1) break;
+            if (q >= lo && q < hi) {
+                c = i;
+                break;
+            }
+        }
+        SeedStart& st = starts[k];
+        if (c < 0) {  // SeedNotDisclosed, ordered before the hashing errors of the same position
+            std::memset(&st, 0, sizeof st);
+            const unsigned long long pos = first_entry ? first_entry[k] : k;
+            *host_err = std::min<unsigned long long>(*host_err, pos << 1);
+            continue;
+        }
+        std::memcpy(st.value, ds.nodes[c].value, 16);
+        st.rel = q - (uint32_t)((uint64_t)ds.nodes[c].index << ds.nodes[c].depth);
+        st.depth = ds.nodes[c].depth;
+    }
+    return POSLO_OK;
+}
+
 struct Prepared {
     EntryLayout lay{};
     TileMap tm{};
@@ -181,38 +229,9 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     std::vector<SeedStart> starts;  // per-epoch stacks: resolved covering nodes
     unsigned long long host_err = ~0ull;
     if (b->ds_offsets) {
-        starts.resize(b->n_epochs);
-        for (uint32_t k = 0; k < b->n_epochs; k++) {
-            const uint64_t o0 = b->ds_offsets[k], o1 = b->ds_offsets[k + 1];
-            if (o1 < o0 || o1 > b->ds_len)
-                return set_err(err, POSLO_INVALID_ARGUMENT, b->epochs[k], "bad ds_offsets");
-            rc = parse_ds(b->ds + o0, (uint32_t)(o1 - o0), b->ds_capacity, ds, err);
-            if (rc) {
-                if (err) err->epoch = b->epochs[k];
-                return rc;
-            }
-            // sr (seed_manager.cpp:71-85): top of the stack down
-            const uint32_t q = b->epochs[k];
-            int c = -1;
-            for (int i = ds.count - 1; i >= 0; i--) {
-                const uint64_t lo = (uint64_t)ds.nodes[i].index << ds.nodes[i].depth;
-                const uint64_t hi = (uint64_t)(uint32_t)(ds.nodes[i].index + 1u) << ds.nodes[i].depth;
-                if (q >= hi && i == ds.count - 1) break;
-                if (q >= lo && q < hi) {
-                    c = i;
-                    break;
-                }
-            }
-            SeedStart& st = starts[k];
-            if (c < 0) {  // SeedNotDisclosed for this epoch, ordered before its hashing errors
-                std::memset(&st, 0, sizeof st);
-                host_err = std::min<unsigned long long>(host_err, (unsigned long long)k << 1);
-                continue;
-            }
-            std::memcpy(st.value, ds.nodes[c].value, 16);
-            st.rel = q - (uint32_t)((uint64_t)ds.nodes[c].index << ds.nodes[c].depth);
-            st.depth = ds.nodes[c].depth;
-        }
+        rc = resolve_seed_starts(b->ds, b->ds_len, b->ds_offsets, b->ds_capacity, b->epochs, b->n_epochs, starts,
+                                 nullptr, &host_err, err);
+        if (rc) return rc;
     } else {
         rc = parse_ds(b->ds, b->ds_len, b->ds_capacity, ds, err);
         if (rc) return rc;
@@ -846,6 +865,154 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
     rc = segfold_dev(ctx, n, d_s, d_r, d_verdict, seg, n_seg, seg_s, seg_r, err);
     if (rc) return rc;
     finish_timing(ctx);
+    return ok(err);
+}
+
+// ---- scheme F ----------------------------------------------------------------
+// Per-entry scalars of a fine batch into device memory (d_e: n x 8 limbs).
+static int fine_scalars_dev(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint32_t** d_e_out, poslo_error* err) {
+    if (!fb) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null batch");
+    if (fb->suite < 1 || fb->suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
+    const uint64_t n = fb->n_entries;
+    if (n >= (1ull << 62)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "too many entries");
+    if (n && !fb->derive_slot && !fb->seeds) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null seeds");
+    if (fb->derive_slot && (!fb->j || (fb->n_slots && !fb->slot_epochs)))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "derived seeds need j and slot_epochs");
+    cudaStream_t s = ctx->stream;
+    // seeds of derived entries: host-resolved covers, one walk per slot
+    std::vector<uint64_t> first(fb->n_slots, ~0ull);
+    if (fb->derive_slot)
+        for (uint64_t t = 0; t < n; t++) {
+            const uint32_t sl = fb->derive_slot[t];
+            if (sl == 0xFFFFFFFFu) continue;
+            if (sl >= fb->n_slots) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "derive_slot out of range");
+            first[sl] = std::min<uint64_t>(first[sl], t);
+        }
+    unsigned long long host_err = ~0ull;
+    std::vector<SeedStart> starts;
+    uint4* d_x0 = nullptr;
+    if (fb->derive_slot && fb->n_slots) {
+        int rc = resolve_seed_starts(fb->ds, fb->ds_len, fb->ds_offsets, fb->ds_capacity, fb->slot_epochs, fb->n_slots,
+                                     starts, first.data(), &host_err, err);
+        if (rc) return rc;
+        for (uint32_t k = 0; k < fb->n_slots; k++)  // slots no entry uses cannot fail
+            if (first[k] == ~0ull && host_err == (~0ull << 1)) host_err = ~0ull;
+        SeedStart* d_starts;
+        ENSURE(b_starts_ds, fb->n_slots, d_starts);
+        ENSURE(b_x0, fb->n_slots, d_x0);
+        CU(cudaMemcpyAsync(d_starts, starts.data(), starts.size() * sizeof(SeedStart), cudaMemcpyHostToDevice, s));
+        launch_seed_walk(fb->suite, d_starts, fb->n_slots, d_x0, ctx->d_t0, s);
+        ctx->launches += 1;
+    }
+    // entries
+    EntryLayout lay{};
+    lay.entry_len = fb->entry_len;
+    if (fb->device_resident) {
+        lay.payload = fb->payload;
+        lay.offsets = fb->offsets;
+    } else {
+        uint8_t* d_pay;
+        ENSURE(b_payload, fb->payload_bytes, d_pay);
+        if (fb->payload_bytes) CU(cudaMemcpyAsync(d_pay, fb->payload, fb->payload_bytes, cudaMemcpyHostToDevice, s));
+        lay.payload = d_pay;
+        if (fb->offsets) {
+            uint64_t* d_off;
+            ENSURE(b_offsets, n + 1, d_off);
+            CU(cudaMemcpyAsync(d_off, fb->offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+            lay.offsets = d_off;
+        }
+    }
+    uint4* d_seeds = nullptr;
+    uint32_t *d_slot = nullptr, *d_j = nullptr, *d_e;
+    unsigned long long* d_err;
+    if (fb->seeds) UPLOAD(b_pts, fb->seeds, (size_t)std::max<uint64_t>(n, 1) * 16, d_seeds);
+    if (fb->derive_slot) {
+        UPLOAD(b_epochs, fb->derive_slot, (size_t)std::max<uint64_t>(n, 1) * 4, d_slot);
+        UPLOAD(b_tbegin, fb->j, (size_t)std::max<uint64_t>(n, 1) * 4, d_j);
+    }
+    ENSURE(b_e, (size_t)std::max<uint64_t>(n, 1) * 8, d_e);
+    ENSURE(b_err, 1, d_err);
+    ctx->stage->err_init = host_err;
+    CU(cudaMemcpyAsync(d_err, &ctx->stage->err_init, 8, cudaMemcpyHostToDevice, s));
+    launch_fine_scalars(fb->suite, lay, n, d_seeds, d_slot, d_j, d_x0, d_e, d_err, ctx->d_t0, s);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&ctx->stage->err_key, d_err, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const unsigned long long key = ctx->stage->err_key;
+    if (key != ~0ull) {
+        const uint64_t t = key >> 1;
+        if ((key & 1) == 0) {
+            const uint32_t ep = fb->derive_slot && t < n && fb->derive_slot[t] < fb->n_slots
+                                    ? fb->slot_epochs[fb->derive_slot[t]] : 0;
+            return set_err(err, POSLO_SEED_NOT_DISCLOSED, ep, "seed for epoch %u not yet disclosed", ep);
+        }
+        return set_err(err, POSLO_FORMAT_ERROR, (uint32_t)t, "modular-addition hash: entry too long for this suite");
+    }
+    *d_e_out = d_e;
+    return POSLO_OK;
+}
+
+int poslo_gpu_fine_scalars(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint8_t* e_out, uint8_t* e_sum,
+                           poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    Guard g(ctx);
+    uint32_t* d_e;
+    int rc = fine_scalars_dev(ctx, fb, &d_e, err);
+    if (rc) return rc;
+    if (e_sum) {
+        uint32_t *d_sum, *d_scr;
+        ENSURE(b_sum, 8, d_sum);
+        ENSURE(b_scratch, 17 * 1024, d_scr);
+        launch_sum_mod_l(d_e, 8, fb->n_entries, nullptr, d_sum, d_scr, ctx->stream);
+        ctx->launches += 2;
+        CU(cudaMemcpyAsync(e_sum, d_sum, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (e_out && fb->n_entries)
+        CU(cudaMemcpyAsync(e_out, d_e, fb->n_entries * 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
+int poslo_gpu_fine_verify(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const uint8_t y[32], const uint8_t* s,
+                          const uint8_t* r, uint8_t* verdicts, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!fb || !y || (fb->n_entries && (!s || !r || !verdicts)))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    if (fb->n_entries > 0xFFFFFFFFull) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "too many entries");
+    Guard g(ctx);
+    uint32_t* d_e;
+    int rc = fine_scalars_dev(ctx, fb, &d_e, err);
+    if (rc) return rc;
+    const uint32_t n = (uint32_t)fb->n_entries;
+    if (!n) return ok(err);
+    uint32_t* d_s;
+    uint8_t* d_r;
+    UPLOAD(b_s, s, (size_t)n * 32, d_s);
+    UPLOAD(b_r, r, (size_t)n * 32, d_r);
+    rc = group_check_dev(ctx, y, n, d_e, d_s, d_r, verdicts, nullptr, err);
+    if (rc) return rc;
+    return ok(err);
+}
+
+int poslo_gpu_aver_f_batch(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const uint8_t y[32], const uint8_t s[32],
+                           const uint8_t r[32], uint8_t* verdict, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!fb || !y || !s || !r || !verdict) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    Guard g(ctx);
+    uint32_t* d_e;
+    int rc = fine_scalars_dev(ctx, fb, &d_e, err);
+    if (rc) return rc;
+    uint32_t *d_sum, *d_scr, *d_s;
+    uint8_t* d_r;
+    ENSURE(b_sum, 8, d_sum);
+    ENSURE(b_scratch, 17 * 1024, d_scr);
+    launch_sum_mod_l(d_e, 8, fb->n_entries, nullptr, d_sum, d_scr, ctx->stream);  // empty: e_sum = 0
+    ctx->launches += 2;
+    UPLOAD(b_s, s, 32, d_s);
+    UPLOAD(b_r, r, 32, d_r);
+    rc = group_check_dev(ctx, y, 1, d_sum, d_s, d_r, verdict, nullptr, err);
+    if (rc) return rc;
     return ok(err);
 }
 

@@ -54,12 +54,9 @@ struct OtsMsg {  // x0 || be32(j) (AES suites)
     }
 };
 
-// Per-entry contribution as a 512-bit integer (16 limbs); false on a
-// suite-3 over-length entry (primitives.cpp:179-181).
+// x = onetime_seed(x0, j) (primitives.cpp:209-223) as little-endian memory words.
 template <class T0>
-PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L,
-                            const uint32_t x0m[4], uint32_t j, uint32_t limbs[16]) {
-    uint32_t x[4];
+PHD void entry_seed(int suite, const T0& t0, const uint32_t x0m[4], uint32_t j, uint32_t x[4]) {
     if (suite == 1) {
         const uint32_t x0w[4] = {bswap32(x0m[0]), bswap32(x0m[1]), bswap32(x0m[2]), bswap32(x0m[3])};
         uint32_t pre[8], xw[4];
@@ -71,6 +68,14 @@ PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L,
         OtsMsg om{{x0m[0], x0m[1], x0m[2], x0m[3]}, j};
         mmo_hash_dev(t0, om, 20, x);
     }
+}
+
+// hash_to_scalar(m, x) (primitives.cpp:149-193) for a given one-time seed x
+// (memory words) as a raw 512-bit integer (16 limbs); false on a suite-3
+// over-length entry (:179-181). Scheme F's aver_f_single supplies x directly.
+template <class T0>
+PHD bool entry_limbs_x(int suite, const T0& t0, const uint8_t* m, uint32_t L, const uint32_t x[4],
+                       uint32_t limbs[16]) {
     if (suite == 3) {
         if (L > 31) return false;
         // (int_be(m) + int_be(x)) < 2^248 + 2^128 < l: no reduction needed
@@ -120,6 +125,14 @@ PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L,
     return true;
 }
 
+// Per-entry contribution e(m, onetime_seed(x0, j)) as 16 limbs (agg_ekeys).
+template <class T0>
+PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L, const uint32_t x0m[4], uint32_t j,
+                     uint32_t limbs[16]) {
+    uint32_t x[4];
+    entry_seed(suite, t0, x0m, j, x);
+    return entry_limbs_x(suite, t0, m, L, x, limbs);
+}
 
 // ---- fast path, suite 1, 32-byte entry: m as 8 big-endian words, x0w the
 // epoch seed as big-endian words with its hoisted onetime_seed mid-state.

@@ -51,6 +51,11 @@ struct SeedStart {
 };
 void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d_x0, const uint32_t* d_t0,
                       cudaStream_t s);
+// Scheme F per-entry scalars mod l (8 limbs each): x from seeds[t], or
+// onetime_seed(x0[dslot[t]], j[t]) where dslot[t] != UINT32_MAX.
+void launch_fine_scalars(int suite, const EntryLayout& lay, uint64_t n, const uint4* d_seeds, const uint32_t* d_dslot,
+                         const uint32_t* d_j, const uint4* d_x0, uint32_t* d_e, unsigned long long* d_err,
+                         const uint32_t* d_t0, cudaStream_t s);
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s);
 

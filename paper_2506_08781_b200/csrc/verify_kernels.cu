@@ -112,6 +112,52 @@ __global__ void k_seed_walk(int suite, const SeedStart* __restrict__ starts, uin
     x0[k] = make_uint4(x[0], x[1], x[2], x[3]);
 }
 
+// Scheme F per-entry scalars (poslo_f.cpp:223-246, distiller.cpp:103-115):
+// e_t = hash_to_scalar(m_t, x_t) mod l, x_t the signature's seed tail or
+// onetime_seed(x0[slot_t], j_t) when the entry's seed is derived from a stack.
+__global__ void __launch_bounds__(128) k_fine_scalars(int suite, EntryLayout lay, uint64_t n,
+                                                      const uint4* __restrict__ seeds,
+                                                      const uint32_t* __restrict__ dslot,
+                                                      const uint32_t* __restrict__ jj,
+                                                      const uint4* __restrict__ x0,
+                                                      uint32_t* __restrict__ e_out,
+                                                      unsigned long long* err,
+                                                      const uint32_t* __restrict__ t0g) {
+    extern __shared__ uint32_t sT0[];
+    if (suite != 1) load_t0(sT0, t0g);
+    SmemT0 t0{sT0, threadIdx.x & 31u};
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint8_t* m;
+    uint32_t L;
+    if (lay.offsets) {
+        const uint64_t o0 = lay.offsets[t];
+        m = lay.payload + o0;
+        L = (uint32_t)(lay.offsets[t + 1] - o0);
+    } else {
+        m = lay.payload + t * lay.entry_len;
+        L = lay.entry_len;
+    }
+    uint32_t x[4];
+    if (dslot && dslot[t] != 0xFFFFFFFFu) {
+        const uint4 xr = __ldg(x0 + dslot[t]);
+        const uint32_t x0m[4] = {xr.x, xr.y, xr.z, xr.w};
+        entry_seed(suite, t0, x0m, jj[t], x);
+    } else {
+        const uint4 xr = __ldg(seeds + t);
+        x[0] = xr.x; x[1] = xr.y; x[2] = xr.z; x[3] = xr.w;
+    }
+    uint32_t limbs[16], e[8];
+    if (!entry_limbs_x(suite, t0, m, L, x, limbs)) {
+        err_min(err, (t << 1) | 1ull);  // FormatError (suite 3, L > 31)
+#pragma unroll
+        for (int k = 0; k < 16; k++) limbs[k] = 0;
+    }
+    sc_reduce_limbs(limbs, 16, e);
+#pragma unroll
+    for (int k = 0; k < 8; k++) e_out[t * 8 + k] = e[k];
+}
+
 // ---------------------------------------------------------------- generic K1+K2
 __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay, TileMap tm,
                                                       const uint4* __restrict__ x0,
@@ -313,6 +359,16 @@ void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d
     size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
     if (smem) cudaFuncSetAttribute(k_seed_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_seed_walk<<<(n + T - 1) / T, T, smem, s>>>(suite, d_starts, n, d_x0, d_t0);
+}
+
+void launch_fine_scalars(int suite, const EntryLayout& lay, uint64_t n, const uint4* d_seeds, const uint32_t* d_dslot,
+                         const uint32_t* d_j, const uint4* d_x0, uint32_t* d_e, unsigned long long* d_err,
+                         const uint32_t* d_t0, cudaStream_t s) {
+    if (!n) return;
+    size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
+    if (smem) cudaFuncSetAttribute(k_fine_scalars, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_fine_scalars<<<(unsigned)((n + 127) / 128), 128, smem, s>>>(suite, lay, n, d_seeds, d_dslot, d_j, d_x0, d_e,
+                                                                 d_err, d_t0);
 }
 
 void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,

@@ -95,14 +95,29 @@ class ColdCryptoData:
         batches = {i0 + k: list(m) for k, m in enumerate(msgs_list)}
         sig_of = {i0 + k: s for k, s in enumerate(sigs)}
         # umbrella pieces: cut where an epoch index is a multiple of w
-        seg = [0] + [k for k in range(1, n) if (i0 + k) % w == 0] + [n]
-        verdicts, parts = self.v.distill_coarse(pk, batches, sig_of, seg)
-        nseg = len(seg) - 1
-        has = [any(verdicts[seg[g]:seg[g + 1]]) for g in range(nseg)]
-        # one device fold for the running aggregates: group 0 = valid, group 1 + g = umbrella
-        # accumulator after piece g (piece 0 continues the incoming accumulator)
-        sc, pt, bounds = [], [], [0]
-        sc.append(self.valid_[0]); pt.append(self.valid_[1])
+        cuts = [0] + [k for k in range(1, n) if (i0 + k) % w == 0] + [n]
+        verdicts, parts = self.v.distill_coarse(pk, batches, sig_of, cuts)
+        has = [any(verdicts[cuts[g]:cuts[g + 1]]) for g in range(len(cuts) - 1)]
+        for k in range(n):
+            i = i0 + k
+            if not verdicts[k]:
+                self.invalid.append((i, sig_of[i].s_hat, pk.r_hats[i]))
+        self._accumulate(parts, has, [i0 + c for c in cuts[1:]])
+        for k in range(n):
+            del pk.r_hats[i0 + k]
+        if n:
+            self.ds = sigs[-1].ds
+        self.next_epoch += n
+
+    def _accumulate(self, parts, has, piece_end_epoch):
+        """Folds per-piece sums of valid (s, r) into the running aggregates
+        (fold_valid, distiller.cpp:45-53) and emits the umbrella records that
+        complete (:82-88). One device segfold for every running aggregate:
+        group 0 = valid, group 1 + g = the umbrella accumulator after piece g
+        (piece 0 continues the incoming accumulator)."""
+        w = self.umbrella_width()
+        nseg = len(parts)
+        sc, pt, bounds = [self.valid_[0]], [self.valid_[1]], [0]
         for g in range(nseg):
             if has[g]:
                 sc.append(parts[g][0]); pt.append(parts[g][1])
@@ -117,23 +132,69 @@ class ColdCryptoData:
         if any(has):
             self.valid_ = folded[0]
             self.has_valid = True
-        for k in range(n):
-            i = i0 + k
-            if not verdicts[k]:
-                self.invalid.append((i, sig_of[i].s_hat, pk.r_hats[i]))
         for g in range(nseg):
             acc = folded[1 + g]
             nonempty = has[g] or (g == 0 and self.umb_nonempty)
-            end = i0 + seg[g + 1]  # epochs distilled after this piece
+            end = piece_end_epoch[g]  # epochs distilled after this piece
             if end % w == 0:
                 self.umbrellas.append(((end - 1) // w, acc[0], acc[1]))
                 self.umb_acc, self.umb_nonempty = (ZERO, IDENTITY), False
             else:
                 self.umb_acc, self.umb_nonempty = acc, nonempty
-        for k in range(n):
-            del pk.r_hats[i0 + k]
+
+    # -- fine-grained distillation (distiller.cpp:91-129)
+    def distill_epoch_fine(self, pk, msgs: Sequence[bytes], sigs):
+        self.distill_epochs_fine(pk, [msgs], [sigs])
+
+    def distill_epochs_fine(self, pk, msgs_list, sigs_list):
+        """distill_epoch_fine for epochs next_epoch, next_epoch + 1, ... in one batch.
+        pk: fine.PoslofPublicKey; sigs_list[k]: the epoch's n2 FineSignatures."""
+        if self.scheme != FINE:
+            raise StateError("fine distillation on a coarse stream")
+        stop, exc = len(msgs_list), None
+        for k, (msgs, sigs) in enumerate(zip(msgs_list, sigs_list)):
+            if self.next_epoch + k >= self.suite.n1:
+                stop, exc = k, StateError("stream already complete")
+                break
+            if len(msgs) != self.suite.n2 or len(sigs) != self.suite.n2:
+                stop, exc = k, StateError("epoch must hold exactly n2 entries and signatures")
+                break
+            if not sigs[-1].carries_ds():
+                stop, exc = k, FormatError("last entry of the epoch must carry ds")
+                break
+        if stop:
+            try:
+                self._run_fine(pk, msgs_list[:stop], sigs_list[:stop])
+            except (api.SeedNotDisclosed, FormatError) as e:
+                bad = getattr(e, "epoch", None)
+                if isinstance(e, FormatError) and bad is not None:
+                    bad = self.next_epoch + bad // self.suite.n2  # entry position -> epoch
+                done = (bad - self.next_epoch) if bad is not None else 0
+                if 0 < done < stop:
+                    self._run_fine(pk, msgs_list[:done], sigs_list[:done])
+                raise
+        if exc is not None:
+            raise exc
+
+    def _run_fine(self, pk, msgs_list, sigs_list):
+        from . import fine as F
+        n, i0, n2, w = len(msgs_list), self.next_epoch, self.suite.n2, self.umbrella_width()
+        msgs = [m for ms in msgs_list for m in ms]
+        sigs = [sg for ss in sigs_list for sg in ss]
+        # entries carrying ds derive x from the epoch's NEW stack (its last signature's ds)
+        derive = [(t // n2, t % n2) if sg.carries_ds() else None for t, sg in enumerate(sigs)]
+        fb = F.FineBatch(self.suite.suite, msgs, [None if sg.carries_ds() else sg.tail for sg in sigs], derive,
+                         [i0 + k for k in range(n)], [ss[-1].tail for ss in sigs_list], None, self.suite.depth())
+        verdicts = F.fine_verify(self.v, fb, pk.y, [sg.s for sg in sigs], [sg.r for sg in sigs])
+        cuts = [0] + [k * n2 for k in range(1, n) if (i0 + k) % w == 0] + [n * n2]
+        parts = self.v.segfold([sg.s for sg in sigs], [sg.r for sg in sigs], verdicts, cuts)
+        has = [any(verdicts[cuts[g]:cuts[g + 1]]) for g in range(len(cuts) - 1)]
+        for t, ok in enumerate(verdicts):
+            if not ok:
+                self.invalid.append((i0 * n2 + t, sigs[t].s, sigs[t].r))
+        self._accumulate(parts, has, [i0 + c // n2 for c in cuts[1:]])
         if n:
-            self.ds = sigs[-1].ds
+            self.ds = sigs_list[-1][-1].tail
         self.next_epoch += n
 
     def finalize(self):
@@ -142,21 +203,79 @@ class ColdCryptoData:
             self.umbrellas.append(((self.next_epoch - 1) // self.umbrella_width(), *self.umb_acc))
             self.umb_acc, self.umb_nonempty = (ZERO, IDENTITY), False
 
-    # -- SeBVer (distiller.cpp:181-233), on the device
+    # -- SeBVer (distiller.cpp:156-233), on the device
     def sebver(self, y: bytes, all_msgs: Dict[int, Sequence[bytes]], mode: str) -> List[bool]:
-        if self.scheme != COARSE:
-            raise StateError("fine-grained SeBVer is not part of the GPU path")
+        if mode not in ("V", "U", "I"):
+            raise StateError("unknown mode")
         if mode == "V" and not self.has_valid:
             raise StateError("mode V needs a valid aggregate")
-        for i in range(self.next_epoch):
+        if self.scheme == FINE:
+            return self._sebver_fine(y, all_msgs, mode)
+        w = self.umbrella_width()
+        if mode == "I":
+            need = [i for i, _, _ in self.invalid]
+        elif mode == "V":
+            need = list(range(self.next_epoch))
+        else:
+            need = sorted({i for u, _, _ in self.umbrellas for i in range(u * w, min((u + 1) * w, self.next_epoch))})
+        for i in need:  # collect_epochs (:140-154) / the mode-I lookup (:208-210)
             if i not in all_msgs:
-                raise FormatError(f"messages for epoch {i} missing")
-            if len(all_msgs[i]) != self.suite.n2:
+                raise FormatError("messages for invalid epoch missing" if mode == "I"
+                                  else f"messages for epoch {i} missing")
+            if mode != "I" and len(all_msgs[i]) != self.suite.n2:
                 raise FormatError("epoch batch size mismatch")
         res = self.v.sebver(y, self.suite, all_msgs, self.ds, self.next_epoch, self.invalid,
                             self.umbrellas if mode == "U" else [],
                             self.valid_ if mode == "V" else None)
         return res[mode]
+
+    def _sebver_fine(self, y, all_msgs, mode):
+        from . import fine as F
+        n2, w = self.suite.n2, self.umbrella_width()
+        bad = {t for t, _, _ in self.invalid}
+        if mode == "I":
+            msgs, derive, eps = [], [], []
+            for t, _, _ in self.invalid:
+                i, j = t // n2, t % n2
+                if i not in all_msgs or len(all_msgs[i]) <= j:
+                    raise FormatError("message for invalid entry missing")
+                msgs.append(all_msgs[i][j])
+                eps.append(i)
+            slots = sorted(set(eps))
+            derive = [(slots.index(t // n2), t % n2) for t, _, _ in self.invalid]
+            if not msgs:
+                return []
+            fb = F.FineBatch(self.suite.suite, msgs, [None] * len(msgs), derive, slots, None, self.ds,
+                             self.suite.depth())
+            return F.fine_verify(self.v, fb, y, [s for _, s, _ in self.invalid], [r for _, _, r in self.invalid])
+        ranges = [(0, self.next_epoch, self.valid_)] if mode == "V" else \
+            [(u * w, (u + 1) * w, (sv, rv)) for u, sv, rv in self.umbrellas]
+        ranges = [(lo, min(hi, self.next_epoch), sig) for lo, hi, sig in ranges]
+        epochs = sorted({i for lo, hi, _ in ranges for i in range(lo, hi)})
+        for i in epochs:  # collect_epochs (:140-154)
+            if i not in all_msgs:
+                raise FormatError(f"messages for epoch {i} missing")
+            if len(all_msgs[i]) != n2:
+                raise FormatError("epoch batch size mismatch")
+        pos = {i: k for k, i in enumerate(epochs)}
+        msgs = [m for i in epochs for m in all_msgs[i]]
+        derive = [(k, j) for k in range(len(epochs)) for j in range(n2)]
+        es = []
+        if msgs:
+            fb = F.FineBatch(self.suite.suite, msgs, [None] * len(msgs), derive, epochs, None, self.ds,
+                             self.suite.depth())
+            es, _ = F.fine_scalars(self.v, fb)
+        # e-sum per range over its non-invalid entries: one masked segfold over concatenated items
+        items, mask, bounds = [], [], [0]
+        for lo, hi, _ in ranges:
+            for i in range(lo, hi):
+                for j in range(n2):
+                    items.append(es[pos[i] * n2 + j])
+                    mask.append((i * n2 + j) not in bad)
+            bounds.append(len(items))
+        sums = self.v.segfold(items, [], mask, bounds) if ranges else []
+        return self.v.group_check(y, [s for s, _ in sums], [sig[0] for _, _, sig in ranges],
+                                  [sig[1] for _, _, sig in ranges]) if ranges else []
 
     # -- wire format (distiller.cpp:235-304)
     def serialize(self) -> bytes:
