@@ -51,8 +51,11 @@ def parse():
     ap.add_argument("--cpu-log2n", type=int, default=21)
     ap.add_argument("--varlen", action="store_true",
                     help="syslog-style entries of 64..1024 printable bytes (BASELINE config 4)")
-    ap.add_argument("--mode", default="coarse", choices=["coarse", "epoch"],
-                    help="coarse: one aggregate (config 2); epoch: per-epoch verdicts (config 3)")
+    ap.add_argument("--mode", default="coarse", choices=["coarse", "epoch", "tamper"],
+                    help="coarse: one aggregate (config 2); epoch: per-epoch verdicts (config 3); "
+                         "tamper: k tampered entries localised by distillation (config 5)")
+    ap.add_argument("--tamper", type=int, default=16, help="tampered entries per GPU (mode tamper)")
+    ap.add_argument("--n-u", type=int, default=1024, help="umbrellas over the whole job (mode tamper)")
     return ap.parse_args()
 
 
@@ -76,6 +79,15 @@ def config_dict(a, n_gpus):
                 "suite": a.suite, "mode": a.mode,
                 "parallelism": f"epoch-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
                 "l2": "inputs larger than L2"}
+    if a.mode == "tamper":
+        return {"workload": f"BASELINE config 5 (per GPU): 2^{a.log2n} x {a.entry_len}-byte entries with {a.tamper} "
+                            f"tampered entries, hierarchical localisation by coarse distillation (per-epoch verdicts, "
+                            f"epoch = {a.n2} entries, + umbrella folds, n_u = {a.n_u} over the job; suite {a.suite}), "
+                            f"inputs resident in HBM",
+                "entries_per_gpu": 1 << a.log2n, "entry_len": a.entry_len, "n2": a.n2, "suite": a.suite,
+                "mode": a.mode, "tampered_per_gpu": a.tamper, "n_u": a.n_u,
+                "parallelism": f"epoch-sharded x{n_gpus}" if n_gpus > 1 else "single GPU",
+                "l2": "inputs larger than L2 (2 GiB log per GPU vs 126 MB L2)"}
     return {
         "workload": (f"BASELINE config 2: 2^{a.log2n} x {a.entry_len}-byte entries per GPU, coarse single-aggregate "
                      f"PAVer (suite {a.suite}, n2={a.n2}), inputs resident in HBM") if a.mode == "coarse" else
@@ -372,10 +384,18 @@ def main():
                                               [r.to_bytes(32, "little") for r in r_list]))
         s_buf = ctypes.create_string_buffer(s_bytes, len(s_bytes))
         r_buf = ctypes.create_string_buffer(r_enc, len(r_enc))
+        # signatures are inputs too: resident in HBM for the device-timed steps
+        s_dev = torch.frombuffer(bytearray(s_bytes), dtype=torch.uint8).cuda()
+        r_dev = torch.frombuffer(bytearray(r_enc), dtype=torch.uint8).cuda()
         verd = ctypes.create_string_buffer(n1_local)
 
+        def sig_ptrs(b):
+            if b.device_resident:
+                return ctypes.c_void_p(s_dev.data_ptr()), ctypes.c_void_p(r_dev.data_ptr())
+            return s_buf, r_buf
+
         def step_epoch(b):
-            call(lib.poslo_gpu_epoch_verify, ctypes.byref(b), Yb, s_buf, r_buf, verd, None)
+            call(lib.poslo_gpu_epoch_verify, ctypes.byref(b), Yb, *sig_ptrs(b), verd, None)
             bad = n1_local - sum(verd.raw[:n1_local])
             if world > 1:
                 bad = sum(int.from_bytes(x, "little") for x in MG.all_gather_bytes(bad.to_bytes(4, "little")))
@@ -383,13 +403,64 @@ def main():
 
         step = step_epoch
 
+    if a.mode == "tamper":
+        # per-epoch signatures as in epoch mode, then k seeded entries tampered (one bit
+        # flipped after signing); a step distils every epoch: per-epoch verdicts (the
+        # invalid-epoch list) + valid (s, R) folded per umbrella piece on the device
+        et = ctypes.create_string_buffer(n1_local * 32)
+        call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), et, None)
+        r_list = [rng.randrange(1, L_ORDER) for _ in range(n1_local)]
+        et_raw = et.raw
+        s_bytes = b"".join(((r_list[k] - int.from_bytes(et_raw[32 * k:32 * k + 32], "little") * y) % L_ORDER)
+                           .to_bytes(32, "little") for k in range(n1_local))
+        r_enc = b"".join(v.commit_check_batch(bytes(32), [bytes(32)] * n1_local,
+                                              [r.to_bytes(32, "little") for r in r_list]))
+        s_buf = ctypes.create_string_buffer(s_bytes, len(s_bytes))
+        r_buf = ctypes.create_string_buffer(r_enc, len(r_enc))
+        s_dev = torch.frombuffer(bytearray(s_bytes), dtype=torch.uint8).cuda()
+        r_dev = torch.frombuffer(bytearray(r_enc), dtype=torch.uint8).cuda()
+
+        def sig_ptrs(b):
+            if b.device_resident:
+                return ctypes.c_void_p(s_dev.data_ptr()), ctypes.c_void_p(r_dev.data_ptr())
+            return s_buf, r_buf
+
+        trng = random.Random(a.seed * 7919 + rank)
+        tampered = sorted(trng.sample(range(n), min(a.tamper, n)))
+        for t in tampered:
+            log[t * L] ^= 1
+        torch.cuda.synchronize()
+        expect_bad = sorted({t // a.n2 for t in tampered})
+        w = max(1, n1_total // max(1, a.n_u))
+        e0 = rank * n1_local
+        cuts = [0] + [k for k in range(1, n1_local) if (e0 + k) % w == 0] + [n1_local]
+        seg_arr = np.array(cuts, dtype=np.uint32)
+        n_seg = len(cuts) - 1
+        verd = ctypes.create_string_buffer(n1_local)
+        seg_s = ctypes.create_string_buffer(32 * n_seg)
+        seg_r = ctypes.create_string_buffer(32 * n_seg)
+
+        def step_tamper(b):
+            call(lib.poslo_gpu_distill_coarse, ctypes.byref(b), Yb, *sig_ptrs(b),
+                 ctypes.c_void_p(seg_arr.ctypes.data), n_seg, verd, seg_s, seg_r)
+            ok = 1
+            if world > 1:
+                ok = min(int(x[0]) for x in MG.all_gather_bytes(bytes([ok])))
+            return ok
+
+        step = step_tamper
+
     # ---- warm-up + correctness of the fixture
     for _ in range(a.warmup):
         ok = step(bdev)
+    if a.mode == "tamper":
+        raw = verd.raw
+        found = [e0 + k for k in range(n1_local) if not raw[k]]
+        assert found == [e0 + k for k in expect_bad], f"localisation mismatch: {found[:8]} vs {expect_bad[:8]}"
     if rank == 0:
         assert ok == 1, "verifier rejected a valid aggregate"
     # tamper check (untimed): one flipped bit must be rejected
-    if world == 1:
+    if world == 1 and a.mode != "tamper":
         saved = log[0].item()
         log[0] = saved ^ 1
         torch.cuda.synchronize()
@@ -449,11 +520,14 @@ def main():
             e2e_ms = t.item()
         e2e_value = world * n / (e2e_ms * 1e-3)
         del host
-        h2d = payload_bytes + (8 * (n + 1) if offsets_dev is not None else 0) + 4 * n1_local + len(ds_bytes) + 8 + (64 * n1_local if a.mode == "epoch" else 32)
-        d2h = (n1_local if a.mode == "epoch" else 1) + 8
+        per_epoch_in = 64 * n1_local if a.mode in ("epoch", "tamper") else 32
+        h2d = payload_bytes + (8 * (n + 1) if offsets_dev is not None else 0) + 4 * n1_local + len(ds_bytes) + 8 + per_epoch_in
+        if a.mode == "tamper":
+            h2d += 4 * (n_seg + 1)
+        d2h = (n1_local if a.mode in ("epoch", "tamper") else 1) + 8 + (64 * n_seg if a.mode == "tamper" else 0)
         e2e = {"value": round(e2e_value, 1), "unit": "entries/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-               "path": f"poslo_gpu_{'paver' if a.mode == 'coarse' else 'epoch_verify'}(device_resident=0) "
+               "path": f"poslo_gpu_{dict(coarse='paver', epoch='epoch_verify', tamper='distill_coarse')[a.mode]}(device_resident=0) "
                        f"on a pinned host log, 64 MiB chunked H2D overlapped with hashing"}
 
     if rank != 0:

@@ -141,7 +141,9 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t 
 
 /* ---- per-epoch verification (distill_epoch verdicts, distiller.cpp:60-89) ---
  * verdicts[k] = (commit_check(Y, e~_k, s_hats[k]) == r_hats[k]) for every
- * queried epoch; e_tilde_out optional (n_epochs x 32 B). */
+ * queried epoch; e_tilde_out optional (n_epochs x 32 B). When the batch is
+ * device_resident, s_hats / r_hats are device pointers too (scalars already
+ * canonical: they were validated when the signatures were parsed). */
 int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
                            const uint8_t* s_hats, const uint8_t* r_hats, uint8_t* verdicts,
                            uint8_t* e_tilde_out, poslo_error* err);
@@ -170,7 +172,8 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t
  * seg_s[g] = sum of s_hats mod l (Scalar::add fold, :48) and seg_r[g] = the
  * group_combine fold of r_hats (:49, identity = 32 zero bytes when none).
  * The running CCD state (valid/umbrella accumulators, invalid list, ds) is
- * the caller's; see paper_2506_08781_b200/distill.py. */
+ * the caller's; see paper_2506_08781_b200/distill.py. s_hats / r_hats are
+ * device pointers when the batch is device_resident (as epoch_verify). */
 int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
                              const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg,
                              uint32_t n_seg, uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r,

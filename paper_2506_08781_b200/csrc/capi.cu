@@ -742,6 +742,24 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     return ok(err);
 }
 
+// Per-epoch signature arrays (s-hat LE, R-hat): device pointers as given when
+// the batch is device-resident, else uploaded.
+static int sig_arrays(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t* s_hats, const uint8_t* r_hats,
+                      const uint32_t** d_s_out, const uint8_t** d_r_out, poslo_error* err) {
+    if (b->device_resident) {
+        *d_s_out = reinterpret_cast<const uint32_t*>(s_hats);
+        *d_r_out = r_hats;
+        return POSLO_OK;
+    }
+    uint32_t* d_s;
+    uint8_t* d_r;
+    UPLOAD(b_s, s_hats, (size_t)b->n_epochs * 32, d_s);
+    UPLOAD(b_r, r_hats, (size_t)b->n_epochs * 32, d_r);
+    *d_s_out = d_s;
+    *d_r_out = d_r;
+    return POSLO_OK;
+}
+
 int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
                            const uint8_t* s_hats, const uint8_t* r_hats, uint8_t* verdicts,
                            uint8_t* e_tilde_out, poslo_error* err) {
@@ -749,17 +767,18 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     if (!b || !y || (b->n_epochs && (!s_hats || !r_hats || !verdicts)))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
     Guard g(ctx);
-    for (uint32_t k = 0; k < b->n_epochs; k++)
-        if (!scalar_canonical(s_hats + 32 * (size_t)k))
-            return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    if (!b->device_resident)  // device-resident signature arrays were validated when parsed
+        for (uint32_t k = 0; k < b->n_epochs; k++)
+            if (!scalar_canonical(s_hats + 32 * (size_t)k))
+                return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
     Prepared P;
     int rc = run_hash(ctx, b, P, err);
     if (rc) return rc;
     mark(ctx, kEvSum);
-    uint32_t* d_s;
-    uint8_t* d_r;
-    UPLOAD(b_s, s_hats, (size_t)b->n_epochs * 32, d_s);
-    UPLOAD(b_r, r_hats, (size_t)b->n_epochs * 32, d_r);
+    const uint32_t* d_s;
+    const uint8_t* d_r;
+    rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+    if (rc) return rc;
     mark(ctx, kEvGroup);
     rc = check_hash_errors(ctx, b, err);
     if (rc) return rc;
@@ -845,10 +864,11 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
     if (rc) return rc;
     const uint32_t n = b->n_epochs;
     if (!n) return ok(err);
-    uint32_t* d_s;
-    uint8_t* d_r;
-    UPLOAD(b_s, s_hats, (size_t)n * 32, d_s);
-    UPLOAD(b_r, r_hats, (size_t)n * 32, d_r);
+    const uint32_t* d_s;
+    const uint8_t* d_r;
+    rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+    if (rc) return rc;
+    mark(ctx, kEvSum);
     mark(ctx, kEvGroup);
     // per-epoch verdicts stay on the device as the fold mask
     int* d_flags;

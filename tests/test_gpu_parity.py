@@ -339,3 +339,40 @@ def test_multi_epoch_tiles_match_oracle(verifier, n2):
     ref = _oracle_etilde(1, batches, ds)
     assert [p[1] for p in parts] == ref
     assert e_hat == O.sum_scalars(ref)
+
+
+def test_device_resident_signatures_match_host(verifier):
+    """epoch_verify / distill_coarse with a device-resident batch take the
+    per-epoch signature arrays from HBM too; verdicts equal the host path."""
+    import ctypes
+
+    import torch
+    from paper_2506_08781_b200 import _native as N
+    from conftest import load_golden
+    from golden_util import Stream
+    api = A()
+    st = Stream(load_golden("stream_s1_tamper.json"))
+    suite, pk, ds = st.api_objects()
+    s_hats = {i: st.sigs[i].s_hat_le for i in range(st.n1)}
+    host_verdicts = verifier.epoch_verify(pk, st.batches, s_hats, ds)
+    flat = b"".join(m for i in range(st.n1) for m in st.batches[i])
+    pay = torch.frombuffer(bytearray(flat), dtype=torch.uint8).cuda()
+    s_dev = torch.frombuffer(bytearray(b"".join(s_hats[i] for i in range(st.n1))), dtype=torch.uint8).cuda()
+    r_dev = torch.frombuffer(bytearray(b"".join(pk.r_hats[i] for i in range(st.n1))), dtype=torch.uint8).cuda()
+    dsb = ds.serialize()
+    dsbuf = ctypes.create_string_buffer(dsb, len(dsb))
+    epochs = np.arange(st.n1, dtype=np.uint32)
+    b = N.PosloBatch()
+    b.suite, b.n2, b.payload, b.payload_bytes = 1, st.n2, pay.data_ptr(), len(flat)
+    b.offsets, b.entry_len, b.n_entries = None, 32, st.n1 * st.n2
+    b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, st.n1
+    b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(dsbuf), len(dsb), ds.capacity, 1
+    verd = ctypes.create_string_buffer(st.n1)
+    verifier._call(verifier._lib.poslo_gpu_epoch_verify, ctypes.byref(b), pk.y, ctypes.c_void_p(s_dev.data_ptr()),
+                   ctypes.c_void_p(r_dev.data_ptr()), verd, None)
+    assert [bool(x) for x in verd.raw] == host_verdicts
+    seg = np.array([0, 5, st.n1], dtype=np.uint32)
+    so, ro = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+    verifier._call(verifier._lib.poslo_gpu_distill_coarse, ctypes.byref(b), pk.y, ctypes.c_void_p(s_dev.data_ptr()),
+                   ctypes.c_void_p(r_dev.data_ptr()), ctypes.c_void_p(seg.ctypes.data), 2, verd, so, ro)
+    assert [bool(x) for x in verd.raw] == host_verdicts
