@@ -81,6 +81,10 @@ typedef struct poslo_batch {
                                       is then derived from its OWN stack ds[ds_offsets[k] ..
                                       ds_offsets[k+1]) (EpochSignature::ds, the distill_epoch
                                       semantics). NULL: one stack `ds` for every epoch. */
+    uint32_t record_header;        /* 0, or 4 for a raw log file (log_file.hpp:34-51): `payload` is
+                                      the file's bytes, offsets[t] the position of record t's LE32
+                                      length and the entry is payload[offsets[t] + 4 .. offsets[t+1])
+                                      (offsets from poslo_log_scan; zero-copy ingestion) */
 } poslo_batch;
 
 /* Scheme F (POSLO-F, include/poslo/poslo_f.hpp) entries: each entry t has a
@@ -107,6 +111,16 @@ typedef struct poslo_fine_batch {
     uint32_t ds_capacity;
     const uint64_t* ds_offsets;    /* n_slots + 1 (host) or NULL */
 } poslo_fine_batch;
+
+/* ---- log ingestion (read_log, include/poslo/log_file.hpp:34-51) -------------
+ * Host-side scan of a raw log file image (records: LE32 length + payload).
+ * Writes the record header positions to offsets[0..n] (offsets[n] = len)
+ * and n to *n_records. FormatError "truncated log record" exactly where
+ * read_log throws it. cap = capacity of `offsets` in records (it needs n + 1
+ * slots); when too small, returns POSLO_INVALID_ARGUMENT with *n_records =
+ * the count needed. Pure host code; no device is touched. */
+int poslo_log_scan(const uint8_t* raw, uint64_t len, uint64_t* offsets, uint64_t cap, uint64_t* n_records,
+                   poslo_error* err);
 
 /* ---- context -------------------------------------------------------------- */
 int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);

@@ -36,6 +36,7 @@ class PosloBatch(ctypes.Structure):
         ("ds_capacity", ctypes.c_uint32),
         ("device_resident", ctypes.c_int32),
         ("ds_offsets", ctypes.c_void_p),
+        ("record_header", ctypes.c_uint32),
     ]
 
 
@@ -67,7 +68,7 @@ EXPORTS = [
     "poslo_gpu_group_fold", "poslo_gpu_point_valid", "poslo_gpu_seed_retrieve",
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
     "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold", "poslo_gpu_fine_scalars",
-    "poslo_gpu_fine_verify", "poslo_gpu_aver_f_batch",
+    "poslo_gpu_fine_verify", "poslo_gpu_aver_f_batch", "poslo_log_scan",
 ]
 
 _lib = None
@@ -116,6 +117,7 @@ def load():
         "poslo_gpu_fine_scalars": ([P, F, P, P, E], c.c_int),
         "poslo_gpu_fine_verify": ([P, F, P, P, P, P, E], c.c_int),
         "poslo_gpu_aver_f_batch": ([P, F, P, P, P, P, E], c.c_int),
+        "poslo_log_scan": ([P, c.c_uint64, P, c.c_uint64, c.POINTER(c.c_uint64), E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -336,6 +336,26 @@ class Verifier:
         pb = PackedBatch(suite.suite, suite.n2, batches, ds)
         return self.agg_ekeys_packed(pb)
 
+    def agg_ekeys_log(self, rb):
+        """agg_ekeys over a RecordBatch (logfile.py): the raw log image is hashed in place."""
+        return self.agg_ekeys_packed(rb)
+
+    def paver_log(self, pk: PoslocPublicKey, rb, s_hat: bytes, r_hat_agg: Optional[bytes] = None) -> bool:
+        """paver over a RecordBatch (every epoch holds n2 records by construction)."""
+        r_hats = None
+        if r_hat_agg is None:
+            rows = []
+            for i in rb.epochs:
+                if int(i) not in pk.r_hats:
+                    raise StateError(f"commitment for epoch {int(i)} no longer in public key")
+                rows.append(pk.r_hats[int(i)])
+            r_hats = b"".join(rows)
+        cb = rb.cstruct()
+        v = ctypes.c_uint8(0)
+        self._call(self._lib.poslo_gpu_paver, ctypes.byref(cb), _buf(pk.y), _buf(s_hat),
+                   _buf(r_hat_agg), _buf(r_hats), ctypes.byref(v))
+        return bool(v.value)
+
     def agg_ekeys_packed(self, pb: PackedBatch):
         n = len(pb.epochs)
         out = ctypes.create_string_buffer(max(n, 1) * 32)

@@ -259,6 +259,9 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     // stream in epoch-aligned 64 MiB chunks on the copy stream, each chunk's
     // hashing waiting only for its own bytes (SPEC.md:496 chunked streaming).
     P.lay.entry_len = b->entry_len;
+    if (b->record_header != 0 && (b->record_header != 4 || !b->offsets))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "record_header must be 0, or 4 with record offsets");
+    P.lay.header = b->record_header;
     const uint64_t epoch_bytes = (uint64_t)b->n2 * b->entry_len;
     const bool chunked = !b->device_resident && P.uniform && !b->offsets && epoch_bytes > 0 &&
                          b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
@@ -631,6 +634,29 @@ int poslo_gpu_last_timings(poslo_gpu_ctx* ctx, float out_ms[6]) {
     if (!ctx || !out_ms) return POSLO_INVALID_ARGUMENT;
     std::memcpy(out_ms, ctx->last_ms, sizeof ctx->last_ms);
     return POSLO_OK;
+}
+
+int poslo_log_scan(const uint8_t* raw, uint64_t len, uint64_t* offsets, uint64_t cap, uint64_t* n_records,
+                   poslo_error* err) {
+    // read_log (log_file.hpp:34-51): LE32 length, then that many bytes; the
+    // walk is inherently sequential (each record's position depends on every
+    // earlier length), so it is one tight host loop over the file image.
+    if (!n_records || (len && !raw)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    uint64_t off = 0, n = 0;
+    while (off < len) {
+        if (len - off < 4) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated log record");
+        uint32_t l;
+        std::memcpy(&l, raw + off, 4);  // little-endian host (x86-64 / aarch64)
+        if (len - off - 4 < l) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated log record");
+        if (offsets && n < cap) offsets[n] = off;
+        off += 4 + (uint64_t)l;
+        n++;
+    }
+    *n_records = n;
+    if (!offsets || n + 1 > cap) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "offsets capacity %llu < %llu",
+                                                (unsigned long long)cap, (unsigned long long)(n + 1));
+    offsets[n] = len;
+    return ok(err);
 }
 
 uint32_t poslo_gpu_last_launches(poslo_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
         const uint64_t ent = ebase + j0 + i;
-        const uint64_t L = lay.offsets ? lay.offsets[ent + 1] - lay.offsets[ent] : lay.entry_len;
+        const uint64_t L = lay.offsets ? lay.offsets[ent + 1] - lay.offsets[ent] - lay.header : lay.entry_len;
         atomicAdd(&bucket_count[min(nblocks(L + 17), (uint32_t)kVarBuckets - 1)], 1u);
     }
     __syncthreads();
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
         const uint64_t ent = ebase + j0 + i;
-        const uint64_t L = lay.offsets ? lay.offsets[ent + 1] - lay.offsets[ent] : lay.entry_len;
+        const uint64_t L = lay.offsets ? lay.offsets[ent + 1] - lay.offsets[ent] - lay.header : lay.entry_len;
         const uint32_t slot = atomicAdd(&bucket_base[min(nblocks(L + 17), (uint32_t)kVarBuckets - 1)], 1u);
         order[slot] = (uint16_t)i;
     }
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
         const uint64_t ent = ebase + j;
         uint64_t L;
         if (lay.offsets) {
-            const uint64_t o0 = lay.offsets[ent];
+            const uint64_t o0 = lay.offsets[ent] + lay.header;
             v.m = lay.payload + o0;
             L = lay.offsets[ent + 1] - o0;
         } else {

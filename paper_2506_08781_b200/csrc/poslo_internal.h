@@ -23,6 +23,7 @@ struct EntryLayout {
     const uint8_t* payload;   // entry bytes
     const uint64_t* offsets;  // n_entries + 1 byte offsets, or nullptr (fixed stride)
     uint32_t entry_len;       // stride / length when offsets == nullptr
+    uint32_t header;          // bytes before each entry at offsets[t] (4: LE32 log records), else 0
 };
 
 // Tiles: a tile is a contiguous run of entries of ONE epoch that one CTA

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(128) k_fine_scalars(int suite, EntryLayout lay
     const uint8_t* m;
     uint32_t L;
     if (lay.offsets) {
-        const uint64_t o0 = lay.offsets[t];
+        const uint64_t o0 = lay.offsets[t] + lay.header;
         m = lay.payload + o0;
         L = (uint32_t)(lay.offsets[t + 1] - o0);
     } else {
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay
         const uint8_t* m;
         uint32_t L;
         if (lay.offsets) {
-            uint64_t o0 = lay.offsets[ent], o1 = lay.offsets[ent + 1];
+            uint64_t o0 = lay.offsets[ent] + lay.header, o1 = lay.offsets[ent + 1];
             m = lay.payload + o0;
             L = (uint32_t)(o1 - o0);
         } else {

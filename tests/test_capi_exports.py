@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "poslo_gpu.h")).read()
-    return sorted(set(re.findall(r"\b(poslo_gpu_[a-z_0-9]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(poslo_(?:gpu|log)_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_header_matches_binding():

@@ -1,0 +1,60 @@
+"""Log ingestion (log_file.hpp read_log / write_log, tools/poslo.cpp epochs_of):
+the host scanner is exercised on CPU; GPU tests hash the raw file image in place."""
+import os
+
+import pytest
+
+from conftest import STREAMS, load_golden
+from golden_util import Stream
+
+
+def _lib_present():
+    from paper_2506_08781_b200 import _native as N
+    return os.path.exists(N.LIB_PATH)
+
+
+pytestmark_cpu = pytest.mark.skipif(not _lib_present(), reason="libposlo_gpu.so not built")
+
+
+@pytestmark_cpu
+def test_scan_roundtrip_and_truncation(tmp_path):
+    from paper_2506_08781_b200 import api
+    from paper_2506_08781_b200.logfile import RecordLog, write_log
+    recs = [b"", b"a", bytes(range(256)) * 3, b"xyz" * 1000, b"\x00\x01\x02\x03"]
+    p = str(tmp_path / "log.bin")
+    write_log(p, recs)
+    log = RecordLog.read(p)
+    assert len(log) == len(recs) and [log.record(t) for t in range(len(recs))] == recs
+    raw = open(p, "rb").read()
+    for cut in (1, 3, 5, len(raw) - 1):  # truncated header / body, as read_log
+        with pytest.raises(api.FormatError, match="truncated log record"):
+            RecordLog(raw[:cut] if cut < 4 else raw[:len(raw) - 1] if cut == len(raw) - 1 else raw[:cut])
+    assert len(RecordLog(b"")) == 0
+    with pytest.raises(api.FormatError):
+        RecordLog(b"").epochs_of(4)
+    with pytest.raises(api.FormatError):
+        log.epochs_of(2)  # 5 records
+    with pytest.raises(api.FormatError):
+        RecordLog.read(str(tmp_path / "missing.bin"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", STREAMS)
+def test_log_file_batches_match_reference(verifier, tmp_path, name):
+    """write_log the golden stream, read it back as a file image and verify it
+    in place (record_header = 4): e~, e-hat and paver equal the reference's."""
+    from paper_2506_08781_b200.logfile import RecordLog, write_log
+    st = Stream(load_golden(name + ".json"))
+    suite, pk, ds = st.api_objects()
+    p = str(tmp_path / "stream.log")
+    write_log(p, [m for i in range(st.n1) for m in st.batches[i]])
+    log = RecordLog.read(p)
+    assert log.epochs_of(st.n2) == st.n1
+    rb = log.batch(st.suite, st.n2, ds)
+    parts, e_hat = verifier.agg_ekeys_log(rb)
+    assert [x[1] for x in parts] == st.e_tilde and e_hat == st.e_hat
+    assert verifier.paver_log(pk, rb, st.s_hat) == bool(st.d["paver"])
+    # a sub-range of epochs (offsets rebased onto the slice of the image)
+    sub = log.batch(st.suite, st.n2, ds, range(1, st.n1))
+    parts2, _ = verifier.agg_ekeys_log(sub)
+    assert [x[1] for x in parts2] == st.e_tilde[1:]
