@@ -50,7 +50,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
@@ -599,7 +599,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_flags, &ctx->b_payload, &ctx->b_offsets, &ctx->b_e, &ctx->b_s,
                       &ctx->b_r, &ctx->b_enc, &ctx->b_verdict, &ctx->b_mask, &ctx->b_seg, &ctx->b_y,
                       &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
-                      &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r};
+                      &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
@@ -768,6 +768,30 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     return ok(err);
 }
 
+// R-hat decoding for batched checks: queued on the side stream behind
+// everything already on the main stream (their upload), so it overlaps the
+// hashing that follows; split_checks waits for it.
+static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
+                        poslo_error* err) {
+    ENSURE(b_dpts, (size_t)std::max<uint32_t>(n, 1) * kPointBytes, *d_pts);
+    ENSURE(b_dok, std::max<uint32_t>(n, 1), *d_ok);
+    CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
+    launch_decode_points(d_r, n, *d_pts, *d_ok, ctx->side);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
+    return POSLO_OK;
+}
+
+static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const void* d_pts,
+                        const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err) {
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
+    launch_check_split(ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_pts, d_ok, d_verdict, ctx->stream);
+    ctx->launches += n ? 1 : 0;
+    CU(cudaGetLastError());
+    return POSLO_OK;
+}
+
 // Per-epoch signature arrays (s-hat LE, R-hat): device pointers as given when
 // the batch is device-resident, else uploaded.
 static int sig_arrays(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t* s_hats, const uint8_t* r_hats,
@@ -797,19 +821,52 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         for (uint32_t k = 0; k < b->n_epochs; k++)
             if (!scalar_canonical(s_hats + 32 * (size_t)k))
                 return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    const uint32_t n = b->n_epochs;
+    const bool split = n > kCtaCheckMax;
+    const uint32_t* d_s = nullptr;
+    const uint8_t* d_r = nullptr;
+    void* d_pts = nullptr;
+    uint8_t* d_ok = nullptr;
+    int rc;
+    if (split) {  // tables and R-hat decoding ahead of (and overlapping) the hashing
+        int* d_flags;
+        ENSURE(b_flags, 4, d_flags);
+        CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+        rc = ensure_tables(ctx, y, d_flags, err, true);
+        if (rc) return rc;
+        rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+        if (rc) return rc;
+        rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
+        if (rc) return rc;
+    }
     Prepared P;
-    int rc = run_hash(ctx, b, P, err);
-    if (rc) return rc;
+    rc = run_hash(ctx, b, P, err);
+    if (rc) {
+        cudaStreamSynchronize(ctx->side);
+        return rc;
+    }
     mark(ctx, kEvSum);
-    const uint32_t* d_s;
-    const uint8_t* d_r;
-    rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
-    if (rc) return rc;
+    if (!split) {
+        rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+        if (rc) return rc;
+    }
     mark(ctx, kEvGroup);
     rc = check_hash_errors(ctx, b, err);
-    if (rc) return rc;
-    rc = group_check_dev(ctx, y, b->n_epochs, P.d_etilde, d_s, d_r, verdicts, nullptr, err);
-    if (rc) return rc;
+    if (rc) {
+        cudaStreamSynchronize(ctx->side);
+        return rc;
+    }
+    if (split) {
+        uint8_t* d_verdict;
+        ENSURE(b_verdict, n, d_verdict);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    } else {
+        rc = group_check_dev(ctx, y, n, P.d_etilde, d_s, d_r, verdicts, nullptr, err);
+        if (rc) return rc;
+    }
     if (e_tilde_out && b->n_epochs)
         CU(cudaMemcpy(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost));
     finish_timing(ctx);
@@ -883,33 +940,67 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         for (uint32_t k = 0; k < b->n_epochs; k++)
             if (b->epoch_starts[k + 1] - b->epoch_starts[k] != b->n2)
                 return set_err(err, POSLO_STATE_ERROR, b->epochs[k], "every batch must hold exactly n2 entries");
-    Prepared P;
-    int rc = run_hash(ctx, b, P, err);
-    if (rc) return rc;
-    rc = check_hash_errors(ctx, b, err);
-    if (rc) return rc;
     const uint32_t n = b->n_epochs;
-    if (!n) return ok(err);
-    const uint32_t* d_s;
-    const uint8_t* d_r;
-    rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+    const bool split = n > kCtaCheckMax;
+    const uint32_t* d_s = nullptr;
+    const uint8_t* d_r = nullptr;
+    void* d_pts = nullptr;
+    uint8_t* d_ok = nullptr;
+    int* d_flags;
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    int rc = ensure_tables(ctx, y, d_flags, err, split);
     if (rc) return rc;
+    if (n) {
+        rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
+        if (rc) return rc;
+    }
+    if (split) {  // R-hat decoded once, on the side stream during hashing, for the checks AND the fold
+        rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
+        if (rc) return rc;
+    }
+    Prepared P;
+    rc = run_hash(ctx, b, P, err);
+    if (!rc) rc = check_hash_errors(ctx, b, err);
+    if (rc) {
+        cudaStreamSynchronize(ctx->side);
+        return rc;
+    }
+    if (!n) return ok(err);
     mark(ctx, kEvSum);
     mark(ctx, kEvGroup);
     // per-epoch verdicts stay on the device as the fold mask
-    int* d_flags;
     uint8_t* d_verdict;
-    ENSURE(b_flags, 4, d_flags);
-    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
-    rc = ensure_tables(ctx, y, d_flags, err, n > kCtaCheckMax);
-    if (rc) return rc;
     ENSURE(b_verdict, n, d_verdict);
-    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s, d_r,
-                            nullptr, d_verdict, ctx->stream);
-    ctx->launches += 1;
+    if (split) {
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);
+        if (rc) return rc;
+    } else {
+        launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s,
+                                d_r, nullptr, d_verdict, ctx->stream);
+        ctx->launches += 1;
+    }
     CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
-    rc = segfold_dev(ctx, n, d_s, d_r, d_verdict, seg, n_seg, seg_s, seg_r, err);
-    if (rc) return rc;
+    if (split) {  // scalars as before; points from the decoded R-hats (no second decode)
+        rc = segfold_dev(ctx, n, d_s, nullptr, d_verdict, seg, n_seg, seg_s, nullptr, err);
+        if (rc) return rc;
+        if (n_seg) {
+            for (uint32_t g2 = 0; g2 < n_seg; g2++)
+                if (seg[g2] > seg[g2 + 1] || seg[g2 + 1] > n)
+                    return set_err(err, POSLO_INVALID_ARGUMENT, 0, "segments must be non-decreasing within [0, n]");
+            uint32_t* d_seg;
+            uint8_t* d_out;
+            UPLOAD(b_seg32, seg, (size_t)(n_seg + 1) * 4, d_seg);
+            ENSURE(b_out_r, (size_t)n_seg * 32, d_out);
+            launch_segfold_decoded(d_pts, d_seg, n_seg, d_verdict, d_out, ctx->stream);
+            ctx->launches += 1;
+            CU(cudaMemcpyAsync(seg_r, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        CU(cudaStreamSynchronize(ctx->stream));
+    } else {
+        rc = segfold_dev(ctx, n, d_s, d_r, d_verdict, seg, n_seg, seg_s, seg_r, err);
+        if (rc) return rc;
+    }
     finish_timing(ctx);
     return ok(err);
 }

@@ -232,6 +232,112 @@ __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict_
     }
 }
 
+// ---- batched checks with R decoded ahead ----------------------------------
+// commit_check(Y, e, s) == R (byte equality of canonical encodings) <=> R is
+// a valid encoding and eY + sB == R as ristretto classes (RFC 9496 §4.3.3).
+// Decoding R does not depend on the hashes, so it runs on a side stream
+// while the log is hashed; the check itself is then 64 mixed additions spread
+// over 8 lanes (8 radix-256 windows each, 4 of e and 4 of s) and a 3-level
+// shuffle tree, plus a 4-multiplication compare: no inverse square root on
+// the critical path and 8x the threads of the thread-per-check kernel.
+__global__ void __launch_bounds__(128) k_decode_pts(const uint8_t* __restrict__ enc, uint32_t n,
+                                                    gpt* __restrict__ out, uint8_t* __restrict__ ok) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t b[32];
+    load32(enc + (size_t)i * 32, b);
+    gpt P;
+    const bool v = rist_decode(b, P);
+    out[i] = v ? P : pt_identity();
+    ok[i] = v ? 1 : 0;
+}
+
+__device__ __forceinline__ gpt shfl_pt(const gpt& p, int off) {
+    gpt r;
+    const fe* src[4] = {&p.X, &p.Y, &p.Z, &p.T};
+    fe* dst[4] = {&r.X, &r.Y, &r.Z, &r.T};
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+#pragma unroll
+        for (int k = 0; k < 8; k++) dst[c]->v[k] = __shfl_down_sync(0xffffffffu, src[c]->v[k], off, 8);
+    return r;
+}
+
+__global__ void __launch_bounds__(128) k_check_split(const gcached* __restrict__ tabY,
+                                                     const gcached* __restrict__ tabB, uint32_t n,
+                                                     const uint32_t* __restrict__ e,
+                                                     const uint32_t* __restrict__ s,
+                                                     const gpt* __restrict__ R,
+                                                     const uint8_t* __restrict__ rok,
+                                                     uint8_t* __restrict__ verdict) {
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = gid >> 3, sub = gid & 7;
+    const bool live = i < n;
+    const uint32_t ic = live ? i : 0;
+    // this lane's windows: signed radix-256 digits 4 sub .. 4 sub + 3 of e (Y
+    // table) and of s (alpha table); the recoding carry runs through all 32
+    uint32_t ve[8], vs[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        ve[k] = e[(size_t)ic * 8 + k];
+        vs[k] = s[(size_t)ic * 8 + k];
+    }
+    int de[4] = {0, 0, 0, 0}, dsg[4] = {0, 0, 0, 0};
+    int ce = 0, cs = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+        const int a = (int)((ve[k >> 2] >> (8 * (k & 3))) & 255u) + ce;
+        ce = (a + 128) >> 8;
+        const int b = (int)((vs[k >> 2] >> (8 * (k & 3))) & 255u) + cs;
+        cs = (b + 128) >> 8;
+        if ((uint32_t)(k >> 2) == sub) {
+            de[k & 3] = a - (ce << 8);
+            dsg[k & 3] = b - (cs << 8);
+        }
+    }
+    gpt acc = pt_identity();
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int k = 4 * (int)sub + q;
+        if (de[q]) {
+            const int a = de[q] < 0 ? -de[q] : de[q];
+            const gcached c = tabY[128 * k + a - 1];
+            acc = pt_add_cached(acc, de[q] < 0 ? cached_neg(c) : c);
+        }
+        if (dsg[q]) {
+            const int a = dsg[q] < 0 ? -dsg[q] : dsg[q];
+            const gcached c = tabB[128 * k + a - 1];
+            acc = pt_add_cached(acc, dsg[q] < 0 ? cached_neg(c) : c);
+        }
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+        const gpt o = shfl_pt(acc, off);
+        if (sub < (uint32_t)off) acc = pt_add(acc, o);
+    }
+    if (live && sub == 0) verdict[i] = (rok[i] && rist_equal(acc, R[i])) ? 1 : 0;
+}
+
+// Masked segmented fold over already-decoded points (distillation after the
+// split checks: R-hat is decoded once for both).
+__global__ void __launch_bounds__(128) k_segfold_gpt(const gpt* __restrict__ pts,
+                                                     const uint32_t* __restrict__ seg,
+                                                     const uint8_t* __restrict__ mask,
+                                                     uint8_t* __restrict__ out) {
+    __shared__ gpt sh[128];
+    const uint32_t g = blockIdx.x, lo = seg[g], hi = seg[g + 1];
+    gpt acc = pt_identity();
+    for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
+        if (!mask || mask[k]) acc = pt_add(acc, pts[k]);
+    block_reduce_pt(acc, sh);
+    if (threadIdx.x == 0) {
+        uint8_t o[32];
+        rist_encode(acc, o);
+#pragma unroll
+        for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
+    }
+}
+
 // ---- split single check: commit_check(Y, e, s) == R <=> e*Y == R - s*B ----
 // The pre part (R decode + s*B) does not depend on e-hat, so paver runs it on
 // a side stream concurrently with hashing; after hashing only e*Y (64 table
@@ -331,6 +437,27 @@ __global__ void __launch_bounds__(128) k_segfold_points(const uint8_t* __restric
 }
 
 }  // namespace
+
+void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s) {
+    if (!n) return;
+    k_decode_pts<<<(n + 127) / 128, 128, 0, s>>>(d_enc, n, static_cast<gpt*>(d_pts), d_ok);
+}
+
+void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n, const uint32_t* d_e,
+                        const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                        cudaStream_t s) {
+    if (!n) return;
+    const uint64_t threads = (uint64_t)n * 8;
+    k_check_split<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
+        static_cast<const gcached*>(d_tabY256), static_cast<const gcached*>(d_tabB256), n, d_e, d_s,
+        static_cast<const gpt*>(d_pts), d_ok, d_verdict);
+}
+
+void launch_segfold_decoded(const void* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
+                            uint8_t* d_out, cudaStream_t s) {
+    if (!n_seg) return;
+    k_segfold_gpt<<<n_seg, 128, 0, s>>>(static_cast<const gpt*>(d_pts), d_seg, d_mask, d_out);
+}
 
 void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
                            uint8_t* d_out, int* d_bad, cudaStream_t s) {

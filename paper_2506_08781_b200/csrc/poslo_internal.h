@@ -120,6 +120,16 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
 // (identity = zeros). *d_bad set when a point fails to decode.
 void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
                            uint8_t* d_out, int* d_bad, cudaStream_t s);
+// Batched checks with R decoded ahead (side stream, overlapping the hashing):
+// d_pts n x 128 B (extended coordinates), d_ok n bytes; check_split runs 8
+// lanes per check on the radix-256 combs; segfold_decoded folds decoded points.
+constexpr size_t kPointBytes = 128;
+void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s);
+void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n, const uint32_t* d_e,
+                        const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                        cudaStream_t s);
+void launch_segfold_decoded(const void* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
+                            uint8_t* d_out, cudaStream_t s);
 // Radix-256 tables (kComb256TableBytes) for the thread-per-check path.
 void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s);
 void launch_group_check_comb(const void* d_tabY, const void* d_tabB, const void* d_tabY256,
