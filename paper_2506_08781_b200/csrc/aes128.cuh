@@ -53,6 +53,21 @@ PHD uint32_t byte_of(uint32_t x, int k) { return (x >> (8 * k)) & 0xffu; }
 
 // Encrypts `in` under `key` (both 4 memory words); round keys are expanded
 // on the fly alongside the rounds (MMO rekeys on every block).
+// Byte assembly of the last round / SubWord: S[x] = byte 1 of T0[x]; picks
+// byte 1 of each of four T0 values into bytes 0..3 (two PRMTs + one).
+PHD uint32_t sbox4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+#ifdef __CUDA_ARCH__
+    const uint32_t ab = __byte_perm(a, b, 0x0051u);  // bytes: a.1, b.1
+    const uint32_t cd = __byte_perm(c, d, 0x0051u);  // bytes: c.1, d.1
+    return __byte_perm(ab, cd, 0x5410u);
+#else
+    return ((a >> 8) & 0xffu) | (b & 0xff00u) | ((c << 8) & 0xff0000u) | ((d << 16) & 0xff000000u);
+#endif
+}
+
+// Encrypts `in` under `key` (both 4 memory words); round keys are expanded
+// on the fly alongside the rounds (MMO rekeys on every block). The T-table
+// functor supplies lk(w, k) = T0[byte k of w].
 template <class T0>
 PHD void aes128_encrypt(const T0& t0, const uint32_t key[4], const uint32_t in[4], uint32_t out[4]) {
     uint32_t k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
@@ -60,10 +75,8 @@ PHD void aes128_encrypt(const T0& t0, const uint32_t key[4], const uint32_t in[4
     uint32_t rcon = 1;
 #pragma unroll
     for (int r = 1; r <= 10; r++) {
-        // next round key: w = SubWord(RotWord(k3)) ^ rcon
-        uint32_t rw = rotr32(k3, 8);
-        uint32_t sw = ((t0(byte_of(rw, 0)) >> 8) & 0xffu) | (t0(byte_of(rw, 1)) & 0xff00u) |
-                      ((t0(byte_of(rw, 2)) << 8) & 0xff0000u) | ((t0(byte_of(rw, 3)) << 16) & 0xff000000u);
+        // next round key: w = SubWord(RotWord(k3)) ^ rcon; RotWord folds into the byte picks
+        const uint32_t sw = sbox4(t0.lk(k3, 1), t0.lk(k3, 2), t0.lk(k3, 3), t0.lk(k3, 0));
         k0 ^= sw ^ rcon;
         k1 ^= k0;
         k2 ^= k1;
@@ -71,24 +84,16 @@ PHD void aes128_encrypt(const T0& t0, const uint32_t key[4], const uint32_t in[4
         rcon = aes_xtime((uint8_t)rcon);
         uint32_t n0, n1, n2, n3;
         if (r < 10) {
-            n0 = t0(byte_of(s0, 0)) ^ rotl32(t0(byte_of(s1, 1)), 8) ^ rotl32(t0(byte_of(s2, 2)), 16) ^
-                 rotl32(t0(byte_of(s3, 3)), 24);
-            n1 = t0(byte_of(s1, 0)) ^ rotl32(t0(byte_of(s2, 1)), 8) ^ rotl32(t0(byte_of(s3, 2)), 16) ^
-                 rotl32(t0(byte_of(s0, 3)), 24);
-            n2 = t0(byte_of(s2, 0)) ^ rotl32(t0(byte_of(s3, 1)), 8) ^ rotl32(t0(byte_of(s0, 2)), 16) ^
-                 rotl32(t0(byte_of(s1, 3)), 24);
-            n3 = t0(byte_of(s3, 0)) ^ rotl32(t0(byte_of(s0, 1)), 8) ^ rotl32(t0(byte_of(s1, 2)), 16) ^
-                 rotl32(t0(byte_of(s2, 3)), 24);
+            n0 = t0.lk(s0, 0) ^ rotl32(t0.lk(s1, 1), 8) ^ rotl32(t0.lk(s2, 2), 16) ^ rotl32(t0.lk(s3, 3), 24);
+            n1 = t0.lk(s1, 0) ^ rotl32(t0.lk(s2, 1), 8) ^ rotl32(t0.lk(s3, 2), 16) ^ rotl32(t0.lk(s0, 3), 24);
+            n2 = t0.lk(s2, 0) ^ rotl32(t0.lk(s3, 1), 8) ^ rotl32(t0.lk(s0, 2), 16) ^ rotl32(t0.lk(s1, 3), 24);
+            n3 = t0.lk(s3, 0) ^ rotl32(t0.lk(s0, 1), 8) ^ rotl32(t0.lk(s1, 2), 16) ^ rotl32(t0.lk(s2, 3), 24);
         } else {
-            // SubBytes + ShiftRows only: S[x] = byte 1 of T0[x]
-            n0 = ((t0(byte_of(s0, 0)) >> 8) & 0xffu) | (t0(byte_of(s1, 1)) & 0xff00u) |
-                 ((t0(byte_of(s2, 2)) << 8) & 0xff0000u) | ((t0(byte_of(s3, 3)) << 16) & 0xff000000u);
-            n1 = ((t0(byte_of(s1, 0)) >> 8) & 0xffu) | (t0(byte_of(s2, 1)) & 0xff00u) |
-                 ((t0(byte_of(s3, 2)) << 8) & 0xff0000u) | ((t0(byte_of(s0, 3)) << 16) & 0xff000000u);
-            n2 = ((t0(byte_of(s2, 0)) >> 8) & 0xffu) | (t0(byte_of(s3, 1)) & 0xff00u) |
-                 ((t0(byte_of(s0, 2)) << 8) & 0xff0000u) | ((t0(byte_of(s1, 3)) << 16) & 0xff000000u);
-            n3 = ((t0(byte_of(s3, 0)) >> 8) & 0xffu) | (t0(byte_of(s0, 1)) & 0xff00u) |
-                 ((t0(byte_of(s1, 2)) << 8) & 0xff0000u) | ((t0(byte_of(s2, 3)) << 16) & 0xff000000u);
+            // SubBytes + ShiftRows only
+            n0 = sbox4(t0.lk(s0, 0), t0.lk(s1, 1), t0.lk(s2, 2), t0.lk(s3, 3));
+            n1 = sbox4(t0.lk(s1, 0), t0.lk(s2, 1), t0.lk(s3, 2), t0.lk(s0, 3));
+            n2 = sbox4(t0.lk(s2, 0), t0.lk(s3, 1), t0.lk(s0, 2), t0.lk(s1, 3));
+            n3 = sbox4(t0.lk(s3, 0), t0.lk(s0, 1), t0.lk(s1, 2), t0.lk(s2, 3));
         }
         s0 = n0 ^ k0;
         s1 = n1 ^ k1;

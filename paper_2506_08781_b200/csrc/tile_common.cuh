@@ -15,6 +15,12 @@ struct SmemT0 {
     const uint32_t* s;
     uint32_t lane;
     PD uint32_t operator()(uint32_t x) const { return s[(x << 5) | lane]; }
+    // T0[byte k of w]: one PRMT (byte extract, ALU) + one IMAD (row address,
+    // FMA pipe) + the LDS, instead of shift/mask/or on the ALU pipe
+    PD uint32_t lk(uint32_t w, int k) const {
+        const uint32_t x = __byte_perm(w, 0u, 0x4440u + (uint32_t)k);
+        return s[x * 32u + lane];
+    }
 };
 
 static __device__ __forceinline__ void load_t0(uint32_t* sT0, const uint32_t* t0g) {

@@ -19,6 +19,7 @@ struct HostT0 {
         for (int x = 0; x < 256; x++) t[x] = aes_t0_entry(aes_sbox_compute(x));
     }
     uint32_t operator()(uint32_t x) const { return t[x]; }
+    uint32_t lk(uint32_t w, int k) const { return t[(w >> (8 * k)) & 0xffu]; }
 };
 const HostT0& T0() {
     static HostT0 t;
