@@ -208,6 +208,17 @@ struct Prepared {
     int sum_limbs = 8;
 };
 
+// Entries per tile of the generic / variable-length kernels (<= 1024, the
+// kernels' sort buffer). POSLO_VAR_TILE overrides for experiments.
+uint32_t var_tile_entries() {
+    static const uint32_t te = [] {
+        const char* e = std::getenv("POSLO_VAR_TILE");
+        uint32_t v = e ? (uint32_t)std::atoi(e) : 1024u;
+        return (v >= 128 && v <= 1024) ? v : 1024u;
+    }();
+    return te;
+}
+
 bool is_uniform(const poslo_batch* b) {
     if (!b->epoch_starts) return true;
     for (uint32_t k = 0; k <= b->n_epochs; k++)
@@ -313,13 +324,13 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         else if (P.fast)
             tm.tile_entries = b->n2 <= 128 ? 128 : (b->n2 <= 256 ? 256 : 1024);
         else
-            tm.tile_entries = 1024;
+            tm.tile_entries = var_tile_entries();
         tm.tiles_per_epoch = b->n2 ? (b->n2 + tm.tile_entries - 1) / tm.tile_entries : 0;
         tm.n_tiles = n_ep * tm.tiles_per_epoch;
     } else {
         std::vector<uint4> tiles;
         std::vector<uint32_t> tbegin(n_ep + 1);
-        const uint32_t te = 1024;
+        const uint32_t te = var_tile_entries();
         for (uint32_t k = 0; k < n_ep; k++) {
             tbegin[k] = (uint32_t)tiles.size();
             uint64_t cnt = b->epoch_starts[k + 1] - b->epoch_starts[k];

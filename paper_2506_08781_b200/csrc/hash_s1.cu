@@ -126,22 +126,21 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
                     r0 = 4;
                 } else {
                     const uint4 a = __ldg(pe), b = __ldg(pe + 1);
-                    const uint32_t m[8] = {bswap32(a.x), bswap32(a.y), bswap32(a.z), bswap32(a.w),
-                                           bswap32(b.x), bswap32(b.y), bswap32(b.z), bswap32(b.w)};
+                    const uint32_t r[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};  // little-endian words
                     if (c == 1) {  // m || x
 #pragma unroll
-                        for (int k = 0; k < 8; k++) W[k] = m[k];
+                        for (int k = 0; k < 8; k++) W[k] = bswap32(r[k]);
                         W[8] = x[0]; W[9] = x[1]; W[10] = x[2]; W[11] = x[3];
                         W[12] = 0x80000000u; W[13] = 0; W[14] = 0; W[15] = 384u;
-                    } else {  // 0x01 || m || x
-                        W[0] = 0x01000000u | (m[0] >> 8);
+                    } else {  // 0x01 || m || x: each big-endian word is one PRMT of two raw words
+                        W[0] = __byte_perm(r[0], 1u, 0x4012u);
 #pragma unroll
-                        for (int k = 1; k < 8; k++) W[k] = fshr32(m[k], m[k - 1], 8);
-                        W[8] = fshr32(x[0], m[7], 8);
+                        for (int k = 1; k < 8; k++) W[k] = __byte_perm(r[k - 1], r[k], 0x3456u);
+                        W[8] = __byte_perm(x[0], r[7], 0x7321u);
                         W[9] = fshr32(x[1], x[0], 8);
                         W[10] = fshr32(x[2], x[1], 8);
                         W[11] = fshr32(x[3], x[2], 8);
-                        W[12] = (x[3] << 24) | 0x00800000u;
+                        W[12] = __byte_perm(x[3], 0x80u, 0x0455u);
                         W[13] = 0; W[14] = 0; W[15] = 392u;
                     }
                     sha256_init(st);
