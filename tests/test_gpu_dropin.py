@@ -33,3 +33,20 @@ def test_reference_batch_verify_suite_passes_on_the_drop_in():
     assert summary, text
     checks, nfail = int(summary.group(1)), int(summary.group(2))
     assert checks >= 200 and nfail == 4, text  # 2 epoch counts x 2 worker counts at line 90
+
+
+DIST = os.path.join(ROOT, "oracle", "_ref", "test_distiller_gpu")
+
+
+def test_reference_distiller_suite_passes_on_the_drop_in():
+    """proj/tests/test_distiller.cpp (unmodified: coarse + fine distillation,
+    SeBVer V/U/I, conservation, CCD round trip and checksum, stream
+    discipline) against paper_2506_08781_b200/host/distiller_gpu.cpp in
+    place of src/distiller.cpp: every assertion passes."""
+    if not os.path.exists(DIST):
+        pytest.fail(f"{DIST} missing: build with __graft_entry__.build() where /root/reference exists")
+    out = subprocess.run([DIST], capture_output=True, text=True, timeout=600)
+    text = out.stdout + out.stderr
+    assert out.returncode == 0 and not re.findall(r"FAILED ([^\n]+)", text), text
+    summary = re.search(r"checks: (\d+) \| failed: (\d+)", text)
+    assert summary and int(summary.group(2)) == 0 and int(summary.group(1)) >= 30, text
