@@ -50,3 +50,21 @@ def test_reference_distiller_suite_passes_on_the_drop_in():
     assert out.returncode == 0 and not re.findall(r"FAILED ([^\n]+)", text), text
     summary = re.search(r"checks: (\d+) \| failed: (\d+)", text)
     assert summary and int(summary.group(2)) == 0 and int(summary.group(1)) >= 30, text
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_gpu")
+
+
+def test_reference_acceptance_on_both_drop_ins():
+    """proj/tests/acceptance.cpp (unmodified) on the GPU batch verifier and
+    distiller: every criterion passes except C08, which asserts the CPU group
+    op counters (one double exponentiation per mode-V check); the device check
+    does not bump them by design, as for test_batch_verify.cpp:90."""
+    if not os.path.exists(ACC):
+        pytest.fail(f"{ACC} missing: build with __graft_entry__.build() where /root/reference exists")
+    out = subprocess.run([ACC], capture_output=True, text=True, timeout=1500)
+    text = out.stdout + out.stderr
+    fails = re.findall(r"^(C\d+[ab]?) FAIL", text, re.M)
+    passes = re.findall(r"^(C\d+[ab]?) PASS", text, re.M)
+    assert fails == ["C08"], text
+    assert len(passes) >= 11, text
