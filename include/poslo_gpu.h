@@ -218,6 +218,22 @@ int poslo_gpu_fine_verify(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const 
 int poslo_gpu_aver_f_batch(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const uint8_t y[32],
                            const uint8_t s[32], const uint8_t r[32], uint8_t* verdict, poslo_error* err);
 
+/* ---- signer side: fixtures with the reference's own key derivation ----------
+ * (PoslocSecretKey::kg / sig_epoch, poslo_c.cpp:91-134)
+ * kg_commitments: for each of the n epochs, r-hat_i = sum over j < n2 of
+ * nonce_to_scalar(suite, r_seed, i, j) (primitives.cpp:195-207) and the
+ * public commitment R-hat_i = alpha^r-hat_i; r_hats_out n x 32 B
+ * (ristretto255), r_scalars_out n x 32 B LE or NULL.
+ * sig_epochs: s-hat for every epoch of the batch, = sum_j (r_ij - e_ij y)
+ * = r-hat_i - y e~_i mod l (e~ through the verifier's own hashing of the
+ * batch; the batch's ds must disclose every epoch — the signer's root node
+ * does). y: the secret scalar, 32 B LE. */
+int poslo_gpu_kg_commitments(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t r_seed[16], const uint32_t* epochs,
+                             uint32_t n, uint32_t n2, uint8_t* r_hats_out, uint8_t* r_scalars_out,
+                             poslo_error* err);
+int poslo_gpu_sig_epochs(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t r_seed[16],
+                         const uint8_t y[32], uint8_t* s_hats_out, poslo_error* err);
+
 /* ---- group primitives (group.cpp), batched on the device ----------------------
  * commit_check: out[i] = encode(Y^e[i] * alpha^s[i]) (group.cpp:144-167).
  * Y = identity gives exp_base. */

@@ -248,6 +248,7 @@ int cmd_golden(int argc, char** argv) {
     std::mt19937_64 rng(seed ^ 0xfeedULL);
 
     auto [sk, pk] = PoslocSecretKey::kg(suite);
+    const Bytes sk_fresh = sk.serialize();  // before signing advances it
     Stream st{suite, pk, {}, {}, {}, SeedStack(suite.depth())};
     for (uint32_t i = 0; i < suite.n1; i++) {
         std::vector<Bytes> epoch;
@@ -270,6 +271,7 @@ int cmd_golden(int argc, char** argv) {
     for (size_t k = 0; k < tampers.size(); k++)
         std::printf("%s%llu", k ? "," : "", (unsigned long long)tampers[k]);
     std::printf("],\n\"pk\": \"%s\",\n", hexv(st.pk.serialize()).c_str());
+    std::printf("\"sk\": \"%s\",\n", hexv(sk_fresh).c_str());
     std::printf("\"sigs\": [");
     for (size_t i = 0; i < st.sigs.size(); i++)
         std::printf("%s\"%s\"", i ? "," : "", hexv(st.sigs[i].serialize()).c_str());

@@ -1244,6 +1244,67 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[3
     return ok(err);
 }
 
+int poslo_gpu_kg_commitments(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t r_seed[16], const uint32_t* epochs,
+                             uint32_t n, uint32_t n2, uint8_t* r_hats_out, uint8_t* r_scalars_out,
+                             poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (suite < 1 || suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
+    if (!r_seed || (n && (!epochs || !r_hats_out))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    if (!n) return ok(err);
+    uint32_t rw[4];
+    std::memcpy(rw, r_seed, 16);
+    uint32_t *d_ep, *d_r, *d_zero;
+    UPLOAD(b_epochs, epochs, (size_t)n * 4, d_ep);
+    ENSURE(b_s, (size_t)n * 8, d_r);
+    ENSURE(b_e, (size_t)n * 8, d_zero);
+    CU(cudaMemsetAsync(d_zero, 0, (size_t)n * 32, ctx->stream));
+    launch_nonce_sums(suite, rw, d_ep, n, n2, d_r, ctx->d_t0, ctx->stream);
+    ctx->launches += 1;
+    // R-hat_i = exp_base(r-hat_i) = commit_check(identity, 0, r-hat_i)
+    static const uint8_t identity[32] = {0};
+    int rc = group_check_dev(ctx, identity, n, d_zero, d_r, nullptr, nullptr, r_hats_out, err);
+    if (rc) return rc;
+    if (r_scalars_out) {
+        CU(cudaMemcpyAsync(r_scalars_out, d_r, (size_t)n * 32, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return ok(err);
+}
+
+int poslo_gpu_sig_epochs(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t r_seed[16], const uint8_t y[32],
+                         uint8_t* s_hats_out, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !r_seed || !y || (b->n_epochs && !s_hats_out)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!scalar_canonical(y)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    Guard g(ctx);
+    // sig_epoch (poslo_c.cpp:117-118): every epoch batch holds exactly n2 entries
+    if (b->epoch_starts)
+        for (uint32_t k = 0; k < b->n_epochs; k++)
+            if (b->epoch_starts[k + 1] - b->epoch_starts[k] != b->n2)
+                return set_err(err, POSLO_STATE_ERROR, b->epochs[k], "epoch batch must hold exactly n2 entries");
+    Prepared P;
+    int rc = run_hash(ctx, b, P, err);  // e~ per epoch
+    if (!rc) rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    const uint32_t n = b->n_epochs;
+    if (!n) return ok(err);
+    uint32_t rw[4], yw[8];
+    std::memcpy(rw, r_seed, 16);
+    std::memcpy(yw, y, 32);
+    uint32_t *d_ep, *d_r, *d_out;
+    UPLOAD(b_seg32, b->epochs, (size_t)n * 4, d_ep);
+    ENSURE(b_s, (size_t)n * 8, d_r);
+    ENSURE(b_out_s, (size_t)n * 8, d_out);
+    launch_nonce_sums(b->suite, rw, d_ep, n, b->n2, d_r, ctx->d_t0, ctx->stream);
+    launch_sign_combine(n, d_r, P.d_etilde, yw, d_out, ctx->stream);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(s_hats_out, d_out, (size_t)n * 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return ok(err);
+}
+
 int poslo_gpu_commit_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], const uint8_t* e,
                            const uint8_t* s, uint8_t* out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");

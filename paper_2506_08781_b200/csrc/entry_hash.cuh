@@ -8,6 +8,7 @@
 #pragma once
 #include "aes128.cuh"
 #include "sha256.cuh"
+#include "scalar.cuh"
 
 namespace poslo_gpu {
 
@@ -132,6 +133,49 @@ PHD bool entry_limbs(int suite, const T0& t0, const uint8_t* m, uint32_t L, cons
     uint32_t x[4];
     entry_seed(suite, t0, x0m, j, x);
     return entry_limbs_x(suite, t0, m, L, x, limbs);
+}
+
+// ---- signer side: nonce_to_scalar (primitives.cpp:195-207)
+// r-seed || be32(i) || be32(j) || counter, expanded by expand_wide (:128-146):
+// F(msg || 0x00) || F(msg || 0x01), F = SHA-256 or MDC-2, reduced mod l and
+// retried with the next counter while zero.
+struct NonceMsg {  // the 26-byte expand_wide input
+    uint32_t r[4];  // seed memory words
+    uint32_t i, j, counter, tag;
+    PHDM uint32_t operator()(uint64_t p) const {
+        if (p < 16) return (r[p >> 2] >> (8 * (p & 3))) & 0xffu;
+        if (p < 20) return (i >> (8 * (19 - p))) & 0xffu;
+        if (p < 24) return (j >> (8 * (23 - p))) & 0xffu;
+        return p == 24 ? (counter & 0xffu) : tag;
+    }
+};
+
+template <class T0>
+PHD void nonce_scalar(int suite, const T0& t0, const uint32_t r[4], uint32_t i, uint32_t j, uint32_t out[8]) {
+    for (uint32_t counter = 0;; counter++) {
+        uint32_t limbs[16];
+        for (uint32_t tag = 0; tag < 2; tag++) {
+            NonceMsg nm{{r[0], r[1], r[2], r[3]}, i, j, counter, tag};
+            const int hi = tag ? 7 : 15;  // d0 is the high half of the wide value
+            if (suite == 1) {
+                uint32_t W[16] = {bswap32(r[0]), bswap32(r[1]), bswap32(r[2]), bswap32(r[3]), i, j,
+                                  (counter & 0xffu) << 24 | tag << 16 | 0x8000u, 0, 0, 0, 0, 0, 0, 0, 0, 208u};
+                uint32_t H[8];
+                sha256_init(H);
+                sha256_compress(H, W);
+                for (int k = 0; k < 8; k++) limbs[hi - k] = H[k];
+            } else {
+                uint32_t h[4], h2[4];
+                mdc2_hash_dev(t0, nm, 26, h, h2);
+                for (int k = 0; k < 4; k++) {
+                    limbs[hi - k] = bswap32(h[k]);
+                    limbs[hi - 4 - k] = bswap32(h2[k]);
+                }
+            }
+        }
+        sc_reduce_limbs(limbs, 16, out);
+        if (!sc_is_zero(out)) return;
+    }
 }
 
 // ---- fast path, suite 1, 32-byte entry: m as 8 big-endian words, x0w the

@@ -57,6 +57,12 @@ void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d
 void launch_fine_scalars(int suite, const EntryLayout& lay, uint64_t n, const uint4* d_seeds, const uint32_t* d_dslot,
                          const uint32_t* d_j, const uint4* d_x0, uint32_t* d_e, unsigned long long* d_err,
                          const uint32_t* d_t0, cudaStream_t s);
+// Signer side (kg / sig_epoch): per-epoch nonce sums r-hat (8 limbs) and
+// s-hat = r-hat - y e~ mod l.
+void launch_nonce_sums(int suite, const uint32_t r_words[4], const uint32_t* d_epochs, uint32_t n, uint32_t n2,
+                       uint32_t* d_out, const uint32_t* d_t0, cudaStream_t s);
+void launch_sign_combine(uint32_t n, const uint32_t* d_rhat, const uint32_t* d_e, const uint32_t y_words[8],
+                         uint32_t* d_out, cudaStream_t s);
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s);
 

@@ -184,3 +184,47 @@ PHD bool sc_is_zero(const uint32_t a[8]) {
     for (int i = 0; i < 8; i++) x |= a[i];
     return x == 0;
 }
+
+// (a * b) mod l for canonical a, b (Scalar::mul, group.cpp:82-87): the
+// 512-bit product by column sums, then one Horner reduction.
+PHD void sc_mul(const uint32_t a[8], const uint32_t b[8], uint32_t out[8]) {
+    uint32_t t[16];
+    uint64_t carry = 0;
+    for (int k = 0; k < 15; k++) {
+        uint64_t lo = carry & 0xffffffffu, hi = carry >> 32;
+        for (int i = 0; i < 8; i++) {
+            const int j = k - i;
+            if (j < 0 || j > 7) continue;
+            const uint64_t p = (uint64_t)a[i] * b[j];
+            lo += p & 0xffffffffu;
+            hi += p >> 32;
+        }
+        hi += lo >> 32;
+        t[k] = (uint32_t)lo;
+        carry = hi;
+    }
+    t[15] = (uint32_t)carry;
+    sc_reduce_limbs(t, 16, out);
+}
+
+// (a - b) mod l for canonical a, b (Scalar::sub): a + (l - b), reduced.
+PHD void sc_sub(const uint32_t a[8], const uint32_t b[8], uint32_t out[8]) {
+    const uint32_t L[8] = {SC_L0, SC_L1, SC_L2, SC_L3, 0, 0, 0, SC_L7};
+    uint32_t nb[8];
+    int64_t bw = 0;
+    for (int i = 0; i < 8; i++) {  // l - b >= 1 for b < l (and = l for b = 0, reduced below)
+        const int64_t t = (int64_t)L[i] - b[i] + bw;
+        nb[i] = (uint32_t)t;
+        bw = t >> 32;
+    }
+    uint32_t sum[9];
+    uint64_t c = 0;
+    for (int i = 0; i < 8; i++) {
+        c += (uint64_t)a[i] + nb[i];
+        sum[i] = (uint32_t)c;
+        c >>= 32;
+    }
+    sum[8] = (uint32_t)c;
+    sc_reduce_limbs(sum, 9, out);
+}
+

@@ -158,6 +158,60 @@ __global__ void __launch_bounds__(128) k_fine_scalars(int suite, EntryLayout lay
     for (int k = 0; k < 8; k++) e_out[t * 8 + k] = e[k];
 }
 
+// ---------------------------------------------------------------- signer side
+// kg's commitment scalars r-hat_i = sum_j nonce_to_scalar(r, i, j) mod l
+// (poslo_c.cpp:104-110): one CTA per epoch, entries strided over the threads.
+struct Seed4 {
+    uint32_t w[4];
+};
+
+__global__ void __launch_bounds__(256) k_nonce_sums(int suite, Seed4 r, const uint32_t* __restrict__ epochs,
+                                                    uint32_t n2, uint32_t* __restrict__ out,
+                                                    const uint32_t* __restrict__ t0g) {
+    extern __shared__ uint32_t sT0[];
+    __shared__ uint32_t red[8 * 17];
+    if (suite != 1) load_t0(sT0, t0g);
+    SmemT0 t0{sT0, threadIdx.x & 31u};
+    const uint32_t i = epochs[blockIdx.x];
+    uint32_t acc[17];
+    acc17_zero(acc);
+    for (uint32_t j = threadIdx.x; j < n2; j += blockDim.x) {
+        uint32_t s[8], v[17];
+        nonce_scalar(suite, t0, r.w, i, j, s);
+#pragma unroll
+        for (int k = 0; k < 17; k++) v[k] = k < 8 ? s[k] : 0u;
+        acc17_add17(acc, v);
+    }
+    block_reduce_acc17(acc, red);
+    if (threadIdx.x == 0) {
+        uint32_t e[8];
+        sc_reduce_limbs(acc, 17, e);
+#pragma unroll
+        for (int k = 0; k < 8; k++) out[(size_t)blockIdx.x * 8 + k] = e[k];
+    }
+}
+
+// sig_epoch's s-hat_i = sum_j (r_ij - e_ij y) = r-hat_i - y e~_i mod l (poslo_c.cpp:115-134)
+struct Scalar8 {
+    uint32_t w[8];
+};
+
+__global__ void k_sign_combine(uint32_t n, const uint32_t* __restrict__ r_hat, const uint32_t* __restrict__ e,
+                               Scalar8 y, uint32_t* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint32_t rr[8], ee[8], p[8], o[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        rr[q] = r_hat[(size_t)k * 8 + q];
+        ee[q] = e[(size_t)k * 8 + q];
+    }
+    sc_mul(y.w, ee, p);
+    sc_sub(rr, p, o);
+#pragma unroll
+    for (int q = 0; q < 8; q++) out[(size_t)k * 8 + q] = o[q];
+}
+
 // ---------------------------------------------------------------- generic K1+K2
 __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay, TileMap tm,
                                                       const uint4* __restrict__ x0,
@@ -369,6 +423,24 @@ void launch_fine_scalars(int suite, const EntryLayout& lay, uint64_t n, const ui
     if (smem) cudaFuncSetAttribute(k_fine_scalars, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_fine_scalars<<<(unsigned)((n + 127) / 128), 128, smem, s>>>(suite, lay, n, d_seeds, d_dslot, d_j, d_x0, d_e,
                                                                  d_err, d_t0);
+}
+
+void launch_nonce_sums(int suite, const uint32_t r_words[4], const uint32_t* d_epochs, uint32_t n, uint32_t n2,
+                       uint32_t* d_out, const uint32_t* d_t0, cudaStream_t s) {
+    if (!n) return;
+    Seed4 r;
+    for (int k = 0; k < 4; k++) r.w[k] = r_words[k];
+    size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
+    if (smem) cudaFuncSetAttribute(k_nonce_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_nonce_sums<<<n, 256, smem, s>>>(suite, r, d_epochs, n2, d_out, d_t0);
+}
+
+void launch_sign_combine(uint32_t n, const uint32_t* d_rhat, const uint32_t* d_e, const uint32_t y_words[8],
+                         uint32_t* d_out, cudaStream_t s) {
+    if (!n) return;
+    Scalar8 y;
+    for (int k = 0; k < 8; k++) y.w[k] = y_words[k];
+    k_sign_combine<<<(n + 127) / 128, 128, 0, s>>>(n, d_rhat, d_e, y, d_out);
 }
 
 void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,

@@ -119,6 +119,28 @@ void dm_ots_spec(const uint8_t x0[16], uint32_t j, uint8_t out[16]) {
     }
 }
 
+// signer side: r-hat_i = sum_j nonce_to_scalar(r, i, j) mod l (kg, poslo_c.cpp:104-110)
+void dm_nonce_sum(int suite, const uint8_t r[16], uint32_t i, uint32_t n2, uint8_t out[32]) {
+    uint32_t rm[4], acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    words_le(r, rm, 4);
+    for (uint32_t j = 0; j < n2; j++) {
+        uint32_t s[8];
+        nonce_scalar(suite, T0(), rm, i, j, s);
+        sc_add(acc, s, acc);
+    }
+    le_words_out(acc, out, 8);
+}
+
+void dm_sc_mul_sub(const uint8_t r[32], const uint8_t y[32], const uint8_t e[32], uint8_t out[32]) {
+    uint32_t rr[8], yy[8], ee[8], p[8], o[8];
+    words_le(r, rr, 8);
+    words_le(y, yy, 8);
+    words_le(e, ee, 8);
+    sc_mul(yy, ee, p);
+    sc_sub(rr, p, o);
+    le_words_out(o, out, 8);
+}
+
 // sum of n 16-limb values via the 17-limb accumulator, reduced mod l
 void dm_sum_reduce(const uint32_t* limbs16, uint32_t n, uint8_t e_out[32]) {
     uint32_t acc[17];

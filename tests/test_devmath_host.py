@@ -141,3 +141,40 @@ def test_group_ops(dm, kat):
         o = out(32)
         assert dm.dm_fold(2, bytes.fromhex(a) + bytes.fromhex(b), o) == 0
         assert o.raw.hex() == c
+
+
+def test_signer_math_matches_reference_keys(dm):
+    """kg / sig_epoch on the device math: R-hat_i =
+    alpha^(sum_j nonce_to_scalar(r, i, j)) equals the reference's public key,
+    and s-hat_i = r-hat_i - y e~_i its epoch signatures (untampered epochs)."""
+    import json
+    import os
+    import struct
+    from conftest import GOLDEN
+    from golden_util import Stream
+    for name in ("stream_s1_tamper", "stream_s2_mixed", "stream_s3_mixed"):
+        g = json.load(open(os.path.join(GOLDEN, name + ".json")))
+        st = Stream(g)
+        sk = bytes.fromhex(g["sk"])
+        assert sk[:4] == b"PSKC"
+        y_le = sk[17:49][::-1]
+        r = sk[49:65]
+        for i in range(st.n1):
+            o = out(32)
+            dm.dm_nonce_sum(st.suite, r, i, st.n2, o)
+            assert O.ristretto.exp_base(o.raw) == st.pk.r_hats[i], (name, i)
+            if g["epoch_verdicts"][i]:
+                s = out(32)
+                dm.dm_sc_mul_sub(o.raw, y_le, st.e_tilde[i], s)
+                assert s.raw == st.sigs[i].s_hat_le, (name, i)
+
+
+def test_scalar_mul_sub(dm):
+    rng = random.Random(99)
+    for t in range(200):
+        r, y, e = (rng.randrange(O.L) for _ in range(3))
+        if t == 0:
+            r, y, e = 0, O.L - 1, O.L - 1
+        o = out(32)
+        dm.dm_sc_mul_sub(r.to_bytes(32, "little"), y.to_bytes(32, "little"), e.to_bytes(32, "little"), o)
+        assert int.from_bytes(o.raw, "little") == (r - y * e) % O.L
