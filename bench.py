@@ -336,21 +336,33 @@ def main():
         if rc:
             raise RuntimeError(f"{fn.__name__}: {rc} {e.message.decode()}")
 
-    # ---- fixture (untimed): a valid coarse aggregate signature for the whole job
-    e_part = ctypes.create_string_buffer(32)
-    call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), None, e_part)
-    parts = [e_part.raw]
-    if world > 1:
-        parts = MG.all_gather_bytes(e_part.raw)
-    e_hat = sum(int.from_bytes(p, "little") for p in parts) % L_ORDER
+    # ---- fixture (untimed): keys and signatures by the reference's own
+    # derivation (PoslocSecretKey::kg / sig_epoch, poslo_c.cpp:91-134) on the
+    # device: secret y, nonce seed r, seed-tree root; R-hat_i = alpha^(sum_j
+    # nonce_to_scalar(r, i, j)) and s-hat_i = r-hat_i - y e~_i for this rank's
+    # epochs; the coarse aggregate folds them over every rank.
     y = rng.randrange(1, L_ORDER)
-    r_nonce = rng.randrange(1, L_ORDER)
-    s_hat = (r_nonce - e_hat * y) % L_ORDER
-    Y = v.exp_base(y.to_bytes(32, "little"))
-    R = v.exp_base(r_nonce.to_bytes(32, "little"))
-    s_le = s_hat.to_bytes(32, "little")
+    y_le = y.to_bytes(32, "little")
+    r_seed = bytes(rng.getrandbits(8) for _ in range(16))
+    ep_arr = np.ascontiguousarray(epochs)
+    r_hats_buf = ctypes.create_string_buffer(max(n1_local, 1) * 32)
+    call(lib.poslo_gpu_kg_commitments, a.suite, r_seed, ctypes.c_void_p(ep_arr.ctypes.data), n1_local, a.n2,
+         r_hats_buf, None)
+    s_hats_buf = ctypes.create_string_buffer(max(n1_local, 1) * 32)
+    call(lib.poslo_gpu_sig_epochs, ctypes.byref(bdev), r_seed, y_le, s_hats_buf)
+    r_enc, s_bytes = r_hats_buf.raw[:32 * n1_local], s_hats_buf.raw[:32 * n1_local]
+    R_part = v.group_fold([r_enc[32 * k:32 * k + 32] for k in range(n1_local)])
+    S_part = v.scalar_sum([s_bytes[32 * k:32 * k + 32] for k in range(n1_local)])
+    if world > 1:
+        R_all, S_all = MG.all_gather_bytes(R_part), MG.all_gather_bytes(S_part)
+    else:
+        R_all, S_all = [R_part], [S_part]
+    R = v.group_fold(R_all)
+    s_le = v.scalar_sum(S_all)
+    Y = v.exp_base(y_le)
     Yb, Sb, Rb = (ctypes.create_string_buffer(x, 32) for x in (Y, s_le, R))
     verdict = ctypes.c_uint8(0)
+    e_part = ctypes.create_string_buffer(32)
 
     def step_single(b):
         call(lib.poslo_gpu_paver, ctypes.byref(b), Yb, Sb, Rb, None, ctypes.byref(verdict))
@@ -372,16 +384,8 @@ def main():
     step = step_single if world == 1 else step_multi
 
     if a.mode == "epoch":
-        # per-epoch signatures (s_i, R_i = alpha^{r_i}, s_i = r_i - e~_i y): one
+        # per-epoch signatures (kg/sig_epoch derivation above): one
         # verdict per epoch, no cross-rank exchange except the verdict count
-        et = ctypes.create_string_buffer(n1_local * 32)
-        call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), et, None)
-        r_list = [rng.randrange(1, L_ORDER) for _ in range(n1_local)]
-        et_raw = et.raw
-        s_bytes = b"".join(((r_list[k] - int.from_bytes(et_raw[32 * k:32 * k + 32], "little") * y) % L_ORDER)
-                           .to_bytes(32, "little") for k in range(n1_local))
-        r_enc = b"".join(v.commit_check_batch(bytes(32), [bytes(32)] * n1_local,
-                                              [r.to_bytes(32, "little") for r in r_list]))
         s_buf = ctypes.create_string_buffer(s_bytes, len(s_bytes))
         r_buf = ctypes.create_string_buffer(r_enc, len(r_enc))
         # signatures are inputs too: resident in HBM for the device-timed steps
@@ -407,14 +411,6 @@ def main():
         # per-epoch signatures as in epoch mode, then k seeded entries tampered (one bit
         # flipped after signing); a step distils every epoch: per-epoch verdicts (the
         # invalid-epoch list) + valid (s, R) folded per umbrella piece on the device
-        et = ctypes.create_string_buffer(n1_local * 32)
-        call(lib.poslo_gpu_agg_ekeys, ctypes.byref(bdev), et, None)
-        r_list = [rng.randrange(1, L_ORDER) for _ in range(n1_local)]
-        et_raw = et.raw
-        s_bytes = b"".join(((r_list[k] - int.from_bytes(et_raw[32 * k:32 * k + 32], "little") * y) % L_ORDER)
-                           .to_bytes(32, "little") for k in range(n1_local))
-        r_enc = b"".join(v.commit_check_batch(bytes(32), [bytes(32)] * n1_local,
-                                              [r.to_bytes(32, "little") for r in r_list]))
         s_buf = ctypes.create_string_buffer(s_bytes, len(s_bytes))
         r_buf = ctypes.create_string_buffer(r_enc, len(r_enc))
         s_dev = torch.frombuffer(bytearray(s_bytes), dtype=torch.uint8).cuda()
@@ -592,7 +588,7 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "entries/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic (counter-based log, include/poslo_synth.h)",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (counter-based log, include/poslo_synth.h); keys and signatures by the reference's kg/sig_epoch derivation, on the device",
         "config": config_dict(a, world),
         "e2e": e2e,
         "roofline": roof,
