@@ -3,6 +3,7 @@
 // the R-hat fold of paver (batch_verify.cpp:75-81, group_combine
 // group.cpp:169-178) and point validation (GroupElement::from_bytes,
 // group.cpp:107-114). One thread per check; folds are block trees.
+#define POSLO_FE_CALL 1  // out-of-line field multiplication in the group kernels (i-cache)
 #include "poslo_internal.h"
 #include "ristretto.cuh"
 
@@ -295,22 +296,25 @@ __global__ void __launch_bounds__(128) k_check_split(const gcached* __restrict__
             dsg[k & 3] = b - (cs << 8);
         }
     }
-    gpt acc = pt_identity();
+    // one addition site for the 8 windows (e then s per window): a rolled loop
+    // keeps the kernel small enough for the instruction cache
+    uint32_t pe = 0, ps = 0;  // the four signed digits, one per byte
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-        const int k = 4 * (int)sub + q;
-        if (de[q]) {
-            const int a = de[q] < 0 ? -de[q] : de[q];
-            const gcached c = tabY[128 * k + a - 1];
-            acc = pt_add_cached(acc, de[q] < 0 ? cached_neg(c) : c);
-        }
-        if (dsg[q]) {
-            const int a = dsg[q] < 0 ? -dsg[q] : dsg[q];
-            const gcached c = tabB[128 * k + a - 1];
-            acc = pt_add_cached(acc, dsg[q] < 0 ? cached_neg(c) : c);
-        }
+        pe |= ((uint32_t)de[q] & 0xffu) << (8 * q);
+        ps |= ((uint32_t)dsg[q] & 0xffu) << (8 * q);
     }
-#pragma unroll
+    gpt acc = pt_identity();
+#pragma unroll 1
+    for (int t = 0; t < 8; t++) {
+        const int q = t >> 1;
+        const int dig = (int)(int8_t)(((t & 1) ? ps : pe) >> (8 * q));
+        if (!dig) continue;
+        const int a = dig < 0 ? -dig : dig;
+        const gcached c = ((t & 1) ? tabB : tabY)[128 * (4 * (int)sub + q) + a - 1];
+        acc = pt_add_cached(acc, dig < 0 ? cached_neg(c) : c);
+    }
+#pragma unroll 1
     for (int off = 4; off >= 1; off >>= 1) {
         const gpt o = shfl_pt(acc, off);
         if (sub < (uint32_t)off) acc = pt_add(acc, o);

@@ -116,9 +116,21 @@ __device__ __forceinline__ fe fe_mul_ptx(const fe& a, const fe& b) {
 // is summed on its own (96-bit column accumulators), so only the final carry
 // sweep is serial — short dependency chains for the latency-bound single-
 // check path, where the old row-by-row carry chain dominated.
+#if defined(__CUDA_ARCH__) && defined(POSLO_FE_CALL)
+// Out-of-line field multiplication (~170 SASS instructions): the group
+// kernels call it instead of inlining it at every use, which keeps a point
+// addition at a few hundred instructions and the kernels inside the
+// instruction cache (inlined, k_check_split stalled on no_instruction).
+__device__ __noinline__ fe fe_mul_call(fe a, fe b) { return fe_mul_ptx(a, b); }
+#endif
+
 PHD fe fe_mul(const fe& a, const fe& b) {
 #ifdef __CUDA_ARCH__
+#ifdef POSLO_FE_CALL
+    return fe_mul_call(a, b);
+#else
     return fe_mul_ptx(a, b);
+#endif
 #endif
     uint32_t t[16];
     uint64_t carry = 0;  // < 2^36
