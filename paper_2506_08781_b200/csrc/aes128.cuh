@@ -73,28 +73,37 @@ PHD void aes128_encrypt(const T0& t0, const uint32_t key[4], const uint32_t in[4
     uint32_t k0 = key[0], k1 = key[1], k2 = key[2], k3 = key[3];
     uint32_t s0 = in[0] ^ k0, s1 = in[1] ^ k1, s2 = in[2] ^ k2, s3 = in[3] ^ k3;
     uint32_t rcon = 1;
-#pragma unroll
-    for (int r = 1; r <= 10; r++) {
+    // rounds 1..9 as a rolled loop: one copy of the round code per call site
+    // (17 AES per 32-byte suite-2 entry; unrolled they overflow the
+    // instruction cache), then the final round without MixColumns
+#pragma unroll 1
+    for (int r = 1; r < 10; r++) {
         // next round key: w = SubWord(RotWord(k3)) ^ rcon; RotWord folds into the byte picks
         const uint32_t sw = sbox4(t0.lk(k3, 1), t0.lk(k3, 2), t0.lk(k3, 3), t0.lk(k3, 0));
         k0 ^= sw ^ rcon;
         k1 ^= k0;
         k2 ^= k1;
         k3 ^= k2;
-        rcon = aes_xtime((uint8_t)rcon);
-        uint32_t n0, n1, n2, n3;
-        if (r < 10) {
-            n0 = t0.lk(s0, 0) ^ rotl32(t0.lk(s1, 1), 8) ^ rotl32(t0.lk(s2, 2), 16) ^ rotl32(t0.lk(s3, 3), 24);
-            n1 = t0.lk(s1, 0) ^ rotl32(t0.lk(s2, 1), 8) ^ rotl32(t0.lk(s3, 2), 16) ^ rotl32(t0.lk(s0, 3), 24);
-            n2 = t0.lk(s2, 0) ^ rotl32(t0.lk(s3, 1), 8) ^ rotl32(t0.lk(s0, 2), 16) ^ rotl32(t0.lk(s1, 3), 24);
-            n3 = t0.lk(s3, 0) ^ rotl32(t0.lk(s0, 1), 8) ^ rotl32(t0.lk(s1, 2), 16) ^ rotl32(t0.lk(s2, 3), 24);
-        } else {
-            // SubBytes + ShiftRows only
-            n0 = sbox4(t0.lk(s0, 0), t0.lk(s1, 1), t0.lk(s2, 2), t0.lk(s3, 3));
-            n1 = sbox4(t0.lk(s1, 0), t0.lk(s2, 1), t0.lk(s3, 2), t0.lk(s0, 3));
-            n2 = sbox4(t0.lk(s2, 0), t0.lk(s3, 1), t0.lk(s0, 2), t0.lk(s1, 3));
-            n3 = sbox4(t0.lk(s3, 0), t0.lk(s0, 1), t0.lk(s1, 2), t0.lk(s2, 3));
-        }
+        rcon = (rcon << 1) ^ ((rcon & 0x80u) ? 0x11bu : 0u);
+        const uint32_t n0 = t0.lk(s0, 0) ^ rotl32(t0.lk(s1, 1), 8) ^ rotl32(t0.lk(s2, 2), 16) ^ rotl32(t0.lk(s3, 3), 24);
+        const uint32_t n1 = t0.lk(s1, 0) ^ rotl32(t0.lk(s2, 1), 8) ^ rotl32(t0.lk(s3, 2), 16) ^ rotl32(t0.lk(s0, 3), 24);
+        const uint32_t n2 = t0.lk(s2, 0) ^ rotl32(t0.lk(s3, 1), 8) ^ rotl32(t0.lk(s0, 2), 16) ^ rotl32(t0.lk(s1, 3), 24);
+        const uint32_t n3 = t0.lk(s3, 0) ^ rotl32(t0.lk(s0, 1), 8) ^ rotl32(t0.lk(s1, 2), 16) ^ rotl32(t0.lk(s2, 3), 24);
+        s0 = n0 ^ k0;
+        s1 = n1 ^ k1;
+        s2 = n2 ^ k2;
+        s3 = n3 ^ k3;
+    }
+    {  // round 10: SubBytes + ShiftRows + AddRoundKey (rcon = 0x36 here)
+        const uint32_t sw = sbox4(t0.lk(k3, 1), t0.lk(k3, 2), t0.lk(k3, 3), t0.lk(k3, 0));
+        k0 ^= sw ^ rcon;
+        k1 ^= k0;
+        k2 ^= k1;
+        k3 ^= k2;
+        const uint32_t n0 = sbox4(t0.lk(s0, 0), t0.lk(s1, 1), t0.lk(s2, 2), t0.lk(s3, 3));
+        const uint32_t n1 = sbox4(t0.lk(s1, 0), t0.lk(s2, 1), t0.lk(s3, 2), t0.lk(s0, 3));
+        const uint32_t n2 = sbox4(t0.lk(s2, 0), t0.lk(s3, 1), t0.lk(s0, 2), t0.lk(s1, 3));
+        const uint32_t n3 = sbox4(t0.lk(s3, 0), t0.lk(s0, 1), t0.lk(s1, 2), t0.lk(s2, 3));
         s0 = n0 ^ k0;
         s1 = n1 ^ k1;
         s2 = n2 ^ k2;

@@ -198,8 +198,11 @@ PHD void mdc2_digest_limbs(const T0& t0, const uint32_t blk[16],
                                                   uint32_t limbs_hi_index, uint32_t limbs[16]) {
     uint32_t h[4] = {MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD, MMO_IV_WORD};
     uint32_t h2[4] = {MDC2_IV2_WORD, MDC2_IV2_WORD, MDC2_IV2_WORD, MDC2_IV2_WORD};
-#pragma unroll
-    for (int b = 0; b < 4; b++) mdc2_step(t0, h, h2, blk + 4 * b);
+#pragma unroll 1
+    for (int b = 0; b < 4; b++) {  // rolled: one copy of the two AES per call site
+        const uint32_t m[4] = {blk[4 * b], blk[4 * b + 1], blk[4 * b + 2], blk[4 * b + 3]};
+        mdc2_step(t0, h, h2, m);
+    }
     // digest bytes h || h2 read as big-endian words 0..7
 #pragma unroll
     for (int k = 0; k < 4; k++) {
