@@ -193,45 +193,64 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
             L = lay.entry_len;
         }
         v.L = (uint32_t)L;
-        {  // x = onetime_seed(x0, j), resumed at round 4; kept in the slot tail (bytes, stream order)
-            uint32_t W[16], st[8];
-#pragma unroll
-            for (int k = 0; k < 4; k++) W[k] = s_x0w[k];
-            W[4] = j;
-            W[5] = 0x80000000u;
-#pragma unroll
-            for (int k = 6; k < 15; k++) W[k] = 0;
-            W[15] = 160u;
-#pragma unroll
-            for (int k = 0; k < 8; k++) st[k] = s_pre[k];
-            sha256_rounds_compact<2>(st, W, 4, pk);
-            const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
-#pragma unroll
-            for (int k = 0; k < 4; k++) v.slot[24 + k] = bswap32(st[k] + iv[k]);
-        }
+        // One job loop shares ONE copy of the compression code (the kernel
+        // stays inside the instruction cache): job 0 is x = onetime_seed(x0, j)
+        // (resumed at round 4), then block b of stream 0 and of stream 1
+        // alternate; Hc/Ho are the current/other stream's chaining values,
+        // swapped after every job so both stay in registers.
         const uint32_t nb0 = nblocks(L + 16), nb1 = nblocks(L + 17);
-        uint32_t H0[8], H1[8];
-        sha256_init(H0);
-        sha256_init(H1);
+        uint32_t Hc[8], Ho[8];
+        sha256_init(Hc);
+        sha256_init(Ho);
 #pragma unroll 1
-        for (uint32_t b = 0; b < nb1; b++) {
-            stage_window(v, b);
-            uint32_t W[16];
-            if (b < nb0) {
-                load_block(v, b, 0, W);
-                if (b == nb0 - 1) {
-                    W[14] = (uint32_t)(((L + 16) * 8) >> 32);
-                    W[15] = (uint32_t)((L + 16) * 8);
+        for (uint32_t job = 0; job <= 2 * nb1; job++) {
+            uint32_t W[16], st[8];
+            int r0 = 0;
+            bool active = true;
+            if (job == 0) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) W[k] = s_x0w[k];
+                W[4] = j;
+                W[5] = 0x80000000u;
+#pragma unroll
+                for (int k = 6; k < 15; k++) W[k] = 0;
+                W[15] = 160u;
+#pragma unroll
+                for (int k = 0; k < 8; k++) st[k] = s_pre[k];
+                r0 = 4;
+            } else {
+                const uint32_t b = (job - 1) >> 1, stream = (job - 1) & 1;
+                if (!stream) stage_window(v, b);
+                active = stream || b < nb0;
+                if (active) {
+                    load_block(v, b, stream, W);
+                    const uint32_t nb = stream ? nb1 : nb0;
+                    if (b == nb - 1) {
+                        const uint64_t bits = (L + 16 + stream) * 8;
+                        W[14] = (uint32_t)(bits >> 32);
+                        W[15] = (uint32_t)bits;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; k++) st[k] = Hc[k];
                 }
-                compress_into(H0, W, pk);
             }
-            load_block(v, b, 1, W);
-            if (b == nb1 - 1) {
-                W[14] = (uint32_t)(((L + 17) * 8) >> 32);
-                W[15] = (uint32_t)((L + 17) * 8);
+            if (active) sha256_rounds_compact<2>(st, W, r0, pk);
+            if (job == 0) {  // x kept in the slot tail (bytes in stream order) for the suffix writes
+                const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
+#pragma unroll
+                for (int k = 0; k < 4; k++) v.slot[24 + k] = bswap32(st[k] + iv[k]);
+                continue;
             }
-            compress_into(H1, W, pk);
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint32_t c = active ? Hc[k] + st[k] : Hc[k];
+                Hc[k] = Ho[k];
+                Ho[k] = c;
+            }
         }
+        // an even number of swaps: Hc is stream 0 (H0), Ho stream 1 (H1)
+        uint32_t* H0 = Hc;
+        uint32_t* H1 = Ho;
         // H0 is the high half of the 512-bit wide value: digest word k is limb 7 - k of its half
         uint32_t d[8];
 #pragma unroll
