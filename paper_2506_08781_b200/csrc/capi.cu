@@ -232,9 +232,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     if (!b) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null batch");
     if (b->suite < 1 || b->suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
     if (b->n_epochs && !b->epochs) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null epochs");
-    for (uint32_t k = 1; k < b->n_epochs; k++)
-        if (b->epochs[k] <= b->epochs[k - 1])
-            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epochs must be strictly ascending");
+    // (the strictly-ascending check of `epochs` runs on the host after the
+    // kernels are queued, overlapping them; see the end of this function)
     DsParam ds;
     int rc = POSLO_OK;
     std::vector<SeedStart> starts;  // per-epoch stacks: resolved covering nodes
@@ -297,7 +296,10 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     mark(ctx, kEvSeed);
     ctx->stage->err_init = host_err;
     CU(cudaMemcpyAsync(d_err, &ctx->stage->err_init, 8, cudaMemcpyHostToDevice, s));
-    if (n_ep) CU(cudaMemcpyAsync(d_epochs, b->epochs, (size_t)n_ep * 4, cudaMemcpyHostToDevice, s));
+    // a contiguous epoch range (every full verification) needs no list upload;
+    // with the ascending check below, last - first == n - 1 proves contiguity
+    const bool contiguous = n_ep > 0 && b->epochs[n_ep - 1] - b->epochs[0] == n_ep - 1;
+    if (n_ep && !contiguous) CU(cudaMemcpyAsync(d_epochs, b->epochs, (size_t)n_ep * 4, cudaMemcpyHostToDevice, s));
     if (b->ds_offsets) {
         SeedStart* d_starts;
         ENSURE(b_starts_ds, std::max<size_t>(starts.size(), 1), d_starts);
@@ -306,7 +308,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         CU(cudaStreamSynchronize(s));  // `starts` is a host vector
         launch_seed_walk(b->suite, d_starts, n_ep, d_x0, ctx->d_t0, s);
     } else {
-        launch_seed_derive(b->suite, ds, d_epochs, n_ep, d_x0, d_err, ctx->d_t0, s);
+        launch_seed_derive(b->suite, ds, contiguous ? nullptr : d_epochs, n_ep ? b->epochs[0] : 0, n_ep, d_x0, d_err,
+                           ctx->d_t0, s);
     }
     ctx->launches += n_ep ? 1 : 0;
     mark(ctx, kEvHash);
@@ -414,6 +417,12 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         ctx->launches += 1;
     }
     CU(cudaGetLastError());
+    // host-side argument check, overlapping the queued device work
+    for (uint32_t k = 1; k < n_ep; k++)
+        if (b->epochs[k] <= b->epochs[k - 1]) {
+            cudaStreamSynchronize(s);
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epochs must be strictly ascending");
+        }
     return POSLO_OK;
 }
 
@@ -1379,7 +1388,7 @@ int poslo_gpu_seed_retrieve(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t* ds
     ENSURE(b_err, 1, d_err);
     unsigned long long init = ~0ull;
     CU(cudaMemcpyAsync(d_err, &init, 8, cudaMemcpyHostToDevice, ctx->stream));
-    launch_seed_derive(suite, dsp, d_ep, n, d_x0, d_err, ctx->d_t0, ctx->stream);
+    launch_seed_derive(suite, dsp, d_ep, 0, n, d_x0, d_err, ctx->d_t0, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     unsigned long long key;

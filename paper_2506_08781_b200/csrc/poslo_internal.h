@@ -63,7 +63,8 @@ void launch_nonce_sums(int suite, const uint32_t r_words[4], const uint32_t* d_e
                        uint32_t* d_out, const uint32_t* d_t0, cudaStream_t s);
 void launch_sign_combine(uint32_t n, const uint32_t* d_rhat, const uint32_t* d_e, const uint32_t y_words[8],
                          uint32_t* d_out, cudaStream_t s);
-void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
+// d_epochs == nullptr: epochs epoch0, epoch0 + 1, ..., epoch0 + n_epochs - 1.
+void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t epoch0, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s);
 
 // Fast path: suite 1, 32-byte entries, uniform epochs. Writes per-tile

@@ -44,20 +44,22 @@ __device__ __forceinline__ void ds_walk(int suite, const T0& t0, uint32_t x[4], 
 // the group is walked on its own, exactly as sr does.
 constexpr int kSeedGroup = 8;
 
-__global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict__ epochs,
+__global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict__ epochs_in, uint32_t epoch0,
                               uint32_t n, uint4* __restrict__ x0, unsigned long long* err,
                               const uint32_t* __restrict__ t0g) {
+    // epochs_in == nullptr: the queried epochs are epoch0, epoch0 + 1, ... (no list upload)
+    auto epochs = [&](uint32_t k) { return epochs_in ? epochs_in[k] : epoch0 + k; };
     extern __shared__ uint32_t sT0[];
     if (suite != 1) load_t0(sT0, t0g);
     SmemT0 t0{sT0, threadIdx.x & 31u};
     const uint32_t k0 = (blockIdx.x * blockDim.x + threadIdx.x) * kSeedGroup;
     if (k0 >= n) return;
-    const uint32_t q0 = epochs[k0];
+    const uint32_t q0 = epochs(k0);
     bool dense = (q0 % kSeedGroup) == 0 && k0 + kSeedGroup <= n;
     int c0 = ds_cover(ds, q0);
     if (dense && c0 >= 0 && ds.nodes[c0].depth >= 3) {
 #pragma unroll
-        for (int i = 1; i < kSeedGroup; i++) dense = dense && epochs[k0 + i] == q0 + i;
+        for (int i = 1; i < kSeedGroup; i++) dense = dense && epochs(k0 + i) == q0 + i;
     } else {
         dense = false;
     }
@@ -83,7 +85,7 @@ __global__ void k_seed_derive(int suite, DsParam ds, const uint32_t* __restrict_
     }
     const uint32_t kend = min(n, k0 + kSeedGroup);
     for (uint32_t k = k0; k < kend; k++) {
-        const uint32_t q = epochs[k];
+        const uint32_t q = epochs(k);
         const int c = ds_cover(ds, q);
         if (c < 0) {
             x0[k] = make_uint4(0, 0, 0, 0);
@@ -396,14 +398,14 @@ __global__ void k_synth_var(uint64_t seed, uint64_t first, uint64_t n, const uin
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
-void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t n_epochs,
+void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t epoch0, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s) {
     if (n_epochs == 0) return;
     int T = 64;
     size_t smem = suite == 1 ? 0 : kAesSmemWords * sizeof(uint32_t);
     if (smem) cudaFuncSetAttribute(k_seed_derive, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t groups = (n_epochs + kSeedGroup - 1) / kSeedGroup;
-    k_seed_derive<<<(groups + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, n_epochs, d_x0, d_err, d_t0);
+    k_seed_derive<<<(groups + T - 1) / T, T, smem, s>>>(suite, ds, d_epochs, epoch0, n_epochs, d_x0, d_err, d_t0);
 }
 
 void launch_seed_walk(int suite, const SeedStart* d_starts, uint32_t n, uint4* d_x0, const uint32_t* d_t0,

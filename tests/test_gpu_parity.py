@@ -376,3 +376,20 @@ def test_device_resident_signatures_match_host(verifier):
     verifier._call(verifier._lib.poslo_gpu_distill_coarse, ctypes.byref(b), pk.y, ctypes.c_void_p(s_dev.data_ptr()),
                    ctypes.c_void_p(r_dev.data_ptr()), ctypes.c_void_p(seg.ctypes.data), 2, verd, so, ro)
     assert [bool(x) for x in verd.raw] == host_verdicts
+
+
+def test_epochs_must_ascend(verifier):
+    """A C-ABI misuse (epochs not strictly ascending) is rejected even though
+    the check runs after the kernels are queued."""
+    api = A()
+    cfg, batches, ds = _synthetic(1, 8, 4, 32, seed=3)
+    pb = api.PackedBatch(1, 4, batches, ds)
+    pb.epochs = pb.epochs[[0, 2, 1, 3, 4, 5, 6, 7]].copy()
+    cb = pb.cstruct()
+    out = __import__("ctypes").create_string_buffer(32 * 8)
+    with pytest.raises(ValueError, match="ascending"):
+        verifier._call(verifier._lib.poslo_gpu_agg_ekeys, __import__("ctypes").byref(cb), out, None)
+    pb.epochs = pb.epochs[[0, 1, 2, 3, 4, 5, 7, 7]].copy()  # last - first == n - 1 but a repeat
+    cb = pb.cstruct()
+    with pytest.raises(ValueError, match="ascending"):
+        verifier._call(verifier._lib.poslo_gpu_agg_ekeys, __import__("ctypes").byref(cb), out, None)
