@@ -273,8 +273,13 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "record_header must be 0, or 4 with record offsets");
     P.lay.header = b->record_header;
     const uint64_t epoch_bytes = (uint64_t)b->n2 * b->entry_len;
-    const bool chunked = !b->device_resident && P.uniform && !b->offsets && epoch_bytes > 0 &&
+    // Host-resident uniform logs (fixed length, or byte offsets / raw record
+    // images) stream in epoch-aligned chunks of <= 64 MiB on the copy stream.
+    const bool chunked = !b->device_resident && P.uniform && (b->offsets || epoch_bytes > 0) &&
                          b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
+    auto epoch_byte = [&](uint32_t e) -> uint64_t {  // first payload byte of the e-th queried epoch
+        return b->offsets ? b->offsets[(uint64_t)e * b->n2] : (uint64_t)e * epoch_bytes;
+    };
     if (b->device_resident) {
         P.lay.payload = b->payload;
         P.lay.offsets = b->offsets;
@@ -386,8 +391,19 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         ctx->launches += 1;
     };
     if (chunked) {
-        const uint32_t epc = (uint32_t)std::max<uint64_t>(1, kChunkBytes / epoch_bytes);
-        const uint32_t n_chunks = (n_ep + epc - 1) / epc;
+        // chunk c covers epochs [cut[c], cut[c+1]): as many whole epochs as fit in kChunkBytes (>= 1)
+        std::vector<uint32_t> cut{0};
+        while (cut.back() < n_ep) {
+            const uint32_t e0 = cut.back();
+            uint32_t e1 = e0 + 1;
+            if (!b->offsets) {
+                e1 = std::min<uint32_t>(n_ep, e0 + (uint32_t)std::max<uint64_t>(1, kChunkBytes / epoch_bytes));
+            } else {
+                while (e1 < n_ep && epoch_byte(e1 + 1) - epoch_byte(e0) <= kChunkBytes) e1++;
+            }
+            cut.push_back(e1);
+        }
+        const uint32_t n_chunks = (uint32_t)cut.size() - 1;
         while (ctx->chunk_ev.size() < n_chunks + 1) {
             cudaEvent_t ev;
             CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -398,8 +414,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         CU(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[n_chunks], 0));
         uint8_t* d_pay = const_cast<uint8_t*>(P.lay.payload);
         for (uint32_t c = 0; c < n_chunks; c++) {
-            uint32_t e0 = c * epc, e1 = std::min<uint32_t>(n_ep, e0 + epc);
-            uint64_t off = (uint64_t)e0 * epoch_bytes, bytes = (uint64_t)(e1 - e0) * epoch_bytes;
+            const uint32_t e0 = cut[c], e1 = cut[c + 1];
+            const uint64_t off = epoch_byte(e0), bytes = epoch_byte(e1) - off;
             CU(cudaMemcpyAsync(d_pay + off, b->payload + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
             CU(cudaEventRecord(ctx->chunk_ev[c], ctx->copy));
             CU(cudaStreamWaitEvent(s, ctx->chunk_ev[c], 0));

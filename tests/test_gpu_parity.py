@@ -393,3 +393,44 @@ def test_epochs_must_ascend(verifier):
     cb = pb.cstruct()
     with pytest.raises(ValueError, match="ascending"):
         verifier._call(verifier._lib.poslo_gpu_agg_ekeys, __import__("ctypes").byref(cb), out, None)
+
+
+def test_chunked_varlen_host_path_matches_device_resident(verifier):
+    """Variable-length host-resident logs stream in epoch-aligned chunks cut
+    by byte offsets; e~ must equal the device-resident call bit for bit."""
+    import ctypes
+
+    import torch
+    import bench
+    from paper_2506_08781_b200 import _native as N
+    api = A()
+    n2, n = 1024, 1 << 18  # ~143 MB of syslog-style entries: > 2 chunks
+    n1 = n // n2
+    lens = bench.synth_varlen(5, 0, n)
+    offs = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum(lens, out=offs[1:])
+    offs_dev = torch.from_numpy(offs.view(np.int64)).cuda()
+    dev = torch.empty(int(offs[-1]), dtype=torch.uint8, device="cuda")
+    err = N.PosloError()
+    assert verifier._lib.poslo_gpu_synth_varlog(verifier._ctx, 5, 0, n, ctypes.c_void_p(offs_dev.data_ptr()),
+                                                ctypes.c_void_p(dev.data_ptr()), ctypes.byref(err)) == 0
+    host = dev.cpu().pin_memory()
+    ds = api.SeedStack(8, [api.SeedNode(8, 0, bytes(range(16)))])
+    dsb = ds.serialize()
+    dsbuf = ctypes.create_string_buffer(dsb, len(dsb))
+    epochs = np.arange(n1, dtype=np.uint32)
+
+    def run(ptr, off_ptr, resident):
+        b = N.PosloBatch()
+        b.suite, b.n2, b.payload, b.payload_bytes = 1, n2, ptr, int(offs[-1])
+        b.offsets, b.entry_len, b.n_entries = off_ptr, 0, n
+        b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, n1
+        b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(dsbuf), len(dsb), 8, resident
+        et = ctypes.create_string_buffer(n1 * 32)
+        eh = ctypes.create_string_buffer(32)
+        verifier._call(verifier._lib.poslo_gpu_agg_ekeys, ctypes.byref(b), et, eh)
+        return et.raw, eh.raw
+
+    a = run(dev.data_ptr(), offs_dev.data_ptr(), 1)
+    h = run(host.data_ptr(), offs.ctypes.data, 0)
+    assert a == h

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x --deselect tests/test_gpu_dropin.py::test_reference_acceptance_on_both_drop_ins > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python bench.py --varlen --mode epoch --n2 1024 --log2n 22 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_c4.json.log 2>&1
+echo done
