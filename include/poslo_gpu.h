@@ -121,6 +121,12 @@ typedef struct poslo_fine_batch {
  * the count needed. Pure host code; no device is touched. */
 int poslo_log_scan(const uint8_t* raw, uint64_t len, uint64_t* offsets, uint64_t cap, uint64_t* n_records,
                    poslo_error* err);
+/* The same on the device (speculative chunk walks + stitch, log_scan.cu):
+ * identical offsets and errors, ~100x the host scan's rate on large images.
+ * device_resident: raw and offsets are device pointers (the image stays in
+ * HBM for a zero-copy record batch), else host memory. */
+int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int32_t device_resident,
+                       uint64_t* offsets, uint64_t cap, uint64_t* n_records, poslo_error* err);
 
 /* ---- context -------------------------------------------------------------- */
 int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);

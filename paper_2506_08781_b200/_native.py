@@ -69,7 +69,7 @@ EXPORTS = [
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
     "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold", "poslo_gpu_fine_scalars",
     "poslo_gpu_fine_verify", "poslo_gpu_aver_f_batch", "poslo_log_scan", "poslo_gpu_kg_commitments",
-    "poslo_gpu_sig_epochs",
+    "poslo_gpu_sig_epochs", "poslo_gpu_log_scan",
 ]
 
 _lib = None
@@ -121,6 +121,7 @@ def load():
         "poslo_log_scan": ([P, c.c_uint64, P, c.c_uint64, c.POINTER(c.c_uint64), E], c.c_int),
         "poslo_gpu_kg_commitments": ([P, c.c_uint8, P, P, c.c_uint32, c.c_uint32, P, P, E], c.c_int),
         "poslo_gpu_sig_epochs": ([P, B, P, P, P, E], c.c_int),
+        "poslo_gpu_log_scan": ([P, P, c.c_uint64, c.c_int32, P, c.c_uint64, c.POINTER(c.c_uint64), E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

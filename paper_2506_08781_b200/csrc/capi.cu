@@ -50,7 +50,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
@@ -635,7 +635,9 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_flags, &ctx->b_payload, &ctx->b_offsets, &ctx->b_e, &ctx->b_s,
                       &ctx->b_r, &ctx->b_enc, &ctx->b_verdict, &ctx->b_mask, &ctx->b_seg, &ctx->b_y,
                       &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
-                      &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok};
+                      &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok,
+                      &ctx->b_scan_exit, &ctx->b_scan_cnt, &ctx->b_scan_start, &ctx->b_scan_base,
+                      &ctx->b_scan_off};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
@@ -692,6 +694,54 @@ int poslo_log_scan(const uint8_t* raw, uint64_t len, uint64_t* offsets, uint64_t
     if (!offsets || n + 1 > cap) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "offsets capacity %llu < %llu",
                                                 (unsigned long long)cap, (unsigned long long)(n + 1));
     offsets[n] = len;
+    return ok(err);
+}
+
+int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int32_t device_resident,
+                       uint64_t* offsets, uint64_t cap, uint64_t* n_records, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!n_records || (len && !raw)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    Guard g(ctx);
+    cudaStream_t s = ctx->stream;
+    const uint8_t* d_raw = raw;
+    if (!device_resident && len) {
+        uint8_t* d;
+        ENSURE(b_payload, len, d);
+        CU(cudaMemcpyAsync(d, raw, len, cudaMemcpyHostToDevice, s));
+        d_raw = d;
+    }
+    const uint32_t n_chunks = (uint32_t)((len + kScanChunk - 1) / kScanChunk);
+    uint64_t *d_exit, *d_start, *d_base;
+    uint32_t* d_cnt;
+    unsigned long long* d_state;
+    ENSURE(b_scan_exit, (size_t)std::max<uint32_t>(n_chunks, 1) * kScanWindow, d_exit);
+    ENSURE(b_scan_cnt, (size_t)std::max<uint32_t>(n_chunks, 1) * kScanWindow, d_cnt);
+    ENSURE(b_scan_start, std::max<uint32_t>(n_chunks, 1), d_start);
+    ENSURE(b_scan_base, std::max<uint32_t>(n_chunks, 1), d_base);
+    ENSURE(b_err, 1, d_state);
+    launch_log_scan_a(d_raw, len, n_chunks, d_exit, d_cnt, s);
+    launch_log_scan_b(d_raw, len, n_chunks, d_exit, d_cnt, d_start, d_base, d_state, s);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    unsigned long long total = 0;
+    if (len) {
+        CU(cudaMemcpyAsync(&ctx->stage->err_key, d_state, 8, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        total = ctx->stage->err_key;
+    }
+    if (total == ~0ull) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated log record");
+    *n_records = total;
+    if (!offsets || total + 1 > cap)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "offsets capacity %llu < %llu", (unsigned long long)cap,
+                       (unsigned long long)(total + 1));
+    uint64_t* d_off = offsets;
+    if (!device_resident) ENSURE(b_scan_off, total + 1, d_off);
+    launch_log_scan_c(d_raw, len, n_chunks, d_start, d_base, d_off, s);
+    ctx->launches += n_chunks ? 1 : 0;
+    ctx->stage->err_init = len;
+    CU(cudaMemcpyAsync(d_off + total, &ctx->stage->err_init, 8, cudaMemcpyHostToDevice, s));
+    if (!device_resident) CU(cudaMemcpyAsync(offsets, d_off, (total + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
     return ok(err);
 }
 

@@ -123,6 +123,16 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
                         cudaStream_t s);
 // commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,
 // thread-per-check above).
+// Raw log image scan (log_scan.cu): chunk / window geometry and the three phases.
+constexpr uint64_t kScanChunk = 1ull << 20;
+constexpr uint32_t kScanWindow = 2048;
+void launch_log_scan_a(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, uint64_t* d_exit, uint32_t* d_count,
+                       cudaStream_t s);
+void launch_log_scan_b(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, const uint64_t* d_exit,
+                       const uint32_t* d_count, uint64_t* d_start, uint64_t* d_base, unsigned long long* d_state,
+                       cudaStream_t s);
+void launch_log_scan_c(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, const uint64_t* d_start,
+                       const uint64_t* d_base, uint64_t* d_offsets, cudaStream_t s);
 // Masked segmented group_combine fold: one CTA per segment; out = encodings
 // (identity = zeros). *d_bad set when a point fails to decode.
 void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,

@@ -2,8 +2,9 @@
 records = LE32 length + bytes) read without splitting it into per-record objects.
 
 `RecordLog` keeps the file image as one array plus the record header positions
-from poslo_log_scan (the C-ABI's host scanner, FormatError exactly where
-read_log throws). Batches built from it point the device at the file image
+from poslo_gpu_log_scan (speculative chunk walks on the device) or
+poslo_log_scan (the host scanner); both raise FormatError exactly where
+read_log throws. Batches built from it point the device at the file image
 itself (poslo_batch.record_header = 4): the H2D copy is the file, no per-record
 repacking. `epochs_of` is tools/poslo.cpp:32-40.
 """
@@ -19,7 +20,8 @@ from .api import FormatError
 
 
 class RecordLog:
-    def __init__(self, raw: bytes):
+    def __init__(self, raw: bytes, verifier: Optional[api.Verifier] = None, scanner: str = "device"):
+        """scanner: "device" (poslo_gpu_log_scan, the default) or "host" (poslo_log_scan)."""
         self.raw = np.frombuffer(raw, dtype=np.uint8) if len(raw) else np.zeros(0, np.uint8)
         lib = N.load()
         n = ctypes.c_uint64(0)
@@ -27,19 +29,25 @@ class RecordLog:
         buf = self.raw if len(self.raw) else np.zeros(1, np.uint8)
         cap = max(2, len(raw) // 4 + 1)  # every record takes >= 4 bytes
         offs = np.zeros(cap, dtype=np.uint64)
-        rc = lib.poslo_log_scan(buf.ctypes.data, len(raw), offs.ctypes.data, cap, ctypes.byref(n), ctypes.byref(err))
+        if scanner == "host":
+            rc = lib.poslo_log_scan(buf.ctypes.data, len(raw), offs.ctypes.data, cap, ctypes.byref(n),
+                                    ctypes.byref(err))
+        else:
+            v = verifier or api.default_verifier()
+            rc = lib.poslo_gpu_log_scan(v._ctx, buf.ctypes.data, len(raw), 0, offs.ctypes.data, cap, ctypes.byref(n),
+                                        ctypes.byref(err))
         if rc:
             api._raise(rc, err)
         self.n = int(n.value)
         self.offsets = offs[:self.n + 1].copy()
 
     @staticmethod
-    def read(path: str) -> "RecordLog":
+    def read(path: str, verifier: Optional[api.Verifier] = None, scanner: str = "device") -> "RecordLog":
         """read_file + read_log (log_file.hpp:14-19, 34-51)."""
         if not os.path.exists(path):
             raise FormatError("cannot open " + path)
         with open(path, "rb") as f:
-            return RecordLog(f.read())
+            return RecordLog(f.read(), verifier, scanner)
 
     def __len__(self):
         return self.n

@@ -23,19 +23,19 @@ def test_scan_roundtrip_and_truncation(tmp_path):
     recs = [b"", b"a", bytes(range(256)) * 3, b"xyz" * 1000, b"\x00\x01\x02\x03"]
     p = str(tmp_path / "log.bin")
     write_log(p, recs)
-    log = RecordLog.read(p)
+    log = RecordLog.read(p, scanner="host")
     assert len(log) == len(recs) and [log.record(t) for t in range(len(recs))] == recs
     raw = open(p, "rb").read()
     for cut in (1, 3, 5, len(raw) - 1):  # truncated header / body, as read_log
         with pytest.raises(api.FormatError, match="truncated log record"):
-            RecordLog(raw[:cut] if cut < 4 else raw[:len(raw) - 1] if cut == len(raw) - 1 else raw[:cut])
-    assert len(RecordLog(b"")) == 0
+            RecordLog(raw[:cut], scanner="host")
+    assert len(RecordLog(b"", scanner="host")) == 0
     with pytest.raises(api.FormatError):
-        RecordLog(b"").epochs_of(4)
+        RecordLog(b"", scanner="host").epochs_of(4)
     with pytest.raises(api.FormatError):
         log.epochs_of(2)  # 5 records
     with pytest.raises(api.FormatError):
-        RecordLog.read(str(tmp_path / "missing.bin"))
+        RecordLog.read(str(tmp_path / "missing.bin"), scanner="host")
 
 
 @pytest.mark.gpu
@@ -58,3 +58,39 @@ def test_log_file_batches_match_reference(verifier, tmp_path, name):
     sub = log.batch(st.suite, st.n2, ds, range(1, st.n1))
     parts2, _ = verifier.agg_ekeys_log(sub)
     assert [x[1] for x in parts2] == st.e_tilde[1:]
+
+
+def _image(recs):
+    return b"".join(len(r).to_bytes(4, "little") + r for r in recs)
+
+
+@pytest.mark.gpu
+def test_device_scan_matches_host_scan(verifier):
+    """poslo_gpu_log_scan against the host scanner (read_log semantics) on
+    images that exercise every path: many chunks, records longer than the
+    speculation window (walked in the stitch), empty records (every window
+    position a valid chain), binary payloads with small fake lengths, and
+    truncation at many points."""
+    import random
+
+    import numpy as np
+    from paper_2506_08781_b200 import api
+    from paper_2506_08781_b200.logfile import RecordLog
+    rng = random.Random(7)
+    cases = []
+    cases.append([bytes(rng.getrandbits(8) for _ in range(rng.randrange(64, 1025))) for _ in range(6000)])
+    cases.append([b"\x00" * rng.choice([0, 0, 0, 1, 3, 4, 5000, 70000]) for _ in range(3000)])
+    cases.append([bytes([rng.choice([0, 1, 2, 255])]) * rng.randrange(0, 40) for _ in range(200000)])
+    cases.append([b"x" * (3 << 20), b"", b"y" * 17, b"z" * (1 << 20)])
+    cases.append([])
+    for recs in cases:
+        img = _image(recs)
+        h = RecordLog(img, scanner="host")
+        d = RecordLog(img, verifier, scanner="device")
+        assert len(d) == len(recs) and np.array_equal(h.offsets, d.offsets)
+    img = _image(cases[0])
+    for cut in [1, 3, 5, 1 << 20, (1 << 20) + 3, len(img) - 1, len(img) - 700]:
+        with pytest.raises(api.FormatError, match="truncated log record"):
+            RecordLog(img[:cut], verifier, scanner="device")
+        with pytest.raises(api.FormatError, match="truncated log record"):
+            RecordLog(img[:cut], scanner="host")
