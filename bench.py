@@ -55,6 +55,9 @@ def parse():
                     help="coarse: one aggregate (config 2); epoch: per-epoch verdicts (config 3); "
                          "tamper: k tampered entries localised by distillation (config 5)")
     ap.add_argument("--tamper", type=int, default=16, help="tampered entries per GPU (mode tamper)")
+    ap.add_argument("--records", action="store_true",
+                    help="with --varlen --mode epoch: also time file ingestion end to end (raw LE32-record image "
+                         "in pinned host memory -> H2D -> device record scan -> in-place verification)")
     ap.add_argument("--n-u", type=int, default=1024, help="umbrellas over the whole job (mode tamper)")
     return ap.parse_args()
 
@@ -526,6 +529,60 @@ def main():
                "path": f"poslo_gpu_{dict(coarse='paver', epoch='epoch_verify', tamper='distill_coarse')[a.mode]}(device_resident=0) "
                        f"on a pinned host log, 64 MiB chunked H2D overlapped with hashing"}
 
+    # ---- e2e from a raw log image (log_file.hpp records): H2D, device record
+    # scan (poslo_gpu_log_scan), per-epoch verification of the image in place
+    records = None
+    if a.records and a.varlen and a.mode == "epoch":
+        lens_h = synth_varlen(a.seed, rank * n, n).astype(np.int64)
+        hdr_pos = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens_h + 4, out=hdr_pos[1:])
+        img_bytes = int(hdr_pos[-1])
+        img = torch.empty(img_bytes, dtype=torch.uint8, pin_memory=True)
+        img_np = img.numpy()
+        payload_h = log.cpu().numpy()
+        l32 = lens_h.astype(np.uint32).view(np.uint8).reshape(-1, 4)
+        for k in range(4):
+            img_np[hdr_pos[:-1] + k] = l32[:, k]
+        offs_h = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens_h, out=offs_h[1:])
+        for e in range(n1_local):  # payload bytes of epoch e behind their headers (per epoch: bounded memory)
+            t0_, t1_ = e * a.n2, (e + 1) * a.n2
+            seg = lens_h[t0_:t1_]
+            dst = np.repeat(hdr_pos[t0_:t1_] + 4 - offs_h[t0_:t1_], seg) + np.arange(offs_h[t0_], offs_h[t1_])
+            img_np[dst] = payload_h[offs_h[t0_]:offs_h[t1_]]
+        dimg = torch.empty(img_bytes, dtype=torch.uint8, device="cuda")
+        doffs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        cnt = ctypes.c_uint64()
+
+        def step_records():
+            dimg.copy_(img, non_blocking=True)
+            call(lib.poslo_gpu_log_scan, ctypes.c_void_p(dimg.data_ptr()), img_bytes, 1,
+                 ctypes.c_void_p(doffs.data_ptr()), n + 1, ctypes.byref(cnt))
+            rb = N.PosloBatch()
+            rb.suite, rb.n2, rb.payload, rb.payload_bytes = a.suite, a.n2, dimg.data_ptr(), img_bytes
+            rb.offsets, rb.entry_len, rb.n_entries = doffs.data_ptr(), 0, n
+            rb.epochs, rb.epoch_starts, rb.n_epochs = epochs.ctypes.data, None, n1_local
+            rb.ds, rb.ds_len, rb.ds_capacity = ctypes.addressof(ds_buf), len(ds_bytes), D
+            rb.device_resident, rb.record_header = 1, 4
+            call(lib.poslo_gpu_epoch_verify, ctypes.byref(rb), Yb, ctypes.c_void_p(s_dev.data_ptr()),
+                 ctypes.c_void_p(r_dev.data_ptr()), verd, None)
+            return n1_local - sum(verd.raw[:n1_local])
+
+        assert step_records() == 0 and cnt.value == n, "record-image verification failed"
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(1, a.e2e_steps)
+        for _ in range(reps):
+            bad = step_records()
+        torch.cuda.synchronize()
+        rec_ms = (time.perf_counter() - t0) * 1e3 / reps
+        assert bad == 0
+        records = {"value": round(world * n / (rec_ms * 1e-3), 1), "unit": "entries/s", "ms_per_step": round(rec_ms, 3),
+                   "h2d_bytes_per_step": img_bytes, "d2h_bytes_per_step": n1_local + 16,
+                   "path": "raw LE32-record image (log_file.hpp) in pinned host memory -> H2D -> poslo_gpu_log_scan "
+                           "-> poslo_gpu_epoch_verify(record_header=4) in place"}
+        del img, dimg
+
     if rank != 0:
         dist.destroy_process_group()
         return 0
@@ -591,6 +648,7 @@ def main():
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (counter-based log, include/poslo_synth.h); keys and signatures by the reference's kg/sig_epoch derivation, on the device",
         "config": config_dict(a, world),
         "e2e": e2e,
+        **({"e2e_records": records} if records else {}),
         "roofline": roof,
         "gpu_launches": launches,
         "verdict": bool(ok),
