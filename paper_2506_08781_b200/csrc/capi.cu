@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <vector>
 
@@ -71,6 +72,7 @@ struct poslo_gpu_ctx {
 namespace {
 
 constexpr uint64_t kChunkBytes = 64ull << 20;
+constexpr uint32_t kPipePieces = 8;  // epoch pieces when per-epoch checks overlap hashing
 constexpr int kEvSeed = 0, kEvHash = 1, kEvFin = 2, kEvSum = 3, kEvGroup = 4, kEvEnd = 5;
 
 int set_err(poslo_error* err, int code, uint32_t epoch, const char* fmt, ...) {
@@ -206,6 +208,11 @@ struct Prepared {
     uint32_t* d_etilde = nullptr;   // per-epoch e~ (8 limbs), valid when want_etilde
     const uint32_t* sum_src = nullptr;  // what e-hat sums: e~ (8 limbs) or raw epoch sums (17 limbs)
     int sum_limbs = 8;
+    // Pipelining hook: when set (and the log is device-resident), the hash is
+    // launched in epoch pieces and on_piece(e0, e1) runs after each piece's
+    // e~ are final on the stream, so the caller can start its per-epoch
+    // checks for that piece while the next one hashes.
+    std::function<int(uint32_t, uint32_t)> on_piece;
 };
 
 // Entries per tile of the generic / variable-length kernels (<= 1024, the
@@ -424,6 +431,21 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
             if (t.tile_count) launch_hash(t);
         }
+    } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && n_ep >= 2 * kPipePieces) {
+        // device-resident, uniform: epoch pieces, each finalised and handed to the caller
+        for (uint32_t q = 0; q < kPipePieces; q++) {
+            const uint32_t e0 = (uint32_t)((uint64_t)n_ep * q / kPipePieces);
+            const uint32_t e1 = (uint32_t)((uint64_t)n_ep * (q + 1) / kPipePieces);
+            TileMap t = tm;
+            t.tile_begin = e0 * tm.tiles_per_epoch;
+            t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
+            if (t.tile_count) launch_hash(t);
+            launch_epoch_finalize_range(tm, e0, e1, d_partial, P.d_etilde, s);
+            ctx->launches += 1;
+            int rc2 = P.on_piece(e0, e1);
+            if (rc2) return rc2;
+        }
+        need_finalize = false;
     } else if (tm.n_tiles) {
         launch_hash(tm);
     }
@@ -926,6 +948,21 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         if (rc) return rc;
     }
     Prepared P;
+    uint8_t* d_vpipe = nullptr;
+    bool piped = false;
+    if (split && b->device_resident) {  // checks of piece q overlap the hashing of piece q + 1
+        ENSURE(b_verdict, n, d_vpipe);
+        P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
+            CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+            CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));  // side: after the decode, then this piece
+            launch_check_split(ctx->d_tabY256, ctx->d_tabB256, e1 - e0, P.d_etilde + 8 * (size_t)e0,
+                               d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
+                               d_ok + e0, d_vpipe + e0, ctx->side);
+            ctx->launches += 1;
+            piped = true;
+            return POSLO_OK;
+        };
+    }
     rc = run_hash(ctx, b, P, err);
     if (rc) {
         cudaStreamSynchronize(ctx->side);
@@ -942,7 +979,12 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         cudaStreamSynchronize(ctx->side);
         return rc;
     }
-    if (split) {
+    if (split && piped) {
+        CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
+        CU(cudaMemcpyAsync(verdicts, d_vpipe, n, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    } else if (split) {
         uint8_t* d_verdict;
         ENSURE(b_verdict, n, d_verdict);
         rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);

@@ -95,6 +95,9 @@ void launch_hash_s1_var(const EntryLayout& lay, const TileMap& tm, const uint4* 
 // fast paths, which finalise in the hashing kernel).
 void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,
                            cudaStream_t s);
+// Epochs [e0, e1) only (pipelined per-chunk finalize).
+void launch_epoch_finalize_range(const TileMap& tm, uint32_t e0, uint32_t e1, const uint32_t* d_partial,
+                                 uint32_t* d_etilde, cudaStream_t s);
 
 // out (8 limbs) = sum of n items mod l; items are `limbs`-limb little-endian
 // integers (8 for scalars, 17 for partial accumulators). Optional mask: skip

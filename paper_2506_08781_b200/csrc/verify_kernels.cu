@@ -276,10 +276,10 @@ __global__ void __launch_bounds__(256) k_hash_generic(int suite, EntryLayout lay
 }
 
 // ---------------------------------------------------------------- epoch finalize
-__global__ void k_epoch_finalize(TileMap tm, const uint32_t* __restrict__ partial,
+__global__ void k_epoch_finalize(TileMap tm, uint32_t ep0, uint32_t ep1, const uint32_t* __restrict__ partial,
                                  uint32_t* __restrict__ etilde) {
-    uint32_t ep = blockIdx.x * blockDim.x + threadIdx.x;
-    if (ep >= tm.n_epochs) return;
+    uint32_t ep = ep0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (ep >= ep1) return;
     uint32_t b, e;
     if (tm.tiles) {
         b = tm.epoch_tile_begin[ep];
@@ -458,7 +458,13 @@ void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, c
 void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,
                            cudaStream_t s) {
     if (!tm.n_epochs) return;
-    k_epoch_finalize<<<(tm.n_epochs + 127) / 128, 128, 0, s>>>(tm, d_partial, d_etilde);
+    k_epoch_finalize<<<(tm.n_epochs + 127) / 128, 128, 0, s>>>(tm, 0, tm.n_epochs, d_partial, d_etilde);
+}
+
+void launch_epoch_finalize_range(const TileMap& tm, uint32_t e0, uint32_t e1, const uint32_t* d_partial,
+                                 uint32_t* d_etilde, cudaStream_t s) {
+    if (e1 <= e0) return;
+    k_epoch_finalize<<<(e1 - e0 + 127) / 128, 128, 0, s>>>(tm, e0, e1, d_partial, d_etilde);
 }
 
 void launch_sum_mod_l(const uint32_t* d_items, int limbs, uint64_t n, const uint8_t* d_mask,
