@@ -1088,6 +1088,22 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         if (rc) return rc;
     }
     Prepared P;
+    // per-epoch verdicts stay on the device as the fold mask
+    uint8_t* d_verdict;
+    ENSURE(b_verdict, std::max<uint32_t>(n, 1), d_verdict);
+    bool piped = false;
+    if (split && b->device_resident) {  // checks of piece q overlap the hashing of piece q + 1
+        P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
+            CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+            CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
+            launch_check_split(ctx->d_tabY256, ctx->d_tabB256, e1 - e0, P.d_etilde + 8 * (size_t)e0,
+                               d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
+                               d_ok + e0, d_verdict + e0, ctx->side);
+            ctx->launches += 1;
+            piped = true;
+            return POSLO_OK;
+        };
+    }
     rc = run_hash(ctx, b, P, err);
     if (!rc) rc = check_hash_errors(ctx, b, err);
     if (rc) {
@@ -1097,10 +1113,10 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
     if (!n) return ok(err);
     mark(ctx, kEvSum);
     mark(ctx, kEvGroup);
-    // per-epoch verdicts stay on the device as the fold mask
-    uint8_t* d_verdict;
-    ENSURE(b_verdict, n, d_verdict);
-    if (split) {
+    if (split && piped) {
+        CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
+    } else if (split) {
         rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);
         if (rc) return rc;
     } else {

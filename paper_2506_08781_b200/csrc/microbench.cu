@@ -8,6 +8,7 @@
 //   3  IMAD with an immediate multiplier      4  LOP3 + immediate IMAD
 //   5  SHF.R.W funnel rotate (ALU pipe)       6  IMAD.HI immediate
 //   7  LOP3 + IMAD.HI immediate
+//   8  IMAD.WIDE.U32, 64-bit addend          9  LOP3 + IMAD.WIDE.U32
 // Every thread runs 8 independent chains; lane-ops = threads * iters * 8 (16 for mode 2).
 // Not part of the verifier ABI (separate library libposlo_microbench.so).
 #include <cuda_runtime.h>
@@ -34,6 +35,14 @@ __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uin
                 asm volatile("shf.r.wrap.b32 %0, %0, %0, 13;" : "+r"(x[k]));
             if (MODE == 6 || MODE == 7)  // IMAD.HI, immediate multiplier
                 asm volatile("mad.hi.u32 %0, %0, 0x9e3779b9, %1;" : "+r"(y[k]) : "r"(y[(k + 3) & 7]));
+            if (MODE == 8 || MODE == 9) {  // IMAD.WIDE.U32 with a 64-bit addend (radix-2^26 field products)
+                uint64_t acc = ((uint64_t)x[k] << 32) | y[k];
+                asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(y[(k + 3) & 7]), "r"(a));
+                y[k] = (uint32_t)acc;
+                if (MODE == 8) x[k] = (uint32_t)(acc >> 32);
+            }
+            if (MODE == 9)
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(x[(k + 1) & 7]));
         }
     }
     uint32_t r = 0;
@@ -63,7 +72,9 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
             case 4: k_int_peak<4><<<blocks, 256>>>(out, a, b, iters); break;
             case 5: k_int_peak<5><<<blocks, 256>>>(out, a, b, iters); break;
             case 6: k_int_peak<6><<<blocks, 256>>>(out, a, b, iters); break;
-            default: k_int_peak<7><<<blocks, 256>>>(out, a, b, iters); break;
+            case 7: k_int_peak<7><<<blocks, 256>>>(out, a, b, iters); break;
+            case 8: k_int_peak<8><<<blocks, 256>>>(out, a, b, iters); break;
+            default: k_int_peak<9><<<blocks, 256>>>(out, a, b, iters); break;
         }
     };
     launch();  // warm-up (clock ramp)
@@ -75,7 +86,7 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    double per_iter = (mode == 2 || mode == 4 || mode == 7) ? 16.0 : 8.0;
+    double per_iter = (mode == 2 || mode == 4 || mode == 7 || mode == 9) ? 16.0 : 8.0;
     double ops = (double)blocks * 256 * iters * per_iter * reps;
     *ops_per_s = ops / (ms * 1e-3);
     if (ms_out) *ms_out = ms / reps;
