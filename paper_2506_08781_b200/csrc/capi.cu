@@ -521,7 +521,7 @@ int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void*
 // Comb tables of alpha (once per context) and of Y (cached per Y value).
 // Y validation (GroupElement::from_bytes) happens in the table build.
 int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false) {
-    if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * 128));
+    if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * kGptBytes));
     if (!ctx->d_tabB) {
         CU(cudaMalloc(&ctx->d_tabB, kCombTableBytes));
         launch_build_table(nullptr, ctx->d_pk, ctx->d_tabB, d_flags, ctx->stream);
@@ -824,7 +824,7 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
         uint8_t* d_pts;
         void* d_fs;
         UPLOAD(b_pts, r_hats, (size_t)b->n_epochs * 32, d_pts);
-        ENSURE(b_foldscratch, 1024 * 128, d_fs);
+        ENSURE(b_foldscratch, 1024 * kGptBytes, d_fs);
         launch_point_fold(d_pts, b->n_epochs, d_rhat, d_flags + 1, d_fs, ctx->stream);
         ctx->launches += 2;
     }
@@ -1463,7 +1463,7 @@ int poslo_gpu_group_fold(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* pts, uin
     void* d_fs;
     int* d_flags;
     UPLOAD(b_pts, pts, n * 32, d_pts);
-    ENSURE(b_foldscratch, 1024 * 128, d_fs);
+    ENSURE(b_foldscratch, 1024 * kGptBytes, d_fs);
     ENSURE(b_rhat, 32, d_out);
     ENSURE(b_flags, 4, d_flags);
     CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));

@@ -9,6 +9,9 @@
 
 namespace poslo_gpu {
 
+static_assert(sizeof(fe) == kFeBytes && sizeof(gpt) == kGptBytes && sizeof(gcached) == kCachedBytes,
+              "buffer sizes in poslo_internal.h follow the field representation");
+
 namespace {
 
 __device__ __forceinline__ void load32(const uint8_t* p, uint8_t b[32]) {
@@ -260,7 +263,7 @@ __device__ __forceinline__ gpt shfl_pt(const gpt& p, int off) {
 #pragma unroll
     for (int c = 0; c < 4; c++)
 #pragma unroll
-        for (int k = 0; k < 8; k++) dst[c]->v[k] = __shfl_down_sync(0xffffffffu, src[c]->v[k], off, 8);
+        for (int k = 0; k < (int)(sizeof(fe) / 4); k++) dst[c]->v[k] = __shfl_down_sync(0xffffffffu, src[c]->v[k], off, 8);
     return r;
 }
 
@@ -350,6 +353,7 @@ struct CheckPre {
     gpt T;   // R - s*B
     int ok;  // R decoded
 };
+static_assert(sizeof(CheckPre) <= 256, "b_pre holds one CheckPre");
 
 __device__ __forceinline__ void named_sync64() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 

@@ -118,9 +118,12 @@ void launch_group_check(const uint8_t* d_y, uint32_t n, const uint32_t* d_e, con
                         cudaStream_t s);
 
 // Fixed-base comb table (512 affine Niels points, 48 KiB) of the point encoded at
-// d_enc, or of the generator when d_enc == nullptr. d_pk_scratch >= 64 * 128 B.
-constexpr size_t kCombTableBytes = 512 * 96;       // radix 16: 64 x 8 affine Niels points
-constexpr size_t kComb256TableBytes = 4096 * 96;  // radix 256: 32 x 128 points
+// d_enc, or of the generator when d_enc == nullptr. d_pk_scratch >= 64 * kGptBytes.
+constexpr size_t kFeBytes = 40;                    // field element: 10 x 32-bit limbs (radix 2^25.5)
+constexpr size_t kCachedBytes = 3 * kFeBytes;       // affine Niels point (y+x, y-x, 2dxy)
+constexpr size_t kGptBytes = 4 * kFeBytes;          // extended point (X, Y, Z, T)
+constexpr size_t kCombTableBytes = 512 * kCachedBytes;      // radix 16: 64 x 8 affine Niels points
+constexpr size_t kComb256TableBytes = 4096 * kCachedBytes;  // radix 256: 32 x 128 points
 constexpr uint32_t kCtaCheckMax = 1024;          // larger batches use one thread per check (radix-256 combs)
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s);
@@ -143,7 +146,7 @@ void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t
 // Batched checks with R decoded ahead (side stream, overlapping the hashing):
 // d_pts n x 128 B (extended coordinates), d_ok n bytes; check_split runs 8
 // lanes per check on the radix-256 combs; segfold_decoded folds decoded points.
-constexpr size_t kPointBytes = 128;
+constexpr size_t kPointBytes = kGptBytes;
 void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s);
 void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n, const uint32_t* d_e,
                         const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,

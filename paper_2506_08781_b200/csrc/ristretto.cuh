@@ -6,8 +6,7 @@
 // (:144-167) and group_combine (:169-178), plus the byte-equality of
 // GroupElement::operator== (include/poslo/group.hpp:59).
 //
-// Field GF(2^255-19): 8 x 32-bit limbs, values kept loosely in [0, 2^256)
-// and canonicalised only for encode/compare (2^256 == 38 mod p). Points are
+// Field GF(2^255-19): radix 2^25.5, see the field section below. Points are
 // extended twisted-Edwards (X:Y:Z:T), a = -1. Ristretto decode/encode and
 // SQRT_RATIO_M1 follow the published ristretto255 definition (RFC 9496 §4);
 // constants were derived from their definitions (oracle/ristretto.py) and the
@@ -18,186 +17,183 @@
 #pragma once
 #include "poslo_common.cuh"
 
-#define FE_D_LIMBS 0x135978a3u, 0x75eb4dcau, 0x4141d8abu, 0x00700a4du, 0x7779e898u, 0x8cc74079u, 0x2b6ffe73u, 0x52036ceeu
-#define FE_D2_LIMBS 0x26b2f159u, 0xebd69b94u, 0x8283b156u, 0x00e0149au, 0xeef3d130u, 0x198e80f2u, 0x56dffce7u, 0x2406d9dcu
-#define FE_SQRTM1_LIMBS 0x4a0ea0b0u, 0xc4ee1b27u, 0xad2fe478u, 0x2f431806u, 0x3dfbd7a7u, 0x2b4d0099u, 0x4fc1df0bu, 0x2b832480u
-#define FE_INVSQRT_A_MINUS_D_LIMBS 0x805d40eau, 0x99c8fdaau, 0x5a4172beu, 0x9d2f1617u, 0xfe01d840u, 0x16c27b91u, 0xcfaffca2u, 0x786c8905u
-#define FE_BASE_X_LIMBS 0x8f25d51au, 0xc9562d60u, 0x9525a7b2u, 0x692cc760u, 0xfdd6dc5cu, 0xc0a4e231u, 0xcd6e53feu, 0x216936d3u
-#define FE_BASE_Y_LIMBS 0x66666658u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u, 0x66666666u
-#define FE_BASE_T_LIMBS 0xa5b7dda3u, 0x6dde8ab3u, 0x775152f5u, 0x20f09f80u, 0x64abe37du, 0x66ea4e8eu, 0xd78b7665u, 0x67875f0fu
+// Field GF(2^255-19) in radix 2^25.5 (10 limbs alternating 26 / 25 bits,
+// bit offsets 0, 26, 51, ..., 230): a product of two field elements is 100
+// 32x32->64 multiply-adds (IMAD.WIDE with a 64-bit addend, full rate on the
+// FMA pipe) into 10 column sums that cannot overflow 64 bits, and ONE carry
+// chain — where 32-bit limbs need a carry per product on the ALU pipe.
+// Elements are kept "carried" (limb i < 2^w_i, slack of a few bits on limb 1)
+// after every operation; canonical form only for encode / compare.
+#define FE_D_LIMBS 0x35978a3u, 0x0d37284u, 0x3156ebdu, 0x06a0a0eu, 0x001c029u, 0x179e898u, 0x3a03cbbu, 0x1ce7198u, 0x2e2b6ffu, 0x1480db3u
+#define FE_D2_LIMBS 0x2b2f159u, 0x1a6e509u, 0x22add7au, 0x0d4141du, 0x0038052u, 0x0f3d130u, 0x3407977u, 0x19ce331u, 0x1c56dffu, 0x0901b67u
+#define FE_SQRTM1_LIMBS 0x20ea0b0u, 0x186c9d2u, 0x08f189du, 0x035697fu, 0x0bd0c60u, 0x1fbd7a7u, 0x2804c9eu, 0x1e16569u, 0x004fc1du, 0x0ae0c92u
+#define FE_INVSQRT_A_MINUS_D_LIMBS 0x05d40eau, 0x03f6aa0u, 0x257d339u, 0x0bad20bu, 0x274bc58u, 0x001d840u, 0x13dc8ffu, 0x19442d8u, 0x05cfaffu, 0x1e1b224u
+#define FE_BASE_X_LIMBS 0x325d51au, 0x18b5823u, 0x0f6592au, 0x104a92du, 0x1a4b31du, 0x1d6dc5cu, 0x27118feu, 0x07fd814u, 0x13cd6e5u, 0x085a4dbu
+#define FE_BASE_Y_LIMBS 0x2666658u, 0x1999999u, 0x0ccccccu, 0x1333333u, 0x1999999u, 0x0666666u, 0x3333333u, 0x0ccccccu, 0x2666666u, 0x1999999u
+#define FE_BASE_T_LIMBS 0x1b7dda3u, 0x1a2ace9u, 0x25eadbbu, 0x003ba8au, 0x083c27eu, 0x0abe37du, 0x1274732u, 0x0ccacddu, 0x0fd78b7u, 0x19e1d7cu
 
 struct fe {
-    uint32_t v[8];
+    uint32_t v[10];
 };
 
 struct gpt {  // extended coordinates, x = X/Z, y = Y/Z, xy = T/Z
     fe X, Y, Z, T;
 };
 
-PHD fe fe_from(const uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4, uint32_t a5,
-               uint32_t a6, uint32_t a7) {
+#define FE_M26 0x3ffffffu
+#define FE_M25 0x1ffffffu
+
+PHD constexpr int fe_width(int i) { return (i & 1) ? 25 : 26; }
+PHD constexpr int fe_offset(int i) { return 26 * ((i + 1) / 2) + 25 * (i / 2); }
+
+PHD fe fe_from(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4, uint32_t a5, uint32_t a6,
+               uint32_t a7, uint32_t a8, uint32_t a9) {
     fe r;
-    r.v[0] = a0; r.v[1] = a1; r.v[2] = a2; r.v[3] = a3;
-    r.v[4] = a4; r.v[5] = a5; r.v[6] = a6; r.v[7] = a7;
+    r.v[0] = a0; r.v[1] = a1; r.v[2] = a2; r.v[3] = a3; r.v[4] = a4;
+    r.v[5] = a5; r.v[6] = a6; r.v[7] = a7; r.v[8] = a8; r.v[9] = a9;
     return r;
 }
 #define FE_CONST(LIMBS) fe_from(LIMBS)
 
-PHD fe fe_zero() { return fe_from(0, 0, 0, 0, 0, 0, 0, 0); }
-PHD fe fe_one() { return fe_from(1, 0, 0, 0, 0, 0, 0, 0); }
+PHD fe fe_zero() { return fe_from(0, 0, 0, 0, 0, 0, 0, 0, 0, 0); }
+PHD fe fe_one() { return fe_from(1, 0, 0, 0, 0, 0, 0, 0, 0, 0); }
 
-// r = a + 38 * c folded until no carry remains (c is the overflow count).
-PHD void fe_fold(uint32_t r[8], uint64_t c) {
-    for (int pass = 0; pass < 2; pass++) {
-        uint64_t t = c * 38;
+// One carry pass over 64-bit column values into carried 32-bit limbs:
+// 2^255 == 19 folds the top carry into limb 0.
+PHD fe fe_carry64(uint64_t h[10]) {
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            t += r[i];
-            r[i] = (uint32_t)t;
-            t >>= 32;
-        }
-        c = t;
+    for (int i = 0; i < 9; i++) {
+        h[i + 1] += h[i] >> fe_width(i);
+        h[i] &= (i & 1) ? FE_M25 : FE_M26;
     }
+    h[0] += 19 * (h[9] >> 25);
+    h[9] &= FE_M25;
+    h[1] += h[0] >> 26;
+    h[0] &= FE_M26;
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 10; i++) r.v[i] = (uint32_t)h[i];
+    return r;
+}
+
+PHD fe fe_carry32(const uint32_t t[10]) {
+    uint64_t h[10];
+#pragma unroll
+    for (int i = 0; i < 10; i++) h[i] = t[i];
+    return fe_carry64(h);
 }
 
 PHD fe fe_add(const fe& a, const fe& b) {
-    fe r;
-    uint64_t c = 0;
+    uint32_t t[10];
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        c += (uint64_t)a.v[i] + b.v[i];
-        r.v[i] = (uint32_t)c;
-        c >>= 32;
-    }
-    fe_fold(r.v, c);
-    return r;
+    for (int i = 0; i < 10; i++) t[i] = a.v[i] + b.v[i];
+    return fe_carry32(t);
 }
 
+// a + 2p - b: 2p's limbs dominate every carried b, so no limb underflows.
 PHD fe fe_sub(const fe& a, const fe& b) {
-    fe r;
-    int64_t bw = 0;
+    uint32_t t[10];
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        int64_t t = (int64_t)a.v[i] - b.v[i] + bw;
-        r.v[i] = (uint32_t)t;
-        bw = t >> 32;
+    for (int i = 0; i < 10; i++) {
+        const uint32_t bias = i == 0 ? 0x7ffffdau : ((i & 1) ? 0x3fffffeu : 0x7fffffeu);
+        t[i] = a.v[i] + bias - b.v[i];
     }
-    // a wrapped: true value = r - 2^256 == r - 38 (mod p); at most twice
-    for (int pass = 0; pass < 2 && bw; pass++) {
-        int64_t t2 = -38;
-        bw = 0;
+    return fe_carry32(t);
+}
+
+// Column sums h_k = sum over i + j == k (mod 10) of f_i g_j, with x19 for the
+// wrapped terms (2^255 == 19) and x2 when both limb offsets round down
+// (i and j odd): every term < 2^58, every column < 2^62.
+PHD fe fe_mul_impl(const fe& f, const fe& g) {
+    uint32_t g19[10], f2[10];
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            int64_t t = (int64_t)r.v[i] + (i == 0 ? t2 : 0) + bw;
-            r.v[i] = (uint32_t)t;
-            bw = t >> 32;
+    for (int i = 0; i < 10; i++) {
+        g19[i] = 19u * g.v[i];
+        f2[i] = (i & 1) ? 2u * f.v[i] : f.v[i];
+    }
+    uint64_t h[10];
+#pragma unroll
+    for (int k = 0; k < 10; k++) h[k] = 0;
+#pragma unroll
+    for (int i = 0; i < 10; i++)
+#pragma unroll
+        for (int j = 0; j < 10; j++) {
+            const uint32_t fi = (j & 1) ? f2[i] : f.v[i];
+            const uint32_t gj = (i + j >= 10) ? g19[j] : g.v[j];
+            h[(i + j) % 10] += (uint64_t)fi * gj;
         }
-    }
-    return r;
+    return fe_carry64(h);
 }
 
-#ifdef __CUDA_ARCH__
-// 8x8-limb product with carry-flag chains (two per row: low and high
-// halves), then the 2^256 == 38 fold: ~170 instructions, about half of the
-// portable C version. Identical results (tests/native + GPU parity tests).
-__device__ __forceinline__ fe fe_mul_ptx(const fe& a, const fe& b) {
-    fe r;
-    asm("{\n\t.reg .u32 r<16>;\n\tmov.u32 r0, 0;\n\tmov.u32 r1, 0;\n\tmov.u32 r2, 0;\n\tmov.u32 r3, 0;\n\tmov.u32 r4, 0;\n\tmov.u32 r5, 0;\n\tmov.u32 r6, 0;\n\tmov.u32 r7, 0;\n\tmov.u32 r8, 0;\n\tmov.u32 r9, 0;\n\tmov.u32 r10, 0;\n\tmov.u32 r11, 0;\n\tmov.u32 r12, 0;\n\tmov.u32 r13, 0;\n\tmov.u32 r14, 0;\n\tmov.u32 r15, 0;\n\tmad.lo.cc.u32 r0, %8, %16, r0;\n\tmadc.lo.cc.u32 r1, %9, %16, r1;\n\tmadc.lo.cc.u32 r2, %10, %16, r2;\n\tmadc.lo.cc.u32 r3, %11, %16, r3;\n\tmadc.lo.cc.u32 r4, %12, %16, r4;\n\tmadc.lo.cc.u32 r5, %13, %16, r5;\n\tmadc.lo.cc.u32 r6, %14, %16, r6;\n\tmadc.lo.cc.u32 r7, %15, %16, r7;\n\taddc.u32 r8, 0, 0;\n\tmad.hi.cc.u32 r1, %8, %16, r1;\n\tmadc.hi.cc.u32 r2, %9, %16, r2;\n\tmadc.hi.cc.u32 r3, %10, %16, r3;\n\tmadc.hi.cc.u32 r4, %11, %16, r4;\n\tmadc.hi.cc.u32 r5, %12, %16, r5;\n\tmadc.hi.cc.u32 r6, %13, %16, r6;\n\tmadc.hi.cc.u32 r7, %14, %16, r7;\n\tmadc.hi.u32 r8, %15, %16, r8;\n\tmad.lo.cc.u32 r1, %8, %17, r1;\n\tmadc.lo.cc.u32 r2, %9, %17, r2;\n\tmadc.lo.cc.u32 r3, %10, %17, r3;\n\tmadc.lo.cc.u32 r4, %11, %17, r4;\n\tmadc.lo.cc.u32 r5, %12, %17, r5;\n\tmadc.lo.cc.u32 r6, %13, %17, r6;\n\tmadc.lo.cc.u32 r7, %14, %17, r7;\n\tmadc.lo.cc.u32 r8, %15, %17, r8;\n\taddc.u32 r9, 0, 0;\n\tmad.hi.cc.u32 r2, %8, %17, r2;\n\tmadc.hi.cc.u32 r3, %9, %17, r3;\n\tmadc.hi.cc.u32 r4, %10, %17, r4;\n\tmadc.hi.cc.u32 r5, %11, %17, r5;\n\tmadc.hi.cc.u32 r6, %12, %17, r6;\n\tmadc.hi.cc.u32 r7, %13, %17, r7;\n\tmadc.hi.cc.u32 r8, %14, %17, r8;\n\tmadc.hi.u32 r9, %15, %17, r9;\n\tmad.lo.cc.u32 r2, %8, %18, r2;\n\tmadc.lo.cc.u32 r3, %9, %18, r3;\n\tmadc.lo.cc.u32 r4, %10, %18, r4;\n\tmadc.lo.cc.u32 r5, %11, %18, r5;\n\tmadc.lo.cc.u32 r6, %12, %18, r6;\n\tmadc.lo.cc.u32 r7, %13, %18, r7;\n\tmadc.lo.cc.u32 r8, %14, %18, r8;\n\tmadc.lo.cc.u32 r9, %15, %18, r9;\n\taddc.u32 r10, 0, 0;\n\tmad.hi.cc.u32 r3, %8, %18, r3;\n\tmadc.hi.cc.u32 r4, %9, %18, r4;\n\tmadc.hi.cc.u32 r5, %10, %18, r5;\n\tmadc.hi.cc.u32 r6, %11, %18, r6;\n\tmadc.hi.cc.u32 r7, %12, %18, r7;\n\tmadc.hi.cc.u32 r8, %13, %18, r8;\n\tmadc.hi.cc.u32 r9, %14, %18, r9;\n\tmadc.hi.u32 r10, %15, %18, r10;\n\tmad.lo.cc.u32 r3, %8, %19, r3;\n\tmadc.lo.cc.u32 r4, %9, %19, r4;\n\tmadc.lo.cc.u32 r5, %10, %19, r5;\n\tmadc.lo.cc.u32 r6, %11, %19, r6;\n\tmadc.lo.cc.u32 r7, %12, %19, r7;\n\tmadc.lo.cc.u32 r8, %13, %19, r8;\n\tmadc.lo.cc.u32 r9, %14, %19, r9;\n\tmadc.lo.cc.u32 r10, %15, %19, r10;\n\taddc.u32 r11, 0, 0;\n\tmad.hi.cc.u32 r4, %8, %19, r4;\n\tmadc.hi.cc.u32 r5, %9, %19, r5;\n\tmadc.hi.cc.u32 r6, %10, %19, r6;\n\tmadc.hi.cc.u32 r7, %11, %19, r7;\n\tmadc.hi.cc.u32 r8, %12, %19, r8;\n\tmadc.hi.cc.u32 r9, %13, %19, r9;\n\tmadc.hi.cc.u32 r10, %14, %19, r10;\n\tmadc.hi.u32 r11, %15, %19, r11;\n\tmad.lo.cc.u32 r4, %8, %20, r4;\n\tmadc.lo.cc.u32 r5, %9, %20, r5;\n\tmadc.lo.cc.u32 r6, %10, %20, r6;\n\tmadc.lo.cc.u32 r7, %11, %20, r7;\n\tmadc.lo.cc.u32 r8, %12, %20, r8;\n\tmadc.lo.cc.u32 r9, %13, %20, r9;\n\tmadc.lo.cc.u32 r10, %14, %20, r10;\n\tmadc.lo.cc.u32 r11, %15, %20, r11;\n\taddc.u32 r12, 0, 0;\n\tmad.hi.cc.u32 r5, %8, %20, r5;\n\tmadc.hi.cc.u32 r6, %9, %20, r6;\n\tmadc.hi.cc.u32 r7, %10, %20, r7;\n\tmadc.hi.cc.u32 r8, %11, %20, r8;\n\tmadc.hi.cc.u32 r9, %12, %20, r9;\n\tmadc.hi.cc.u32 r10, %13, %20, r10;\n\tmadc.hi.cc.u32 r11, %14, %20, r11;\n\tmadc.hi.u32 r12, %15, %20, r12;\n\tmad.lo.cc.u32 r5, %8, %21, r5;\n\tmadc.lo.cc.u32 r6, %9, %21, r6;\n\tmadc.lo.cc.u32 r7, %10, %21, r7;\n\tmadc.lo.cc.u32 r8, %11, %21, r8;\n\tmadc.lo.cc.u32 r9, %12, %21, r9;\n\tmadc.lo.cc.u32 r10, %13, %21, r10;\n\tmadc.lo.cc.u32 r11, %14, %21, r11;\n\tmadc.lo.cc.u32 r12, %15, %21, r12;\n\taddc.u32 r13, 0, 0;\n\tmad.hi.cc.u32 r6, %8, %21, r6;\n\tmadc.hi.cc.u32 r7, %9, %21, r7;\n\tmadc.hi.cc.u32 r8, %10, %21, r8;\n\tmadc.hi.cc.u32 r9, %11, %21, r9;\n\tmadc.hi.cc.u32 r10, %12, %21, r10;\n\tmadc.hi.cc.u32 r11, %13, %21, r11;\n\tmadc.hi.cc.u32 r12, %14, %21, r12;\n\tmadc.hi.u32 r13, %15, %21, r13;\n\tmad.lo.cc.u32 r6, %8, %22, r6;\n\tmadc.lo.cc.u32 r7, %9, %22, r7;\n\tmadc.lo.cc.u32 r8, %10, %22, r8;\n\tmadc.lo.cc.u32 r9, %11, %22, r9;\n\tmadc.lo.cc.u32 r10, %12, %22, r10;\n\tmadc.lo.cc.u32 r11, %13, %22, r11;\n\tmadc.lo.cc.u32 r12, %14, %22, r12;\n\tmadc.lo.cc.u32 r13, %15, %22, r13;\n\taddc.u32 r14, 0, 0;\n\tmad.hi.cc.u32 r7, %8, %22, r7;\n\tmadc.hi.cc.u32 r8, %9, %22, r8;\n\tmadc.hi.cc.u32 r9, %10, %22, r9;\n\tmadc.hi.cc.u32 r10, %11, %22, r10;\n\tmadc.hi.cc.u32 r11, %12, %22, r11;\n\tmadc.hi.cc.u32 r12, %13, %22, r12;\n\tmadc.hi.cc.u32 r13, %14, %22, r13;\n\tmadc.hi.u32 r14, %15, %22, r14;\n\tmad.lo.cc.u32 r7, %8, %23, r7;\n\tmadc.lo.cc.u32 r8, %9, %23, r8;\n\tmadc.lo.cc.u32 r9, %10, %23, r9;\n\tmadc.lo.cc.u32 r10, %11, %23, r10;\n\tmadc.lo.cc.u32 r11, %12, %23, r11;\n\tmadc.lo.cc.u32 r12, %13, %23, r12;\n\tmadc.lo.cc.u32 r13, %14, %23, r13;\n\tmadc.lo.cc.u32 r14, %15, %23, r14;\n\taddc.u32 r15, 0, 0;\n\tmad.hi.cc.u32 r8, %8, %23, r8;\n\tmadc.hi.cc.u32 r9, %9, %23, r9;\n\tmadc.hi.cc.u32 r10, %10, %23, r10;\n\tmadc.hi.cc.u32 r11, %11, %23, r11;\n\tmadc.hi.cc.u32 r12, %12, %23, r12;\n\tmadc.hi.cc.u32 r13, %13, %23, r13;\n\tmadc.hi.cc.u32 r14, %14, %23, r14;\n\tmadc.hi.u32 r15, %15, %23, r15;\n\t.reg .u32 t8, c38;\n\tmov.u32 c38, 38;\n\tmad.lo.cc.u32 r0, r8, c38, r0;\n\tmadc.lo.cc.u32 r1, r9, c38, r1;\n\tmadc.lo.cc.u32 r2, r10, c38, r2;\n\tmadc.lo.cc.u32 r3, r11, c38, r3;\n\tmadc.lo.cc.u32 r4, r12, c38, r4;\n\tmadc.lo.cc.u32 r5, r13, c38, r5;\n\tmadc.lo.cc.u32 r6, r14, c38, r6;\n\tmadc.lo.cc.u32 r7, r15, c38, r7;\n\taddc.u32 t8, 0, 0;\n\tmad.hi.cc.u32 r1, r8, c38, r1;\n\tmadc.hi.cc.u32 r2, r9, c38, r2;\n\tmadc.hi.cc.u32 r3, r10, c38, r3;\n\tmadc.hi.cc.u32 r4, r11, c38, r4;\n\tmadc.hi.cc.u32 r5, r12, c38, r5;\n\tmadc.hi.cc.u32 r6, r13, c38, r6;\n\tmadc.hi.cc.u32 r7, r14, c38, r7;\n\tmadc.hi.u32 t8, r15, c38, t8;\n\tmul.lo.u32 t8, t8, c38;\n\tadd.cc.u32 r0, r0, t8;\n\taddc.cc.u32 r1, r1, 0;\n\taddc.cc.u32 r2, r2, 0;\n\taddc.cc.u32 r3, r3, 0;\n\taddc.cc.u32 r4, r4, 0;\n\taddc.cc.u32 r5, r5, 0;\n\taddc.cc.u32 r6, r6, 0;\n\taddc.cc.u32 r7, r7, 0;\n\taddc.u32 t8, 0, 0;\n\tmul.lo.u32 t8, t8, c38;\n\tadd.cc.u32 r0, r0, t8;\n\taddc.cc.u32 r1, r1, 0;\n\taddc.cc.u32 r2, r2, 0;\n\taddc.cc.u32 r3, r3, 0;\n\taddc.cc.u32 r4, r4, 0;\n\taddc.cc.u32 r5, r5, 0;\n\taddc.cc.u32 r6, r6, 0;\n\taddc.cc.u32 r7, r7, 0;\n\taddc.u32 t8, 0, 0;\n\tmov.u32 %0, r0;\n\tmov.u32 %1, r1;\n\tmov.u32 %2, r2;\n\tmov.u32 %3, r3;\n\tmov.u32 %4, r4;\n\tmov.u32 %5, r5;\n\tmov.u32 %6, r6;\n\tmov.u32 %7, r7;\n\t}"
-        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
-          "=r"(r.v[6]), "=r"(r.v[7])
-        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]),
-          "r"(a.v[7]), "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]),
-          "r"(b.v[6]), "r"(b.v[7]));
-    return r;
+// Squaring: the symmetric products once, doubled (55 multiply-adds).
+PHD fe fe_sq_impl(const fe& f) {
+    uint32_t f19[10];
+#pragma unroll
+    for (int i = 0; i < 10; i++) f19[i] = 19u * f.v[i];
+    uint64_t h[10];
+#pragma unroll
+    for (int k = 0; k < 10; k++) h[k] = 0;
+#pragma unroll
+    for (int i = 0; i < 10; i++)
+#pragma unroll
+        for (int j = i; j < 10; j++) {
+            const uint32_t c = (i != j ? 2u : 1u) * ((i & 1) && (j & 1) ? 2u : 1u);
+            const uint32_t fi = c * f.v[i];
+            const uint32_t fj = (i + j >= 10) ? f19[j] : f.v[j];
+            h[(i + j) % 10] += (uint64_t)fi * fj;
+        }
+    return fe_carry64(h);
 }
-#endif
 
-// Product scanning: the 64 32x32 products are independent and every column
-// is summed on its own (96-bit column accumulators), so only the final carry
-// sweep is serial — short dependency chains for the latency-bound single-
-// check path, where the old row-by-row carry chain dominated.
 #if defined(__CUDA_ARCH__) && defined(POSLO_FE_CALL)
-// Out-of-line field multiplication (~170 SASS instructions): the group
-// kernels call it instead of inlining it at every use, which keeps a point
-// addition at a few hundred instructions and the kernels inside the
-// instruction cache (inlined, k_check_split stalled on no_instruction).
-__device__ __noinline__ fe fe_mul_call(fe a, fe b) { return fe_mul_ptx(a, b); }
-#endif
-
-PHD fe fe_mul(const fe& a, const fe& b) {
-#ifdef __CUDA_ARCH__
-#ifdef POSLO_FE_CALL
-    return fe_mul_call(a, b);
+// Out of line in the group kernels: a point addition then stays a few hundred
+// instructions and the kernels fit the instruction cache (inlined,
+// k_check_split stalled on no_instruction).
+__device__ __noinline__ fe fe_mul_call(fe a, fe b) { return fe_mul_impl(a, b); }
+__device__ __noinline__ fe fe_sq_call(fe a) { return fe_sq_impl(a); }
+PHD fe fe_mul(const fe& a, const fe& b) { return fe_mul_call(a, b); }
+PHD fe fe_sq(const fe& a) { return fe_sq_call(a); }
 #else
-    return fe_mul_ptx(a, b);
+PHD fe fe_mul(const fe& a, const fe& b) { return fe_mul_impl(a, b); }
+PHD fe fe_sq(const fe& a) { return fe_sq_impl(a); }
 #endif
-#endif
-    uint32_t t[16];
-    uint64_t carry = 0;  // < 2^36
-#pragma unroll
-    for (int k = 0; k < 15; k++) {
-        uint64_t lo = 0;
-        uint32_t hi = 0;
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const int j = k - i;
-            if (j < 0 || j > 7) continue;
-            const uint64_t p = (uint64_t)a.v[i] * b.v[j];
-            lo += p;
-            hi += lo < p;
-        }
-        lo += carry;
-        hi += lo < carry;
-        t[k] = (uint32_t)lo;
-        carry = (lo >> 32) | ((uint64_t)hi << 32);
-    }
-    t[15] = (uint32_t)carry;
-    // 2^256 == 38 (mod p): r = t_lo + 38 * t_hi, folded twice
-    fe r;
-    uint64_t c = 0;
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        c += (uint64_t)t[i] + (uint64_t)t[i + 8] * 38;
-        r.v[i] = (uint32_t)c;
-        c >>= 32;
-    }
-    fe_fold(r.v, c);
-    return r;
-}
-
-PHD fe fe_sq(const fe& a) { return fe_mul(a, a); }
 
 PHD fe fe_sqn(fe a, int n) {
     for (int i = 0; i < n; i++) a = fe_sq(a);
     return a;
 }
 
-// Canonical representative in [0, p).
+// Canonical representative in [0, p): exact limb widths (two carry passes),
+// then v >= p  <=>  v + 19 >= 2^255.
 PHD fe fe_canon(const fe& a) {
-    fe r = a;
-    // fold bit 255: r = (r mod 2^255) + 19 * (r >> 255)  (< 2^255 + 19)
-    uint32_t top = r.v[7] >> 31;
-    r.v[7] &= 0x7fffffffu;
-    uint64_t c = (uint64_t)top * 19;
+    uint32_t h[10];
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        c += r.v[i];
-        r.v[i] = (uint32_t)c;
-        c >>= 32;
-    }
-    // r >= p  <=>  r + 19 >= 2^255
-    fe s;
-    c = 19;
+    for (int i = 0; i < 10; i++) h[i] = a.v[i];
+    for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        c += r.v[i];
-        s.v[i] = (uint32_t)c;
-        c >>= 32;
+        for (int i = 0; i < 9; i++) {
+            h[i + 1] += h[i] >> fe_width(i);
+            h[i] &= (i & 1) ? FE_M25 : FE_M26;
+        }
+        h[0] += 19 * (h[9] >> 25);
+        h[9] &= FE_M25;
     }
-    if (s.v[7] >> 31) {
-        s.v[7] &= 0x7fffffffu;
-        return s;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {  // h0 may still hold a carry from the fold
+        h[i + 1] += h[i] >> fe_width(i);
+        h[i] &= (i & 1) ? FE_M25 : FE_M26;
     }
+    uint32_t t[10];
+    uint32_t c = 19;
+#pragma unroll
+    for (int i = 0; i < 10; i++) {
+        t[i] = h[i] + c;
+        c = t[i] >> fe_width(i);
+        t[i] &= (i & 1) ? FE_M25 : FE_M26;
+    }
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 10; i++) r.v[i] = c ? t[i] : h[i];
     return r;
 }
 
@@ -207,7 +203,7 @@ PHD bool fe_is_zero(const fe& a) {
     fe c = fe_canon(a);
     uint32_t x = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) x |= c.v[i];
+    for (int i = 0; i < 10; i++) x |= c.v[i];
     return x == 0;
 }
 
@@ -249,24 +245,41 @@ PHD bool fe_sqrt_ratio_m1(const fe& u, const fe& v, fe& r) {
     return correct || flipped;
 }
 
+// 32 little-endian bytes -> limbs; bit 255 is ignored (decode compares the
+// re-encoded bytes to reject it).
 PHD fe fe_from_bytes_le(const uint8_t b[32]) {
+    uint64_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        uint64_t x = 0;
+#pragma unroll
+        for (int i = 7; i >= 0; i--) x = (x << 8) | b[8 * k + i];
+        w[k] = x;
+    }
     fe r;
 #pragma unroll
-    for (int i = 0; i < 8; i++)
-        r.v[i] = (uint32_t)b[4 * i] | (uint32_t)b[4 * i + 1] << 8 | (uint32_t)b[4 * i + 2] << 16 |
-                 (uint32_t)b[4 * i + 3] << 24;
+    for (int i = 0; i < 10; i++) {
+        const int off = fe_offset(i), q = off >> 6, sh = off & 63;
+        uint64_t x = w[q] >> sh;
+        if (sh && q < 3) x |= w[q + 1] << (64 - sh);
+        r.v[i] = (uint32_t)x & ((i & 1) ? FE_M25 : FE_M26);
+    }
     return r;
 }
 
 PHD void fe_to_bytes_le(const fe& a, uint8_t b[32]) {
-    fe c = fe_canon(a);
+    const fe c = fe_canon(a);
+    uint64_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        b[4 * i] = (uint8_t)c.v[i];
-        b[4 * i + 1] = (uint8_t)(c.v[i] >> 8);
-        b[4 * i + 2] = (uint8_t)(c.v[i] >> 16);
-        b[4 * i + 3] = (uint8_t)(c.v[i] >> 24);
+    for (int i = 0; i < 10; i++) {
+        const int off = fe_offset(i), q = off >> 6, sh = off & 63;
+        w[q] |= (uint64_t)c.v[i] << sh;
+        if (sh + fe_width(i) > 64 && q < 3) w[q + 1] |= (uint64_t)c.v[i] >> (64 - sh);
     }
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int i = 0; i < 8; i++) b[8 * k + i] = (uint8_t)(w[k] >> (8 * i));
 }
 
 PHD gpt pt_identity() {
@@ -329,12 +342,13 @@ PHD gpt pt_neg(const gpt& p) {
 // encoding, exactly the set crypto_core_ristretto255_is_valid_point rejects.
 PHD bool rist_decode(const uint8_t b[32], gpt& out) {
     fe s = fe_from_bytes_le(b);
-    // canonical: s < p (so bit 255 clear) and non-negative
-    fe sc = fe_canon(s);
-    bool canonical = true;
+    // canonical: s < p and bit 255 clear (re-encoding reproduces b), non-negative
+    uint8_t rb[32];
+    fe_to_bytes_le(s, rb);
+    uint32_t diff = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) canonical = canonical && (sc.v[i] == s.v[i]);
-    if (!canonical || (s.v[0] & 1)) return false;
+    for (int i = 0; i < 32; i++) diff |= rb[i] ^ b[i];
+    if (diff || (b[0] & 1)) return false;
     const fe d = FE_CONST(FE_D_LIMBS);
     fe ss = fe_sq(s);
     fe u1 = fe_sub(fe_one(), ss);

@@ -141,6 +141,32 @@ void dm_sc_mul_sub(const uint8_t r[32], const uint8_t y[32], const uint8_t e[32]
     le_words_out(o, out, 8);
 }
 
+// field ops through the byte interface: op 0 mul, 1 sq, 2 add, 3 sub, 4 neg, 5 canon (a only)
+void dm_fe_op(int op, const uint8_t a[32], const uint8_t b[32], uint8_t out[32]) {
+    const fe x = fe_from_bytes_le(a), y = fe_from_bytes_le(b);
+    fe r;
+    switch (op) {
+        case 0: r = fe_mul(x, y); break;
+        case 1: r = fe_sq(x); break;
+        case 2: r = fe_add(x, y); break;
+        case 3: r = fe_sub(x, y); break;
+        case 4: r = fe_neg(x); break;
+        default: r = x; break;
+    }
+    fe_to_bytes_le(r, out);
+}
+
+// a long chain of mixed operations (limb bounds under repeated lazy use)
+void dm_fe_chain(const uint8_t a[32], const uint8_t b[32], int n, uint8_t out[32]) {
+    fe x = fe_from_bytes_le(a), y = fe_from_bytes_le(b);
+    for (int i = 0; i < n; i++) {
+        fe s = fe_add(x, y), d = fe_sub(x, y);
+        x = fe_mul(s, d);
+        y = fe_sq(fe_sub(y, fe_add(s, s)));
+    }
+    fe_to_bytes_le(fe_add(x, y), out);
+}
+
 // sum of n 16-limb values via the 17-limb accumulator, reduced mod l
 void dm_sum_reduce(const uint32_t* limbs16, uint32_t n, uint8_t e_out[32]) {
     uint32_t acc[17];

@@ -178,3 +178,36 @@ def test_scalar_mul_sub(dm):
         o = out(32)
         dm.dm_sc_mul_sub(r.to_bytes(32, "little"), y.to_bytes(32, "little"), e.to_bytes(32, "little"), o)
         assert int.from_bytes(o.raw, "little") == (r - y * e) % O.L
+
+
+def test_field_arithmetic_radix_25_5(dm):
+    """GF(2^255-19) in radix 2^25.5 (ristretto.cuh) against Python integers:
+    canonical inputs, the top of the range (p - 1, 2^255 - 1 reduced), and
+    long mixed chains that keep every intermediate in lazy (carried) form."""
+    P = 2**255 - 19
+    rng = random.Random(2551)
+    edge = [0, 1, 2, 19, P - 1, P - 2, P - 19, 2**255 - 20, 2**254, 2**26 - 1, 2**51, (2**255 - 1) % P]
+    vals = edge + [rng.randrange(P) for _ in range(300)]
+    fb = lambda v: v.to_bytes(32, "little")
+    for t_ in range(400):
+        a = vals[t_ % len(vals)]
+        b = vals[(t_ * 7 + 3) % len(vals)]
+        for op, ref in ((0, a * b % P), (1, a * a % P), (2, (a + b) % P), (3, (a - b) % P), (4, (-a) % P), (5, a)):
+            o = out(32)
+            dm.dm_fe_op(op, fb(a), fb(b), o)
+            assert int.from_bytes(o.raw, "little") == ref, (op, a, b)
+    # non-canonical 32-byte inputs (>= p, bit 255 ignored) reduce like the reference's field
+    for v in (P, P + 1, 2**255 - 1):
+        o = out(32)
+        dm.dm_fe_op(5, fb(v), fb(0), o)
+        assert int.from_bytes(o.raw, "little") == (v % 2**255) % P
+    for t_ in range(20):
+        a, b = rng.randrange(P), rng.randrange(P)
+        x, y = a, b
+        for _ in range(50):
+            s, d = (x + y) % P, (x - y) % P
+            x = s * d % P
+            y = pow((y - 2 * s) % P, 2, P)
+        o = out(32)
+        dm.dm_fe_chain(fb(a), fb(b), 50, o)
+        assert int.from_bytes(o.raw, "little") == (x + y) % P

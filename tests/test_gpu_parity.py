@@ -434,3 +434,52 @@ def test_chunked_varlen_host_path_matches_device_resident(verifier):
     a = run(dev.data_ptr(), offs_dev.data_ptr(), 1)
     h = run(host.data_ptr(), offs.ctypes.data, 0)
     assert a == h
+
+
+@pytest.mark.parametrize("resident", [0, 1])
+def test_batched_epoch_checks_large(verifier, resident):
+    """> 1024 per-epoch checks take the split path (R-hat decoded on a side
+    stream, 8 lanes per check; device-resident batches also pipeline the
+    checks behind the hashing): signatures from the reference derivation
+    (signer.py) verify, and exactly the tampered epochs fail."""
+    import ctypes
+
+    import torch
+    from paper_2506_08781_b200 import _native as N
+    from paper_2506_08781_b200 import signer
+    api = A()
+    n1, n2 = 2048, 4
+    suite = api.SuiteConfig(1, n1, n2, 8)
+    rng = random.Random(41)
+    sk = signer.PoslocSecretKey(suite, rng.randrange(1, O.L).to_bytes(32, "little"),
+                                bytes(rng.getrandbits(8) for _ in range(16)),
+                                bytes(rng.getrandbits(8) for _ in range(16)))
+    batches = {i: [bytes(rng.getrandbits(8) for _ in range(32)) for _ in range(n2)] for i in range(n1)}
+    pk = signer.kg_public_key(sk, verifier)
+    s_hats = signer.sign_epochs(sk, batches, verifier)
+    bad = {5, 1024, 2047}
+    for i in bad:
+        m = bytearray(batches[i][1])
+        m[0] ^= 1
+        batches[i][1] = bytes(m)
+    ds = sk.root_stack()
+    if not resident:
+        got = verifier.epoch_verify(pk, batches, s_hats, ds)
+    else:
+        flat = b"".join(m for i in range(n1) for m in batches[i])
+        pay = torch.frombuffer(bytearray(flat), dtype=torch.uint8).cuda()
+        s_dev = torch.frombuffer(bytearray(b"".join(s_hats[i] for i in range(n1))), dtype=torch.uint8).cuda()
+        r_dev = torch.frombuffer(bytearray(b"".join(pk.r_hats[i] for i in range(n1))), dtype=torch.uint8).cuda()
+        dsb = ds.serialize()
+        dsbuf = ctypes.create_string_buffer(dsb, len(dsb))
+        epochs = np.arange(n1, dtype=np.uint32)
+        b = N.PosloBatch()
+        b.suite, b.n2, b.payload, b.payload_bytes = 1, n2, pay.data_ptr(), len(flat)
+        b.offsets, b.entry_len, b.n_entries = None, 32, n1 * n2
+        b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, n1
+        b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(dsbuf), len(dsb), ds.capacity, 1
+        verd = ctypes.create_string_buffer(n1)
+        verifier._call(verifier._lib.poslo_gpu_epoch_verify, ctypes.byref(b), pk.y, ctypes.c_void_p(s_dev.data_ptr()),
+                       ctypes.c_void_p(r_dev.data_ptr()), verd, None)
+        got = [bool(x) for x in verd.raw]
+    assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
