@@ -52,6 +52,25 @@ def test_reference_distiller_suite_passes_on_the_drop_in():
     assert summary and int(summary.group(2)) == 0 and int(summary.group(1)) >= 30, text
 
 
+FIN = os.path.join(ROOT, "oracle", "_ref", "test_poslo_f_gpu")
+
+
+def test_reference_poslo_f_suite_passes_on_the_gpu_verifiers():
+    """proj/tests/test_poslo_f.cpp (unmodified: per-entry verification, BPV
+    commitments, the signing equation, aggregated batch verification over
+    every subset, flipped seed/stack tails, key round trip) against
+    paper_2506_08781_b200/host/poslo_f_verify_gpu.cpp in place of
+    aver_f_single / aver_f_batch (poslo_f.cpp:223-246): every assertion
+    passes."""
+    if not os.path.exists(FIN):
+        pytest.fail(f"{FIN} missing: build with __graft_entry__.build() where /root/reference exists")
+    out = subprocess.run([FIN], capture_output=True, text=True, timeout=600)
+    text = out.stdout + out.stderr
+    assert out.returncode == 0 and not re.findall(r"FAILED ([^\n]+)", text), text
+    summary = re.search(r"checks: (\d+) \| failed: (\d+)", text)
+    assert summary and int(summary.group(2)) == 0 and int(summary.group(1)) >= 20, text
+
+
 ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_gpu")
 
 
