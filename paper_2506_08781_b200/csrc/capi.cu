@@ -73,6 +73,7 @@ namespace {
 
 constexpr uint64_t kChunkBytes = 64ull << 20;
 constexpr uint32_t kPipePieces = 8;  // epoch pieces when per-epoch checks overlap hashing
+constexpr uint32_t kPipeMinTiles = 2048;  // hash CTAs per piece: > 2 waves of 148 SMs x 5-6 CTAs
 constexpr int kEvSeed = 0, kEvHash = 1, kEvFin = 2, kEvSum = 3, kEvGroup = 4, kEvEnd = 5;
 
 int set_err(poslo_error* err, int code, uint32_t epoch, const char* fmt, ...) {
@@ -431,11 +432,14 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
             if (t.tile_count) launch_hash(t);
         }
-    } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && n_ep >= 2 * kPipePieces) {
-        // device-resident, uniform: epoch pieces, each finalised and handed to the caller
-        for (uint32_t q = 0; q < kPipePieces; q++) {
-            const uint32_t e0 = (uint32_t)((uint64_t)n_ep * q / kPipePieces);
-            const uint32_t e1 = (uint32_t)((uint64_t)n_ep * (q + 1) / kPipePieces);
+    } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && n_ep >= 2 * kPipePieces &&
+               tm.n_tiles >= 2 * kPipeMinTiles) {
+        // device-resident, uniform: epoch pieces, each finalised and handed to the caller;
+        // every piece keeps >= kPipeMinTiles CTAs so no piece runs the GPU part-full
+        const uint32_t pieces = std::min<uint32_t>(kPipePieces, tm.n_tiles / kPipeMinTiles);
+        for (uint32_t q = 0; q < pieces; q++) {
+            const uint32_t e0 = (uint32_t)((uint64_t)n_ep * q / pieces);
+            const uint32_t e1 = (uint32_t)((uint64_t)n_ep * (q + 1) / pieces);
             TileMap t = tm;
             t.tile_begin = e0 * tm.tiles_per_epoch;
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;

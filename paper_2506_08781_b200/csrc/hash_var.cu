@@ -23,7 +23,11 @@ constexpr int kVarT = 128;        // threads per CTA
 constexpr int kVarTile = 1024;    // entries per tile
 constexpr int kVarBuckets = 32;   // block-count buckets (clamped)
 
-constexpr int kSlotWords = 28;    // per-thread staging slot: 24-word window + x (4 words)
+// per-thread staging slot: 24-word window + E = [0, x (4 words), 0x80, 0];
+// 36 words keeps the 16-byte alignment of the vector stores and spreads the
+// same-index LDS of a warp over 8 banks (a stride of 32 would put all 32
+// lanes on one bank)
+constexpr int kSlotWords = 36;
 constexpr uint32_t kNoEntry = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t nblocks(uint64_t msg_len) { return (uint32_t)((msg_len + 9 + 63) / 64); }
@@ -56,16 +60,27 @@ __device__ __forceinline__ void stage_window(VarEntry& v, uint32_t b) {
         if (cs < a + v.L && cs + 16 > a) q = __ldg(reinterpret_cast<const uint4*>(cs));
         s4[c] = q;
     }
-    uint8_t* sb = reinterpret_cast<uint8_t*>(v.slot);
-    const int64_t w0 = (int64_t)64 * b - 4;  // m position of the first window byte we need
-    const int64_t off = (int64_t)(a - v.base);  // slot byte of m position 0
-    if (b == 0) sb[off - 1] = 0x01;  // tag byte of the second stream
-    const int64_t wend = (int64_t)64 * b + 68;
-    if (wend > (int64_t)v.L) {
-        const uint8_t* xs = reinterpret_cast<const uint8_t*>(v.slot + 24);
-        for (int64_t q = max(w0, (int64_t)v.L); q < wend; q++) {
-            const int64_t r = q - (int64_t)v.L;
-            sb[off + q] = r < 16 ? xs[r] : (r == 16 ? 0x80 : 0);
+    const int64_t off = (int64_t)(a - v.base);  // slot byte of m position 0 (negative for b > 0)
+    if (b == 0) reinterpret_cast<uint8_t*>(v.slot)[off - 1] = 0x01;  // tag byte of the second stream
+    // Suffix x || 0x80 at m positions L .. L+16. Only those bytes need writing:
+    // a chunk holding position >= L+16 starts past L and was not loaded
+    // (zero), so the neighbour bytes a loaded chunk carries past the entry
+    // all lie in L .. L+14. Five word writes at the suffix start's word
+    // alignment, funnel-shifted out of the slot tail E = [0, x0..x3, 0x80, 0].
+    const int64_t sp = off + (int64_t)v.L;  // slot byte of position L
+    if (sp < 4 * 24 && sp + 17 > 0) {
+        const uint32_t c0 = (uint32_t)sp & 3;
+        const int w0 = (int)(sp >> 2);
+        const uint32_t* E = v.slot + 24 + (c0 == 0);
+        const uint32_t sh = ((4 - c0) & 3) * 8;
+        const uint32_t keep = c0 ? (1u << (8 * c0)) - 1 : 0u;  // bytes of word w0 before position L
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const int wi = w0 + i;
+            if (wi >= 0 && wi < 24) {
+                const uint32_t sw = __funnelshift_r(E[i], E[i + 1], sh);
+                v.slot[wi] = i == 0 ? (v.slot[wi] & keep) | sw : sw;
+            }
         }
     }
 }
@@ -179,6 +194,9 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
 
     VarEntry v;
     v.slot = slots + threadIdx.x * kSlotWords;
+    v.slot[24] = 0;
+    v.slot[29] = 0x80u;
+    v.slot[30] = 0;
 #pragma unroll 1
     for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
         const uint32_t j = j0 + order[i];
@@ -232,18 +250,21 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
                     }
 #pragma unroll
                     for (int k = 0; k < 8; k++) st[k] = Hc[k];
+                } else {  // stream 0 ended one block earlier (L + 25 = 0 mod 64): add nothing
+#pragma unroll
+                    for (int k = 0; k < 8; k++) st[k] = 0;
                 }
             }
             if (active) sha256_rounds_compact<2>(st, W, r0, pk);
             if (job == 0) {  // x kept in the slot tail (bytes in stream order) for the suffix writes
                 const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
 #pragma unroll
-                for (int k = 0; k < 4; k++) v.slot[24 + k] = bswap32(st[k] + iv[k]);
+                for (int k = 0; k < 4; k++) v.slot[25 + k] = bswap32(st[k] + iv[k]);
                 continue;
             }
 #pragma unroll
             for (int k = 0; k < 8; k++) {
-                const uint32_t c = active ? Hc[k] + st[k] : Hc[k];
+                const uint32_t c = Hc[k] + st[k];
                 Hc[k] = Ho[k];
                 Ho[k] = c;
             }

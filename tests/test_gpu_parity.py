@@ -187,6 +187,27 @@ def test_uniform_batches_match_oracle(verifier, suite, n1, n2, L):
     assert e_hat == O.sum_scalars(ref)
 
 
+@pytest.mark.parametrize("suite", [1, 2])
+def test_every_entry_length_and_alignment(verifier, suite):
+    """Every entry length 0..320 (each residue mod 64 five times: the block
+    boundaries of both hash streams, incl. L + 25 = 0 mod 64 where stream 0
+    ends one block before stream 1) at every start alignment mod 16."""
+    api = A()
+    rng = np.random.default_rng(4242 + suite)
+    n1, n2 = 16, 321
+    batches = {}
+    for i in range(n1):
+        lens = rng.permutation(n2)
+        batches[i] = [bytes(rng.integers(0, 256, int(L), dtype=np.uint8)) for L in lens]
+    cfg = api.SuiteConfig(suite, n1, n2, 1)
+    D = (n1 - 1).bit_length()
+    ds = api.SeedStack(D, [api.SeedNode(D, 0, bytes(range(16)))])
+    parts, e_hat = verifier.agg_ekeys(cfg, batches, ds, 1)
+    ref = _oracle_etilde(suite, batches, ds)
+    assert [p[1] for p in parts] == ref
+    assert e_hat == O.sum_scalars(ref)
+
+
 @pytest.mark.parametrize("suite", [1, 2, 3])
 def test_ragged_batches_match_oracle(verifier, suite):
     """Variable-length entries (incl. empty ones) and uneven epoch sizes."""
@@ -448,7 +469,7 @@ def test_batched_epoch_checks_large(verifier, resident):
     from paper_2506_08781_b200 import _native as N
     from paper_2506_08781_b200 import signer
     api = A()
-    n1, n2 = 2048, 4
+    n1, n2 = 4096, 4  # 4096 one-epoch tiles: two pipelined pieces of kPipeMinTiles (capi.cu)
     suite = api.SuiteConfig(1, n1, n2, 8)
     rng = random.Random(41)
     sk = signer.PoslocSecretKey(suite, rng.randrange(1, O.L).to_bytes(32, "little"),
@@ -457,7 +478,7 @@ def test_batched_epoch_checks_large(verifier, resident):
     batches = {i: [bytes(rng.getrandbits(8) for _ in range(32)) for _ in range(n2)] for i in range(n1)}
     pk = signer.kg_public_key(sk, verifier)
     s_hats = signer.sign_epochs(sk, batches, verifier)
-    bad = {5, 1024, 2047}
+    bad = {5, 1024, 2047, 4095}
     for i in bad:
         m = bytearray(batches[i][1])
         m[0] ^= 1
