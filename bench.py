@@ -188,15 +188,22 @@ def cpu_model():
 
 
 def cpu_baseline(a):
-    r = run_ref_tool(a.cpu_log2n, a.n2, a.entry_len, a.suite, a.seed, 1)
+    per_epoch = a.mode != "coarse"
+    # varlen entries cost ~6.6x the compressions of a 32-byte one: a 16x smaller sample
+    log2n = a.cpu_log2n - (4 if a.varlen else 0)
+    r = run_ref_tool(log2n, a.n2, 0 if a.varlen else a.entry_len, a.suite, a.seed, 1,
+                     "epoch" if per_epoch else "coarse")
     if r is None:
         return None
+    what = ("the shipped per-epoch poslo::aver loop (proj/src/poslo_c.cpp:192-213, as acceptance.cpp:477-481), "
+            "epochs sharded over all host threads" if per_epoch else
+            "reference poslo::paver (proj/src/batch_verify.cpp:64-87)")
+    shape = "syslog-style 64..1024-byte" if a.varlen else f"{a.entry_len}-byte"
     return {"value": round(r["eps_best"], 1), "unit": "entries/s", "cores": r["workers"],
             "kind": "reference",
-            "sample": f"reference poslo::paver (proj/src/batch_verify.cpp:64-87, OpenSSL 3 + libsodium 1.0.20) "
-                      f"on an epoch-aligned 2^{a.cpu_log2n}-entry prefix of the same synthetic log "
-                      f"(n2={a.n2}, suite {a.suite}), workers={r['workers']} = all host threads, "
-                      f"{cpu_model()}; {r['best_s']:.2f} s wall"}
+            "sample": f"{what}, OpenSSL 3 + libsodium 1.0.20, on an epoch-aligned 2^{log2n}-entry prefix of the "
+                      f"same synthetic {shape} log (n2={a.n2}, suite {a.suite}), workers={r['workers']} = all "
+                      f"host threads, {cpu_model()}; {r['best_s']:.2f} s wall"}
 
 
 def reference_arm(a, rank, world):
@@ -262,7 +269,7 @@ def int_peak(device):
     lib.poslo_microbench_int_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(ctypes.c_double)]
     res = {}
-    for mode, name in ((0, "alu"), (1, "fma"), (2, "dual")):
+    for mode, name in ((0, "alu"), (1, "fma"), (2, "dual"), (10, "lds")):
         v, ms = ctypes.c_double(), ctypes.c_double()
         if lib.poslo_microbench_int_peak(device, mode, ctypes.byref(v), ctypes.byref(ms)) == 0:
             res[name] = v.value
@@ -655,6 +662,33 @@ def main():
                                        "measured LOP3+IMAD dual-issue rate"},
                 "hbm": {"achieved": round(hbm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(hbm_gbs / hbm_peak, 4), "peak_source": hbm_src},
+                "share_of_step": round(hash_avg_ms / ms_per_step, 4)}
+
+    if a.suite == 2 and not a.varlen and a.entry_len == 32 and hash_avg_ms and peaks.get("lds"):
+        # Suite 2 is bound by the AES T-table lookups (shared memory, one
+        # 32-bit LDS per lookup): 17 AES-128 per entry (onetime_seed's second
+        # MMO block - the first is hoisted per epoch - and 2 x 4 MDC-2 blocks of
+        # 2 AES), each 160 state + 40 key-schedule lookups.
+        LOOKUPS = 17 * 200
+        rate = n / (hash_avg_ms * 1e-3)
+        achieved = LOOKUPS * rate / 1e12
+        peak = peaks["lds"] / 1e12
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            tj = json.load(open(tf)).get("k_hash_s2")
+            if tj and tj.get("entries") == n:
+                traffic = tj["dram_bytes"]
+        roof = {"bound": "shared-memory table lookups (LSU)", "kernel": "k_hash_s2_l32", "achieved": round(achieved, 3),
+                "peak": round(peak, 3), "unit": "T lookups/s (32-bit LDS lanes)", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "traffic_unit": "bytes per launch (dram read + write, ncu --set full)",
+                "algorithmic_bytes": payload_bytes, "ops_per_entry": LOOKUPS,
+                "ops_basis": "17 AES-128 per 32-byte entry x (10 rounds x 16 T-table + 10 x 4 key-schedule lookups)",
+                "ms_per_launch": round(hash_avg_ms, 4),
+                "peak_source": "measured live: data-dependent LDS chains on a bank-replicated 256 x 32 table "
+                               "(paper_2506_08781_b200/csrc/microbench.cu mode 10)",
+                "alu_pipe": {"peak": round(peaks["alu"] / 1e12, 2), "unit": "Tops/s",
+                             "note": "co-bound: PRMT byte picks, rotations and XORs of the rounds"},
                 "share_of_step": round(hash_avg_ms / ms_per_step, 4)}
 
     line = {

@@ -447,7 +447,16 @@ int cmd_bench(int argc, char** argv) {
     for (uint32_t i = 0; i < n1; i++) {
         std::vector<Bytes> ep;
         ep.reserve(n2);
-        for (uint32_t j = 0; j < n2; j++) ep.push_back(synth_entry(seed, uint64_t(i) * n2 + j, len));
+        for (uint32_t j = 0; j < n2; j++) {
+            const uint64_t k = uint64_t(i) * n2 + j;
+            if (len) {
+                ep.push_back(synth_entry(seed, k, len));
+            } else {  // LEN 0: the syslog-style log of BASELINE config 4 (bench.py --varlen)
+                Bytes b(poslo_synth_varlen(seed, k));
+                for (size_t t = 0; t < b.size(); t++) b[t] = poslo_synth_ascii(seed, k, uint32_t(t));
+                ep.push_back(std::move(b));
+            }
+        }
         batches.emplace(i, std::move(ep));
     }
     Scalar y = Scalar::random();

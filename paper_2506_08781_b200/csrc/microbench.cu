@@ -9,6 +9,9 @@
 //   5  SHF.R.W funnel rotate (ALU pipe)       6  IMAD.HI immediate
 //   7  LOP3 + IMAD.HI immediate
 //   8  IMAD.WIDE.U32, 64-bit addend          9  LOP3 + IMAD.WIDE.U32
+//  10  shared-memory table lookups: data-dependent 32-bit LDS from a
+//      bank-replicated 256-entry table ([x][lane], the AES T-table layout of
+//      tile_common.cuh SmemT0), i.e. the suite-2 kernel's bound
 // Every thread runs 8 independent chains; lane-ops = threads * iters * 8 (16 for mode 2).
 // Not part of the verifier ABI (separate library libposlo_microbench.so).
 #include <cuda_runtime.h>
@@ -51,6 +54,24 @@ __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uin
     if (r == 0x12345678u) out[0] = r;
 }
 
+__global__ void __launch_bounds__(256) k_lds_peak(uint32_t* out, uint32_t a, int iters) {
+    extern __shared__ uint32_t tab[];  // 256 x 32 words
+    const uint32_t lane = threadIdx.x & 31u;
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) tab[i] = (uint32_t)i * 0x9e3779b9u ^ a;
+    __syncthreads();
+    uint32_t x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = threadIdx.x * (k + 7) ^ a;
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = tab[__byte_perm(x[k], 0u, 0x4441u) * 32u + lane];
+    }
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) r ^= x[k];
+    if (r == 0x12345678u) out[0] = r;
+}
+
 extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s, double* ms_out) {
     if (cudaSetDevice(device) != cudaSuccess) return 1;
     cudaDeviceProp p;
@@ -58,7 +79,8 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     uint32_t* out;
     cudaMalloc(&out, 4);
     int blocks = p.multiProcessorCount * 8;  // 2048 threads per SM
-    int iters = 1 << 16;
+    int iters = mode == 10 ? 1 << 14 : 1 << 16;
+    if (mode == 10) cudaFuncSetAttribute(k_lds_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -74,6 +96,7 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
             case 6: k_int_peak<6><<<blocks, 256>>>(out, a, b, iters); break;
             case 7: k_int_peak<7><<<blocks, 256>>>(out, a, b, iters); break;
             case 8: k_int_peak<8><<<blocks, 256>>>(out, a, b, iters); break;
+            case 10: k_lds_peak<<<blocks / 2, 256, 32768>>>(out, a, iters); break;
             default: k_int_peak<9><<<blocks, 256>>>(out, a, b, iters); break;
         }
     };
@@ -87,7 +110,7 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     double per_iter = (mode == 2 || mode == 4 || mode == 7 || mode == 9) ? 16.0 : 8.0;
-    double ops = (double)blocks * 256 * iters * per_iter * reps;
+    double ops = (double)(mode == 10 ? blocks / 2 : blocks) * 256 * iters * per_iter * reps;
     *ops_per_s = ops / (ms * 1e-3);
     if (ms_out) *ms_out = ms / reps;
     cudaEventDestroy(e0);

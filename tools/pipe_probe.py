@@ -11,7 +11,8 @@ lib = ctypes.CDLL(os.path.join(ROOT, "paper_2506_08781_b200", "libposlo_microben
 lib.poslo_microbench_int_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_double)]
 names = {0: "LOP3", 1: "IMAD reg", 2: "LOP3+IMAD reg", 3: "IMAD imm", 4: "LOP3+IMAD imm",
-         5: "SHF.R.W", 6: "IMAD.HI imm", 7: "LOP3+IMAD.HI imm", 8: "IMAD.WIDE acc64", 9: "LOP3+IMAD.WIDE"}
+         5: "SHF.R.W", 6: "IMAD.HI imm", 7: "LOP3+IMAD.HI imm", 8: "IMAD.WIDE acc64", 9: "LOP3+IMAD.WIDE",
+         10: "LDS table lookup"}
 out = {}
 for rep in range(2):
     for m, n in names.items():
