@@ -6,12 +6,13 @@
 // "memory words" (byte 4c+r of the block = bits 8r..8r+7 of word c), which is
 // exactly what a 32-bit load of the block from memory yields. Round function
 // is the T-table formulation over ONE table T0 (bytes 2S,S,S,3S), the other
-// three being byte rotations of it. The table lives in shared memory
+// three being byte rotations of it (or stored, see SmemT4). The table lives in shared memory
 // replicated once per bank ([x][lane] layout, 32 KiB) so the 16 data-dependent
 // lookups of a round never bank-conflict; S[x] is byte 1 of T0[x].
 //
 // The table is passed as a "lookup" functor so the same code runs from shared
-// memory on the device and from a plain array in the host-side unit tests.
+// memory on the device and from a plain array in the host-side unit tests:
+// lk(w, k) = T0[byte k of w], lkr(w, k, r) = rotl(T0[byte k of w], 8r).
 #pragma once
 #include "poslo_common.cuh"
 
@@ -85,10 +86,12 @@ PHD void aes128_encrypt(const T0& t0, const uint32_t key[4], const uint32_t in[4
         k2 ^= k1;
         k3 ^= k2;
         rcon = (rcon << 1) ^ ((rcon & 0x80u) ? 0x11bu : 0u);
-        const uint32_t n0 = t0.lk(s0, 0) ^ rotl32(t0.lk(s1, 1), 8) ^ rotl32(t0.lk(s2, 2), 16) ^ rotl32(t0.lk(s3, 3), 24);
-        const uint32_t n1 = t0.lk(s1, 0) ^ rotl32(t0.lk(s2, 1), 8) ^ rotl32(t0.lk(s3, 2), 16) ^ rotl32(t0.lk(s0, 3), 24);
-        const uint32_t n2 = t0.lk(s2, 0) ^ rotl32(t0.lk(s3, 1), 8) ^ rotl32(t0.lk(s0, 2), 16) ^ rotl32(t0.lk(s1, 3), 24);
-        const uint32_t n3 = t0.lk(s3, 0) ^ rotl32(t0.lk(s0, 1), 8) ^ rotl32(t0.lk(s1, 2), 16) ^ rotl32(t0.lk(s2, 3), 24);
+        // T_r[x] = rotl(T0[x], 8r): lkr(w, k, r) = T_r[byte k of w] (a rotation
+        // of a T0 lookup, or a lookup in a stored T_r, per table functor)
+        const uint32_t n0 = t0.lk(s0, 0) ^ t0.lkr(s1, 1, 1) ^ t0.lkr(s2, 2, 2) ^ t0.lkr(s3, 3, 3);
+        const uint32_t n1 = t0.lk(s1, 0) ^ t0.lkr(s2, 1, 1) ^ t0.lkr(s3, 2, 2) ^ t0.lkr(s0, 3, 3);
+        const uint32_t n2 = t0.lk(s2, 0) ^ t0.lkr(s3, 1, 1) ^ t0.lkr(s0, 2, 2) ^ t0.lkr(s1, 3, 3);
+        const uint32_t n3 = t0.lk(s3, 0) ^ t0.lkr(s0, 1, 1) ^ t0.lkr(s1, 2, 2) ^ t0.lkr(s2, 3, 3);
         s0 = n0 ^ k0;
         s1 = n1 ^ k1;
         s2 = n2 ^ k2;

@@ -20,6 +20,7 @@ struct HostT0 {
     }
     uint32_t operator()(uint32_t x) const { return t[x]; }
     uint32_t lk(uint32_t w, int k) const { return t[(w >> (8 * k)) & 0xffu]; }
+    uint32_t lkr(uint32_t w, int k, int r) const { return rotl32(lk(w, k), 8 * r); }
 };
 const HostT0& T0() {
     static HostT0 t;
