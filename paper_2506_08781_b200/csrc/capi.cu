@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -73,6 +74,14 @@ namespace {
 
 constexpr uint64_t kChunkBytes = 64ull << 20;
 constexpr uint32_t kPipePieces = 8;  // epoch pieces when per-epoch checks overlap hashing
+// POSLO_PIPE_PIECES overrides it (tuning; 1 = hash everything, then check)
+uint32_t pipe_pieces() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("POSLO_PIPE_PIECES");
+        return e ? (uint32_t)std::max(1, std::atoi(e)) : kPipePieces;
+    }();
+    return v;
+}
 constexpr uint32_t kPipeMinTiles = 2048;  // hash CTAs per piece: > 2 waves of 148 SMs x 5-6 CTAs
 constexpr int kEvSeed = 0, kEvHash = 1, kEvFin = 2, kEvSum = 3, kEvGroup = 4, kEvEnd = 5;
 
@@ -432,11 +441,11 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
             if (t.tile_count) launch_hash(t);
         }
-    } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && n_ep >= 2 * kPipePieces &&
-               tm.n_tiles >= 2 * kPipeMinTiles) {
+    } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && pipe_pieces() > 1 &&
+               n_ep >= 2 * pipe_pieces() && tm.n_tiles >= 2 * kPipeMinTiles) {
         // device-resident, uniform: epoch pieces, each finalised and handed to the caller;
         // every piece keeps >= kPipeMinTiles CTAs so no piece runs the GPU part-full
-        const uint32_t pieces = std::min<uint32_t>(kPipePieces, tm.n_tiles / kPipeMinTiles);
+        const uint32_t pieces = std::min<uint32_t>(pipe_pieces(), tm.n_tiles / kPipeMinTiles);
         for (uint32_t q = 0; q < pieces; q++) {
             const uint32_t e0 = (uint32_t)((uint64_t)n_ep * q / pieces);
             const uint32_t e1 = (uint32_t)((uint64_t)n_ep * (q + 1) / pieces);
