@@ -84,7 +84,15 @@ typedef struct poslo_batch {
     uint32_t record_header;        /* 0, or 4 for a raw log file (log_file.hpp:34-51): `payload` is
                                       the file's bytes, offsets[t] the position of record t's LE32
                                       length and the entry is payload[offsets[t] + 4 .. offsets[t+1])
-                                      (offsets from poslo_log_scan; zero-copy ingestion) */
+                                      (offsets from poslo_log_scan; zero-copy ingestion).
+                                      With offsets == NULL the payload is a WHOLE raw image whose
+                                      records the device finds itself (read_log + epochs_of): the
+                                      record count must be n_epochs x n2 (uniform epochs). A host
+                                      image is then copied in 64 MiB chunks with the record scan and
+                                      the hashing of every completed epoch behind the copy. Errors:
+                                      FormatError "truncated log record" (read_log), "record count
+                                      must be a nonzero multiple of n2" (epochs_of), then
+                                      INVALID_ARGUMENT when the count names other epochs. */
 } poslo_batch;
 
 /* Scheme F (POSLO-F, include/poslo/poslo_f.hpp) entries: each entry t has a
@@ -131,7 +139,8 @@ int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int
 /* ---- context -------------------------------------------------------------- */
 int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);
 void poslo_gpu_destroy(poslo_gpu_ctx* ctx);
-/* Run subsequent work on this cudaStream_t (NULL = the context's own stream). */
+/* Run subsequent work on this cudaStream_t (NULL = the context's own stream,
+ * a blocking stream: ordered after work on the legacy default stream). */
 int poslo_gpu_set_stream(poslo_gpu_ctx* ctx, void* cuda_stream);
 /* Device stage timings (ms) of the last call when enabled: [seed, hash,
  * epoch_finalize, sum, group, total]. */

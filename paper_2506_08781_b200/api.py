@@ -409,6 +409,26 @@ class Verifier:
         raw = out.raw
         return [bool(raw[k]) for k in range(len(eps))]
 
+    def epoch_verify_packed(self, pk: PoslocPublicKey, pb, s_hats: Dict[int, bytes]):
+        """epoch_verify over a packed / record / image batch (logfile.py). A
+        device-resident batch takes device-resident signature arrays too (the
+        C-ABI contract), so s-hat / R-hat are staged into HBM for it."""
+        eps = [int(e) for e in pb.epochs]
+        s = b"".join(s_hats[e] for e in eps)
+        r = b"".join(pk.r_hats[e] for e in eps)
+        out = ctypes.create_string_buffer(max(len(eps), 1))
+        cb = pb.cstruct()
+        if cb.device_resident:
+            import torch
+            keep = [torch.frombuffer(bytearray(x or b"\0"), dtype=torch.uint8).cuda() for x in (s, r)]
+            torch.cuda.synchronize()
+            sp, rp = (ctypes.c_void_p(t.data_ptr()) for t in keep)
+        else:
+            sp, rp = _buf(s), _buf(r)
+        self._call(self._lib.poslo_gpu_epoch_verify, ctypes.byref(cb), _buf(pk.y), sp, rp, out, None)
+        raw = out.raw
+        return [bool(raw[k]) for k in range(len(eps))]
+
     # -- batched coarse distillation (distiller.cpp:60-89): verdicts + masked umbrella folds
     def distill_coarse(self, pk: PoslocPublicKey, batches, sigs: Dict[int, "EpochSignature"],
                        seg: Sequence[int]):

@@ -38,6 +38,7 @@ struct PinnedStage {  // pinned host landing zone for the per-call small D2H cop
     unsigned long long err_init;  // H2D: error word seeded with host-detected seed failures
     int flags[4];
     uint8_t verdict;
+    unsigned long long scan[3];  // raw-image scan state {next record, records so far} + sentinel
 };
 
 struct poslo_gpu_ctx {
@@ -52,7 +53,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;
@@ -243,6 +244,25 @@ bool is_uniform(const poslo_batch* b) {
     return true;
 }
 
+// After the whole raw image is scanned: read_log's FormatError on a
+// truncated record, epochs_of's on a count that is not a nonzero multiple of
+// n2 (tools/poslo.cpp:32-40), and the batch must name exactly that many
+// epochs; then offsets[n] = image length (the record-end sentinel).
+int raw_scan_result(poslo_gpu_ctx* ctx, const poslo_batch* b, uint64_t n_entries,
+                    const unsigned long long* d_state, uint64_t* d_off, cudaStream_t s, poslo_error* err) {
+    CU(cudaMemcpyAsync(ctx->stage->scan, d_state, 16, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const unsigned long long q = ctx->stage->scan[0], total = ctx->stage->scan[1];
+    if (q == ~0ull) return set_err(err, POSLO_FORMAT_ERROR, 0, "truncated log record");
+    if (total == 0 || total % b->n2) return set_err(err, POSLO_FORMAT_ERROR, 0, "record count must be a nonzero multiple of n2");
+    if (total != n_entries)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "log holds %llu epochs, the batch names %u",
+                       (unsigned long long)(total / b->n2), b->n_epochs);
+    ctx->stage->scan[2] = b->payload_bytes;
+    CU(cudaMemcpyAsync(d_off + total, &ctx->stage->scan[2], 8, cudaMemcpyHostToDevice, s));
+    return POSLO_OK;
+}
+
 // Stages 0-2 for a batch: leaves per-epoch e~ (8 limbs each) in
 // ctx->b_etilde and returns the status after reading the error word.
 int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error* err) {
@@ -264,10 +284,16 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         if (rc) return rc;
     }
     P.uniform = is_uniform(b);
+    // Raw record image (record_header = 4, no offsets): the records are found
+    // on the device (log_scan.cu) and, for a host image, the record scan and
+    // the hashing run chunk by chunk behind the H2D copy.
+    const bool raw_image = b->record_header == 4 && !b->offsets;
+    if (raw_image && !P.uniform)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "a raw record image needs uniform epochs of n2 records");
     uint64_t n_entries = P.uniform ? (uint64_t)b->n_epochs * b->n2 : b->epoch_starts[b->n_epochs];
     if (b->epoch_starts && b->epoch_starts[0] != 0)
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epoch_starts[0] must be 0");
-    if (n_entries > b->n_entries)
+    if (n_entries > b->n_entries && !raw_image)
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "batch describes more entries than given");
     if (n_entries && !b->payload && !(b->offsets == nullptr && b->entry_len == 0))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null payload");
@@ -286,14 +312,15 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     // stream in epoch-aligned 64 MiB chunks on the copy stream, each chunk's
     // hashing waiting only for its own bytes (SPEC.md:496 chunked streaming).
     P.lay.entry_len = b->entry_len;
-    if (b->record_header != 0 && (b->record_header != 4 || !b->offsets))
-        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "record_header must be 0, or 4 with record offsets");
+    if (b->record_header != 0 && b->record_header != 4)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "record_header must be 0 or 4");
     P.lay.header = b->record_header;
     const uint64_t epoch_bytes = (uint64_t)b->n2 * b->entry_len;
     // Host-resident uniform logs (fixed length, or byte offsets / raw record
     // images) stream in epoch-aligned chunks of <= 64 MiB on the copy stream.
-    const bool chunked = !b->device_resident && P.uniform && (b->offsets || epoch_bytes > 0) &&
+    const bool chunked = !raw_image && !b->device_resident && P.uniform && (b->offsets || epoch_bytes > 0) &&
                          b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
+    const bool raw_chunked = raw_image && !b->device_resident && b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
     auto epoch_byte = [&](uint32_t e) -> uint64_t {  // first payload byte of the e-th queried epoch
         return b->offsets ? b->offsets[(uint64_t)e * b->n2] : (uint64_t)e * epoch_bytes;
     };
@@ -303,7 +330,7 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     } else {
         uint8_t* d_pay;
         ENSURE(b_payload, b->payload_bytes, d_pay);
-        if (b->payload_bytes && !chunked)
+        if (b->payload_bytes && !chunked && !raw_chunked)
             CU(cudaMemcpyAsync(d_pay, b->payload, b->payload_bytes, cudaMemcpyHostToDevice, s));
         P.lay.payload = d_pay;
         P.lay.offsets = nullptr;
@@ -312,6 +339,34 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             ENSURE(b_offsets, b->n_entries + 1, d_off);
             CU(cudaMemcpyAsync(d_off, b->offsets, (b->n_entries + 1) * 8, cudaMemcpyHostToDevice, s));
             P.lay.offsets = d_off;
+        }
+    }
+
+    // raw image: record offsets found on the device
+    // record chunks: 1 MiB for a one-shot scan, kRawScanChunk when pipelined
+    // (exits then only for one copy chunk's worth of record chunks at a time)
+    const uint64_t scan_chunk = raw_chunked ? kRawScanChunk : kScanChunk;
+    const uint32_t n_scan = (uint32_t)((b->payload_bytes + scan_chunk - 1) / scan_chunk);
+    const uint32_t exit_chunks = raw_chunked ? (uint32_t)(kChunkBytes / kRawScanChunk) : n_scan;
+    uint64_t *d_sc_exit = nullptr, *d_sc_start = nullptr, *d_sc_base = nullptr;
+    uint32_t* d_sc_cnt = nullptr;
+    unsigned long long* d_sc_state = nullptr;
+    if (raw_image) {
+        uint64_t* d_off;
+        ENSURE(b_scan_off, n_entries + 1, d_off);
+        ENSURE(b_scan_exit, (size_t)std::max<uint32_t>(exit_chunks, 1) * kScanWindow, d_sc_exit);
+        ENSURE(b_scan_cnt, (size_t)std::max<uint32_t>(exit_chunks, 1) * kScanWindow, d_sc_cnt);
+        ENSURE(b_scan_start, std::max<uint32_t>(n_scan, 1), d_sc_start);
+        ENSURE(b_scan_base, std::max<uint32_t>(n_scan, 1), d_sc_base);
+        ENSURE(b_scan_state, 2, d_sc_state);
+        CU(cudaMemsetAsync(d_sc_state, 0, 16, s));
+        P.lay.offsets = d_off;
+        if (!raw_chunked) {
+            launch_log_scan_range(P.lay.payload, b->payload_bytes, 0, n_scan, scan_chunk, d_sc_exit, d_sc_cnt,
+                                  d_sc_start, d_sc_base, d_sc_state, d_off, n_entries + 1, s);
+            ctx->launches += 3;
+            int rc2 = raw_scan_result(ctx, b, n_entries, d_sc_state, d_off, s, err);
+            if (rc2) return rc2;
         }
     }
 
@@ -341,7 +396,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     tm.n_epochs = n_ep;
     tm.n2 = b->n2;
     bool aligned = ((uintptr_t)P.lay.payload & 15) == 0;
-    P.fast = P.uniform && !b->offsets && b->entry_len == 32 && (b->suite == 1 || b->suite == 2) && aligned;
+    P.fast = !raw_image && P.uniform && !b->offsets && b->entry_len == 32 && (b->suite == 1 || b->suite == 2) &&
+             aligned;
     uint32_t* d_partial = nullptr;
     if (P.uniform) {
         if (P.fast && b->suite == 1 && b->n2 <= kLeanMaxN2)
@@ -407,7 +463,58 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         }
         ctx->launches += 1;
     };
-    if (chunked) {
+    if (raw_chunked) {
+        // all copies queued first (kChunkBytes each, on the copy stream); then per
+        // copy chunk c: scan its record chunks once chunk c + 1 has landed (a
+        // record header may straddle into it), extend the true record chain,
+        // and hash every epoch whose records are now all known and present
+        const uint64_t len = b->payload_bytes;
+        const uint32_t n_cc = (uint32_t)((len + kChunkBytes - 1) / kChunkBytes);
+        const uint32_t per_cc = (uint32_t)(kChunkBytes / kRawScanChunk);
+        while (ctx->chunk_ev.size() < n_cc + 1) {
+            cudaEvent_t ev;
+            CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            ctx->chunk_ev.push_back(ev);
+        }
+        CU(cudaEventRecord(ctx->chunk_ev[n_cc], s));
+        CU(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[n_cc], 0));
+        uint8_t* d_pay = const_cast<uint8_t*>(P.lay.payload);
+        for (uint32_t c = 0; c < n_cc; c++) {
+            const uint64_t off = (uint64_t)c * kChunkBytes, bytes = std::min<uint64_t>(kChunkBytes, len - off);
+            CU(cudaMemcpyAsync(d_pay + off, b->payload + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
+            CU(cudaEventRecord(ctx->chunk_ev[c], ctx->copy));
+        }
+        uint64_t* d_off = const_cast<uint64_t*>(P.lay.offsets);
+        uint32_t e_done = 0;
+        for (uint32_t c = 0; c < n_cc; c++) {
+            const bool last = c + 1 == n_cc;
+            CU(cudaStreamWaitEvent(s, ctx->chunk_ev[last ? c : c + 1], 0));
+            launch_log_scan_range(P.lay.payload, len, c * per_cc, std::min<uint32_t>((c + 1) * per_cc, n_scan),
+                                  kRawScanChunk, d_sc_exit, d_sc_cnt, d_sc_start, d_sc_base, d_sc_state, d_off,
+                                  n_entries + 1, s);
+            ctx->launches += 3;
+            uint32_t e_ready;
+            if (last) {
+                int rc2 = raw_scan_result(ctx, b, n_entries, d_sc_state, d_off, s, err);
+                if (rc2) return rc2;
+                e_ready = n_ep;
+            } else {
+                CU(cudaMemcpyAsync(ctx->stage->scan, d_sc_state, 16, cudaMemcpyDeviceToHost, s));
+                CU(cudaStreamSynchronize(s));
+                if (ctx->stage->scan[0] == ~0ull) continue;  // truncated: reported after the last chunk
+                // epoch e is complete once record (e + 1) n2 has been seen (its start bounds e's last record)
+                const uint64_t seen = ctx->stage->scan[1];
+                e_ready = seen ? (uint32_t)std::min<uint64_t>(n_ep, (seen - 1) / b->n2) : 0;
+            }
+            if (e_ready > e_done) {
+                TileMap t = tm;
+                t.tile_begin = e_done * tm.tiles_per_epoch;
+                t.tile_count = (e_ready - e_done) * tm.tiles_per_epoch;
+                launch_hash(t);
+                e_done = e_ready;
+            }
+        }
+    } else if (chunked) {
         // chunk c covers epochs [cut[c], cut[c+1]): as many whole epochs as fit in kChunkBytes (>= 1)
         std::vector<uint32_t> cut{0};
         while (cut.back() < n_ep) {
@@ -634,7 +741,11 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     CU(cudaSetDevice(device));
     poslo_gpu_ctx* ctx = new poslo_gpu_ctx();
     ctx->device = device;
-    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    // The context's own stream is a BLOCKING stream: work a caller queued on
+    // the legacy default stream (e.g. torch's default stream filling a
+    // device-resident batch) is ordered before ours without an explicit
+    // sync. Internal copy / side streams stay non-blocking.
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamDefault);
     if (e != cudaSuccess) {
         delete ctx;
         return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
@@ -672,7 +783,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
                       &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok,
                       &ctx->b_scan_exit, &ctx->b_scan_cnt, &ctx->b_scan_start, &ctx->b_scan_base,
-                      &ctx->b_scan_off};
+                      &ctx->b_scan_off, &ctx->b_scan_state};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);

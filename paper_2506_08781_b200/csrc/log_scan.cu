@@ -38,13 +38,15 @@ __device__ __forceinline__ uint64_t step(const uint8_t* raw, uint64_t n, uint64_
 constexpr int kScanThreads = 256;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_chunk(const uint8_t* __restrict__ raw, uint64_t n,
+                                                             uint32_t first, uint64_t chunk_bytes,
                                                              uint64_t* __restrict__ exit_out,
                                                              uint32_t* __restrict__ count_out) {
     __shared__ uint64_t s_exit[kScanWindow];
     __shared__ uint32_t s_cnt[kScanWindow];
     __shared__ int16_t s_link[kScanWindow];
-    const uint64_t c0 = (uint64_t)blockIdx.x * kScanChunk;
-    const uint64_t cend = min(c0 + kScanChunk, n);
+    const uint32_t chunk = first + blockIdx.x;
+    const uint64_t c0 = (uint64_t)chunk * chunk_bytes;
+    const uint64_t cend = min(c0 + chunk_bytes, n);
     const uint64_t wend = min(c0 + kScanWindow, cend);
     for (uint32_t k = threadIdx.x; k < kScanWindow; k += kScanThreads) {
         const uint64_t q = c0 + k;
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_chunk(const uint8_t* __re
         __syncthreads();
     }
     for (uint32_t k = threadIdx.x; k < kScanWindow; k += kScanThreads) {
-        exit_out[(uint64_t)blockIdx.x * kScanWindow + k] = s_exit[k];
+        exit_out[(uint64_t)blockIdx.x * kScanWindow + k] = s_exit[k];  // relative to `first`
         count_out[(uint64_t)blockIdx.x * kScanWindow + k] = s_cnt[k];
     }
 }
@@ -147,11 +149,72 @@ __global__ void k_scan_emit(const uint8_t* __restrict__ raw, uint64_t n, uint32_
     }
 }
 
+// Incremental form of the stitch for a pipelined ingestion (chunks arrive
+// one after another): continues the true chain from state = {next record
+// position q (kTrunc after a truncated record), records so far} through the
+// chunks [c_first, c_last), which must all have been scanned by k_scan_chunk.
+__global__ void k_scan_stitch_inc(const uint8_t* __restrict__ raw, uint64_t n, uint32_t c_first, uint32_t c_last,
+                                  uint64_t chunk_bytes, const uint64_t* __restrict__ exits,
+                                  const uint32_t* __restrict__ counts, uint64_t* __restrict__ start,
+                                  uint64_t* __restrict__ base, unsigned long long* __restrict__ state) {
+    if (threadIdx.x || blockIdx.x) return;
+    for (uint32_t c = c_first; c < c_last; c++) start[c] = kTrunc;
+    uint64_t q = state[0], total = state[1];
+    const uint64_t lim = min((uint64_t)c_last * chunk_bytes, n);
+    while (q != kTrunc && q < lim) {
+        const uint64_t c = q / chunk_bytes, off = q - c * chunk_bytes;
+        start[c] = q;
+        base[c] = total;
+        uint64_t p;
+        if (off < kScanWindow) {
+            const uint64_t w = (c - c_first) * kScanWindow + off;  // exits of this range only
+            p = exits[w];
+            total += counts[w];
+        } else {
+            const uint64_t cend = min((c + 1) * chunk_bytes, n);
+            p = q;
+            while (p < cend && p != kTrunc) {
+                p = step(raw, n, p);
+                total++;
+            }
+        }
+        q = p;
+    }
+    state[0] = q;
+    state[1] = total;
+}
+
+// Offsets of the records starting in chunks [c_first, c_last); writes only
+// below cap (a log with more records than expected is reported by the caller).
+__global__ void k_scan_emit_range(const uint8_t* __restrict__ raw, uint64_t n, uint32_t c_first, uint32_t c_last,
+                                  uint64_t chunk_bytes, const uint64_t* __restrict__ start,
+                                  const uint64_t* __restrict__ base, uint64_t* __restrict__ offsets, uint64_t cap) {
+    const uint32_t c = c_first + blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c_last || start[c] == kTrunc) return;
+    const uint64_t cend = min((uint64_t)(c + 1) * chunk_bytes, n);
+    uint64_t p = start[c], k = base[c];
+    while (p < cend && k < cap) {
+        offsets[k++] = p;
+        p = step(raw, n, p);
+    }
+}
+
 }  // namespace
+
+void launch_log_scan_range(const uint8_t* d_raw, uint64_t n, uint32_t c_first, uint32_t c_last, uint64_t chunk_bytes,
+                           uint64_t* d_exit, uint32_t* d_count, uint64_t* d_start, uint64_t* d_base,
+                           unsigned long long* d_state, uint64_t* d_offsets, uint64_t cap, cudaStream_t s) {
+    if (c_last <= c_first) return;
+    k_scan_chunk<<<c_last - c_first, kScanThreads, 0, s>>>(d_raw, n, c_first, chunk_bytes, d_exit, d_count);
+    k_scan_stitch_inc<<<1, 1, 0, s>>>(d_raw, n, c_first, c_last, chunk_bytes, d_exit, d_count, d_start, d_base,
+                                      d_state);
+    k_scan_emit_range<<<(c_last - c_first + 127) / 128, 128, 0, s>>>(d_raw, n, c_first, c_last, chunk_bytes, d_start,
+                                                                     d_base, d_offsets, cap);
+}
 
 void launch_log_scan_a(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, uint64_t* d_exit, uint32_t* d_count,
                        cudaStream_t s) {
-    if (n_chunks) k_scan_chunk<<<n_chunks, kScanThreads, 0, s>>>(d_raw, n, d_exit, d_count);
+    if (n_chunks) k_scan_chunk<<<n_chunks, kScanThreads, 0, s>>>(d_raw, n, 0, kScanChunk, d_exit, d_count);
 }
 
 void launch_log_scan_b(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, const uint64_t* d_exit,

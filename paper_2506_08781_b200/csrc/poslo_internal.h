@@ -132,6 +132,15 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
 // Raw log image scan (log_scan.cu): chunk / window geometry and the three phases.
 constexpr uint64_t kScanChunk = 1ull << 20;
 constexpr uint32_t kScanWindow = 2048;
+// Pipelined ingestion: scan + incremental stitch + offsets for chunks
+// [c_first, c_last); d_state = {next record position, records so far}.
+// chunk_bytes: kScanChunk, or kRawScanChunk in the pipelined path (short
+// chunks: each emitting thread walks ~100 records, not ~2000). d_exit /
+// d_count hold the (c_last - c_first) x kScanWindow candidate exits of this range.
+constexpr uint64_t kRawScanChunk = 1ull << 16;
+void launch_log_scan_range(const uint8_t* d_raw, uint64_t n, uint32_t c_first, uint32_t c_last, uint64_t chunk_bytes,
+                           uint64_t* d_exit, uint32_t* d_count, uint64_t* d_start, uint64_t* d_base,
+                           unsigned long long* d_state, uint64_t* d_offsets, uint64_t cap, cudaStream_t s);
 void launch_log_scan_a(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, uint64_t* d_exit, uint32_t* d_count,
                        cudaStream_t s);
 void launch_log_scan_b(const uint8_t* d_raw, uint64_t n, uint32_t n_chunks, const uint64_t* d_exit,

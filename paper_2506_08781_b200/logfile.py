@@ -108,3 +108,38 @@ class RecordBatch:
         b.ds, b.ds_len, b.ds_capacity = ctypes.addressof(self._dsbuf), len(self.ds_bytes), self.ds.capacity
         b.device_resident, b.ds_offsets, b.record_header = 0, None, 4
         return b
+
+
+class ImageBatch:
+    """poslo_batch over a WHOLE raw record image with no offsets
+    (record_header = 4, offsets = NULL): the device finds the records itself
+    and, for a host image, copies it in 64 MiB chunks with the record scan and
+    the hashing of every completed epoch running behind the copy (read_log +
+    epochs_of + verification in one call; the record count must be
+    n_epochs x n2). `image`: bytes / uint8 array in host memory, or a device
+    pointer with device_resident=True (then `nbytes` is required)."""
+
+    def __init__(self, image, suite: int, n2: int, n_epochs: int, ds: api.SeedStack,
+                 device_resident: bool = False, nbytes: Optional[int] = None):
+        self.suite, self.n2, self.ds = suite, n2, ds
+        self.device_resident = device_resident
+        if device_resident:
+            self._ptr, self._len = int(image), int(nbytes)
+        else:
+            arr = np.frombuffer(image, dtype=np.uint8) if isinstance(image, (bytes, bytearray)) else image
+            self._keep = arr if len(arr) else np.zeros(1, np.uint8)
+            self._ptr, self._len = self._keep.ctypes.data, len(arr)
+        self.epochs = np.arange(n_epochs, dtype=np.uint32)
+        self.ds_bytes = ds.serialize()
+
+    def cstruct(self) -> N.PosloBatch:
+        b = N.PosloBatch()
+        b.suite, b.n2 = self.suite, self.n2
+        b.payload, b.payload_bytes = self._ptr, self._len
+        b.offsets, b.entry_len, b.n_entries = None, 0, len(self.epochs) * self.n2
+        b.epochs = self.epochs.ctypes.data if len(self.epochs) else None
+        b.epoch_starts, b.n_epochs = None, len(self.epochs)
+        self._dsbuf = ctypes.create_string_buffer(self.ds_bytes, len(self.ds_bytes))
+        b.ds, b.ds_len, b.ds_capacity = ctypes.addressof(self._dsbuf), len(self.ds_bytes), self.ds.capacity
+        b.device_resident, b.ds_offsets, b.record_header = int(self.device_resident), None, 4
+        return b

@@ -94,3 +94,57 @@ def test_device_scan_matches_host_scan(verifier):
             RecordLog(img[:cut], verifier, scanner="device")
         with pytest.raises(api.FormatError, match="truncated log record"):
             RecordLog(img[:cut], scanner="host")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", STREAMS)
+def test_image_batches_match_reference(verifier, name):
+    """A whole raw record image with no offsets (ImageBatch: record_header = 4,
+    the device finds the records): e~, e-hat and per-epoch verdicts equal the
+    reference's, from host memory and device-resident."""
+    import torch
+    from paper_2506_08781_b200.logfile import ImageBatch
+    st = Stream(load_golden(name + ".json"))
+    suite, pk, ds = st.api_objects()
+    img = _image([m for i in range(st.n1) for m in st.batches[i]])
+    s_hats = {i: st.sigs[i].s_hat_le for i in range(st.n1)}
+    dimg = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
+    for ib in (ImageBatch(img, st.suite, st.n2, st.n1, ds),
+               ImageBatch(dimg.data_ptr(), st.suite, st.n2, st.n1, ds, device_resident=True, nbytes=len(img))):
+        parts, e_hat = verifier.agg_ekeys_packed(ib)
+        assert [x[1] for x in parts] == st.e_tilde and e_hat == st.e_hat
+        verdicts = verifier.epoch_verify_packed(pk, ib, s_hats)
+        assert [int(v) for v in verdicts] == st.d["epoch_verdicts"]
+
+
+@pytest.mark.gpu
+def test_image_batch_pipelined_matches_offsets_path(verifier):
+    """An image of > 2 x 64 MiB takes the pipelined ingestion (chunked H2D, the
+    record scan and the hashing of completed epochs behind the copy): every
+    e~ equals the two-step path (device scan, then the record batch), and the
+    reference's errors come out of it: a truncated record (read_log), a count
+    that is not a multiple of n2 (epochs_of), a batch naming other epochs."""
+    import numpy as np
+    from paper_2506_08781_b200 import api
+    from paper_2506_08781_b200.logfile import ImageBatch, RecordLog
+    rng = np.random.default_rng(11)
+    n2, n1 = 512, 512
+    lens = rng.integers(300, 800, size=n1 * n2)
+    hdr = np.zeros(n1 * n2 + 1, dtype=np.int64)
+    np.cumsum(lens + 4, out=hdr[1:])
+    img = rng.integers(32, 127, size=int(hdr[-1]), dtype=np.uint8)
+    l32 = lens.astype(np.uint32).view(np.uint8).reshape(-1, 4)
+    for k in range(4):
+        img[hdr[:-1] + k] = l32[:, k]
+    assert len(img) > (2 << 26)
+    D = (n1 - 1).bit_length()
+    ds = api.SeedStack(D, [api.SeedNode(D, 0, bytes(range(16)))])
+    want, want_hat = verifier.agg_ekeys_log(RecordLog(img.tobytes(), verifier).batch(1, n2, ds))
+    got, got_hat = verifier.agg_ekeys_packed(ImageBatch(img, 1, n2, n1, ds))
+    assert got == want and got_hat == want_hat
+    with pytest.raises(api.FormatError, match="truncated log record"):
+        verifier.agg_ekeys_packed(ImageBatch(img[:-100], 1, n2, n1, ds))
+    with pytest.raises(api.FormatError, match="multiple of n2"):
+        verifier.agg_ekeys_packed(ImageBatch(img[:int(hdr[-2])], 1, n2, n1, ds))
+    with pytest.raises(ValueError, match="epochs"):
+        verifier.agg_ekeys_packed(ImageBatch(img[:int(hdr[n2 * (n1 - 1)])], 1, n2, n1, ds))
