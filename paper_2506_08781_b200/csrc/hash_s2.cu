@@ -76,20 +76,23 @@ void launch_hash_s2_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
                         uint32_t* d_partial, uint32_t* d_etilde, const uint32_t* d_t0, cudaStream_t s) {
     uint32_t n_tiles = tm.tile_count ? tm.tile_count : tm.n_epochs * tm.tiles_per_epoch;
     if (!n_tiles) return;
-    static int sms = 0, threads = 0;
-    if (!sms) {
-        int dev = 0;
+    struct Cfg {
+        int sms, threads;
+    };
+    static const Cfg cfg = [] {  // once per process (thread-safe static init)
+        int dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const char* e = std::getenv("POSLO_S2_THREADS");  // tuning knob: 256 / 384 / 512 / 768 / 1024
-        threads = e ? std::atoi(e) : 512;
         const size_t smem = kAes4DynBytes;
         cudaFuncSetAttribute(k_hash_s2_p<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_hash_s2_p<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_hash_s2_p<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_hash_s2_p<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_hash_s2_p<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+        return Cfg{sms, e ? std::atoi(e) : 512};
+    }();
+    const int sms = cfg.sms, threads = cfg.threads;
     const size_t smem = kAes4DynBytes;
     // one CTA per SM (128 KiB of tables), fewer when there are fewer tiles than warps
     const uint32_t warps_per_cta = (uint32_t)threads / 32;
