@@ -267,7 +267,10 @@ __device__ __forceinline__ gpt shfl_pt(const gpt& p, int off) {
     return r;
 }
 
-__global__ void __launch_bounds__(128) k_check_split(const gcached* __restrict__ tabY,
+#ifndef POSLO_CHECK_MINB
+#define POSLO_CHECK_MINB 1
+#endif
+__global__ void __launch_bounds__(128, POSLO_CHECK_MINB) k_check_split(const gcached* __restrict__ tabY,
                                                      const gcached* __restrict__ tabB, uint32_t n,
                                                      const uint32_t* __restrict__ e,
                                                      const uint32_t* __restrict__ s,
