@@ -64,6 +64,10 @@ struct poslo_gpu_ctx {
     bool tabY_valid = false;
     uint8_t tabY256_key[32] = {};
     bool tabY256_valid = false;
+    void* d_tabB16 = nullptr;  // radix-2^16 combs (60 MiB each) for large check batches
+    void* d_tabY16 = nullptr;
+    uint8_t tabY16_key[32] = {};
+    bool tabY16_valid = false;
     PinnedStage* stage = nullptr;
     bool timing = false;
     cudaEvent_t ev[7] = {};
@@ -640,7 +644,16 @@ int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void*
 
 // Comb tables of alpha (once per context) and of Y (cached per Y value).
 // Y validation (GroupElement::from_bytes) happens in the table build.
-int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false) {
+// Batches of at least POSLO_COMB16_MIN checks (default 2^17) use the
+// radix-2^16 combs: half the additions per check for a one-time build of
+// alpha's table per context and Y's per Y value (~10 ms each).
+uint32_t comb16_min() {
+    const char* e = std::getenv("POSLO_COMB16_MIN");
+    return e ? (uint32_t)std::strtoul(e, nullptr, 10) : (1u << 17);
+}
+
+int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false,
+                  bool xwide = false) {
     if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * kGptBytes));
     if (!ctx->d_tabB) {
         CU(cudaMalloc(&ctx->d_tabB, kCombTableBytes));
@@ -679,7 +692,32 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
             ctx->tabY256_valid = true;
         }
     }
+    if (xwide) {
+        if (!ctx->d_tabB16) {
+            CU(cudaMalloc(&ctx->d_tabB16, kComb16TableBytes));
+            launch_build_table65536(nullptr, ctx->d_pk, ctx->d_tabB16, d_flags, ctx->stream);
+            ctx->launches += 2;
+        }
+        if (!ctx->d_tabY16) CU(cudaMalloc(&ctx->d_tabY16, kComb16TableBytes));
+        if (!ctx->tabY16_valid || std::memcmp(ctx->tabY16_key, y, 32) != 0) {
+            uint8_t* d_y;
+            UPLOAD(b_y, y, 32, d_y);  // Y already validated by the radix-16 build above
+            launch_build_table65536(d_y, ctx->d_pk, ctx->d_tabY16, d_flags, ctx->stream);
+            ctx->launches += 2;
+            std::memcpy(ctx->tabY16_key, y, 32);
+            ctx->tabY16_valid = true;
+        }
+    }
     return POSLO_OK;
+}
+
+// The batched 8-lane checks on the widest tables ensure_tables built.
+void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
+                   const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st) {
+    if (xwide)
+        launch_check_split16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
+    else
+        launch_check_split(ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
 }
 
 // Batched group check on device arrays; verdicts/encodings to host.
@@ -788,7 +826,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
     if (ctx->stage) cudaFreeHost(ctx->stage);
-    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_tabB256, ctx->d_tabY256, ctx->d_pk})
+    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_tabB256, ctx->d_tabY256, ctx->d_tabB16, ctx->d_tabY16, ctx->d_pk})
         if (p) cudaFree(p);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
@@ -1018,7 +1056,7 @@ static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void
 static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const void* d_pts,
                         const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err) {
     CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
-    launch_check_split(ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_pts, d_ok, d_verdict, ctx->stream);
+    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_pts, d_ok, d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     return POSLO_OK;
@@ -1064,7 +1102,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         int* d_flags;
         ENSURE(b_flags, 4, d_flags);
         CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
-        rc = ensure_tables(ctx, y, d_flags, err, true);
+        rc = ensure_tables(ctx, y, d_flags, err, true, n >= comb16_min());
         if (rc) return rc;
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
@@ -1079,7 +1117,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
             CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));  // side: after the decode, then this piece
-            launch_check_split(ctx->d_tabY256, ctx->d_tabB256, e1 - e0, P.d_etilde + 8 * (size_t)e0,
+            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0,
                                d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
                                d_ok + e0, d_vpipe + e0, ctx->side);
             ctx->launches += 1;
@@ -1201,7 +1239,7 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
     int* d_flags;
     ENSURE(b_flags, 4, d_flags);
     CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
-    int rc = ensure_tables(ctx, y, d_flags, err, split);
+    int rc = ensure_tables(ctx, y, d_flags, err, split, split && n >= comb16_min());
     if (rc) return rc;
     if (n) {
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
@@ -1220,7 +1258,7 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
             CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
-            launch_check_split(ctx->d_tabY256, ctx->d_tabB256, e1 - e0, P.d_etilde + 8 * (size_t)e0,
+            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0,
                                d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
                                d_ok + e0, d_verdict + e0, ctx->side);
             ctx->launches += 1;

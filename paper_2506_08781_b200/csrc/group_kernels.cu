@@ -146,6 +146,23 @@ __global__ void k_table_fill256(const gpt* __restrict__ pk, gcached* __restrict_
     tab[t] = pt_to_cached(q);
 }
 
+// Radix-2^16 fill: thread t = 32768 k + (m - 1) writes m 2^(16k) P for
+// m = 1 .. 32768 (signed digits |d| <= 2^15), by double-and-add on the bits
+// of m (<= 16 doublings + 16 additions) and one inversion to affine Niels.
+__global__ void k_table_fill65536(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 16u * 32768u) return;
+    const uint32_t k = t >> 15, m = (t & 32767u) + 1;
+    const gpt base = pk[k];
+    gpt q = pt_identity();
+#pragma unroll 1
+    for (int b = 15; b >= 0; b--) {
+        q = pt_dbl(q);
+        if ((m >> b) & 1) q = pt_add(q, base);
+    }
+    tab[t] = pt_to_cached(q);
+}
+
 __global__ void k_table_fill(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 512) return;
@@ -328,6 +345,60 @@ __global__ void __launch_bounds__(128, POSLO_CHECK_MINB) k_check_split(const gca
     if (live && sub == 0) verdict[i] = (rok[i] && rist_equal(acc, R[i])) ? 1 : 0;
 }
 
+// k_check_split on radix-2^16 combs (16 windows per scalar, 32768 affine
+// Niels points per window: 60 MiB per base in HBM): each lane adds 2 windows
+// of e and 2 of s, half the additions of the radix-256 form, for batches
+// large enough to amortise the table builds (and Y's, cached per Y).
+__global__ void __launch_bounds__(128) k_check_split16(const gcached* __restrict__ tabY,
+                                                       const gcached* __restrict__ tabB, uint32_t n,
+                                                       const uint32_t* __restrict__ e,
+                                                       const uint32_t* __restrict__ s,
+                                                       const gpt* __restrict__ R,
+                                                       const uint8_t* __restrict__ rok,
+                                                       uint8_t* __restrict__ verdict) {
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = gid >> 3, sub = gid & 7;
+    const bool live = i < n;
+    const uint32_t ic = live ? i : 0;
+    uint32_t ve[8], vs[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        ve[k] = e[(size_t)ic * 8 + k];
+        vs[k] = s[(size_t)ic * 8 + k];
+    }
+    // signed radix-2^16 digits (scalars < 2^253: the top digit never carries out);
+    // this lane keeps digits 2 sub and 2 sub + 1 of each
+    int de[2] = {0, 0}, dsg[2] = {0, 0};
+    int ce = 0, cs = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const int a = (int)((ve[k >> 1] >> (16 * (k & 1))) & 0xffffu) + ce;
+        ce = (a + 32768) >> 16;
+        const int b = (int)((vs[k >> 1] >> (16 * (k & 1))) & 0xffffu) + cs;
+        cs = (b + 32768) >> 16;
+        if ((uint32_t)(k >> 1) == sub) {
+            de[k & 1] = a - (ce << 16);
+            dsg[k & 1] = b - (cs << 16);
+        }
+    }
+    gpt acc = pt_identity();
+#pragma unroll 1
+    for (int t = 0; t < 4; t++) {
+        const int q = t >> 1;
+        const int dig = (t & 1) ? dsg[q] : de[q];
+        if (!dig) continue;
+        const int a = dig < 0 ? -dig : dig;
+        const gcached c = ((t & 1) ? tabB : tabY)[32768 * (2 * (int)sub + q) + a - 1];
+        acc = pt_add_cached(acc, dig < 0 ? cached_neg(c) : c);
+    }
+#pragma unroll 1
+    for (int off = 4; off >= 1; off >>= 1) {
+        const gpt o = shfl_pt(acc, off);
+        if (sub < (uint32_t)off) acc = pt_add(acc, o);
+    }
+    if (live && sub == 0) verdict[i] = (rok[i] && rist_equal(acc, R[i])) ? 1 : 0;
+}
+
 // Masked segmented fold over already-decoded points (distillation after the
 // split checks: R-hat is decoded once for both).
 __global__ void __launch_bounds__(128) k_segfold_gpt(const gpt* __restrict__ pts,
@@ -464,6 +535,16 @@ void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n
         static_cast<const gpt*>(d_pts), d_ok, d_verdict);
 }
 
+void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                          const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                          cudaStream_t s) {
+    if (!n) return;
+    const uint64_t threads = (uint64_t)n * 8;
+    k_check_split16<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
+        static_cast<const gcached*>(d_tabY16), static_cast<const gcached*>(d_tabB16), n, d_e, d_s,
+        static_cast<const gpt*>(d_pts), d_ok, d_verdict);
+}
+
 void launch_segfold_decoded(const void* d_pts, const uint32_t* d_seg, uint32_t n_seg, const uint8_t* d_mask,
                             uint8_t* d_out, cudaStream_t s) {
     if (!n_seg) return;
@@ -501,6 +582,12 @@ void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table,
                         cudaStream_t s) {
     k_table_pow<4><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
     k_table_fill<<<4, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
+}
+
+void launch_build_table65536(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s) {
+    k_table_pow<16><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
+    k_table_fill65536<<<16 * 32768 / 128, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch),
+                                                       static_cast<gcached*>(d_table));
 }
 
 void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s) {

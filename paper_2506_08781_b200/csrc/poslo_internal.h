@@ -124,6 +124,7 @@ constexpr size_t kCachedBytes = 3 * kFeBytes;       // affine Niels point (y+x, 
 constexpr size_t kGptBytes = 4 * kFeBytes;          // extended point (X, Y, Z, T)
 constexpr size_t kCombTableBytes = 512 * kCachedBytes;      // radix 16: 64 x 8 affine Niels points
 constexpr size_t kComb256TableBytes = 4096 * kCachedBytes;  // radix 256: 32 x 128 points
+constexpr size_t kComb16TableBytes = (size_t)16 * 32768 * kCachedBytes;  // radix 2^16: 16 x 32768 points (60 MiB)
 constexpr uint32_t kCtaCheckMax = 1024;          // larger batches use one thread per check (radix-256 combs)
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s);
@@ -157,6 +158,11 @@ void launch_segfold_points(const uint8_t* d_pts, const uint32_t* d_seg, uint32_t
 // lanes per check on the radix-256 combs; segfold_decoded folds decoded points.
 constexpr size_t kPointBytes = kGptBytes;
 void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s);
+// Radix-2^16 tables (kComb16TableBytes) and the 8-lane check on them.
+void launch_build_table65536(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s);
+void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                          const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                          cudaStream_t s);
 void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n, const uint32_t* d_e,
                         const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
                         cudaStream_t s);

@@ -457,12 +457,16 @@ def test_chunked_varlen_host_path_matches_device_resident(verifier):
     assert a == h
 
 
+@pytest.mark.parametrize("comb16", [False, True])
 @pytest.mark.parametrize("resident", [0, 1])
-def test_batched_epoch_checks_large(verifier, resident):
+def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
     """> 1024 per-epoch checks take the split path (R-hat decoded on a side
     stream, 8 lanes per check; device-resident batches also pipeline the
     checks behind the hashing): signatures from the reference derivation
-    (signer.py) verify, and exactly the tampered epochs fail."""
+    (signer.py) verify, and exactly the tampered epochs fail — on the
+    radix-256 combs and (comb16, POSLO_COMB16_MIN = 1) on the radix-2^16
+    combs large batches take by default."""
+    monkeypatch.setenv("POSLO_COMB16_MIN", "1" if comb16 else "4294967295")
     import ctypes
 
     import torch
