@@ -117,33 +117,45 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:  # NVML set up BEFORE the timed region, so even a short region gets samples
+            import pynvml as nv
+            nv.nvmlInit()
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._nv = nv
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv = self._nv
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append([str(sm), str(self._mx), ""] + ["Active" if r & bt else "Not Active" for bt in bits])
+
+    def _sample_smi(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            if out:
+                self.samples.append([x.strip() for x in out.split(",")])
+        except Exception:
+            pass
 
     def _run(self):
         # NVML samples every 5 ms (a 10-step timed region is ~130 ms); nvidia-smi if NVML is absent
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append([str(sm), str(mx), ""] + ["Active" if r & bt else "Not Active" for bt in bits])
-                self._stop.wait(0.005)
-            return
-        except Exception:
-            pass
         while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+            if self._nv is not None:
+                try:
+                    self._sample_nvml()
+                except Exception:
+                    self._nv = None
+                self._stop.wait(0.005)
+            else:
+                self._sample_smi()
+                self._stop.wait(0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -153,6 +165,14 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one sampling period: one sample at its end
+            if self._nv is not None:
+                try:
+                    self._sample_nvml()
+                except Exception:
+                    pass
+            if not self.samples:
+                self._sample_smi()
 
     def summary(self):
         if not self.samples:
