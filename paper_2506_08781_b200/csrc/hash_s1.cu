@@ -223,6 +223,10 @@ static void launch_tiled(uint32_t n_tiles, const uint4* pay, const TileMap& tm, 
                                                   tm.tile_begin, pipek_host());
 }
 
+#ifndef POSLO_S1_FMA
+#define POSLO_S1_FMA 2  // pipe assignment of the lean kernel's SHA rounds (sha256.cuh SHA_RND_SEL)
+#endif
+
 void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,
                         uint32_t* d_partial, uint32_t* d_etilde, cudaStream_t s) {
     uint32_t n_tiles = tm.tile_count ? tm.tile_count : tm.n_epochs * tm.tiles_per_epoch;
@@ -233,9 +237,9 @@ void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
         const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;
         const PipeK pk = pipek_host();
         if (tm.n2 <= 128)
-            k_hash_s1_l32r<256, 8, 2, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
+            k_hash_s1_l32r<256, 8, POSLO_S1_FMA, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         else
-            k_hash_s1_l32r<256, 4, 2, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
+            k_hash_s1_l32r<256, 4, POSLO_S1_FMA, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         return;
     }
     if (tm.tile_entries == 256 * 4)
