@@ -289,10 +289,11 @@ def int_peak(device):
     lib.poslo_microbench_int_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(ctypes.c_double)]
     res = {}
-    for mode, name in ((0, "alu"), (1, "fma"), (2, "dual"), (10, "lds")):
-        v, ms = ctypes.c_double(), ctypes.c_double()
-        if lib.poslo_microbench_int_peak(device, mode, ctypes.byref(v), ctypes.byref(ms)) == 0:
-            res[name] = v.value
+    for _ in range(3):  # best of three: the first pass can run before the clocks settle
+        for mode, name in ((0, "alu"), (1, "fma"), (2, "dual"), (10, "lds")):
+            v, ms = ctypes.c_double(), ctypes.c_double()
+            if lib.poslo_microbench_int_peak(device, mode, ctypes.byref(v), ctypes.byref(ms)) == 0:
+                res[name] = max(res.get(name, 0.0), v.value)
     return res
 
 
