@@ -516,6 +516,7 @@ def main():
     # ---- timed region (device-resident inputs)
     v.enable_timing(True)
     hash_ms = []
+    stage_ms = []
     launches = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -525,7 +526,9 @@ def main():
         ev0.record(stream)
         for _ in range(a.steps):
             ok = step(bdev)
-            hash_ms.append(v.last_timings()["hash"])
+            st_ = v.last_timings()
+            hash_ms.append(st_["hash"])
+            stage_ms.append(st_)
             launches += v.last_launches()
         ev1.record(stream)
         ev1.synchronize()
@@ -736,6 +739,11 @@ def main():
                 "alu_pipe": {"peak": round(peaks["alu"] / 1e12, 2), "unit": "Tops/s",
                              "note": "co-bound: PRMT byte picks, rotations and XORs of the rounds"},
                 "share_of_step": round(hash_avg_ms / ms_per_step, 4)}
+
+    if roof is not None and stage_ms:
+        # device stage times of a step (C-ABI events on its stream): seed (K0), hash (K1+K2, with
+        # the pipelined per-epoch checks when they overlap it), finalize, sum, group (K3), total
+        roof["stages_ms"] = {k: round(statistics.mean(x[k] for x in stage_ms), 4) for k in stage_ms[0]}
 
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "entries/s", "n_gpus": world, "steps": a.steps,
