@@ -248,6 +248,21 @@ bool is_uniform(const poslo_batch* b) {
     return true;
 }
 
+// A device_resident batch must hand the kernels memory they can read:
+// device or managed memory, or registered (pinned, mapped) host memory.
+// Plain pageable host memory would fault inside a kernel and leave the
+// context unusable, so it is rejected up front.
+bool device_readable(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free error of the query
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ||
+           (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr);
+}
+
 // After the whole raw image is scanned: read_log's FormatError on a
 // truncated record, epochs_of's on a count that is not a nonzero multiple of
 // n2 (tools/poslo.cpp:32-40), and the batch must name exactly that many
@@ -329,6 +344,8 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         return b->offsets ? b->offsets[(uint64_t)e * b->n2] : (uint64_t)e * epoch_bytes;
     };
     if (b->device_resident) {
+        if ((b->payload_bytes && !device_readable(b->payload)) || !device_readable(b->offsets))
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "device_resident batch with a host pointer");
         P.lay.payload = b->payload;
         P.lay.offsets = b->offsets;
     } else {
@@ -888,6 +905,8 @@ int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int
     Guard g(ctx);
     cudaStream_t s = ctx->stream;
     const uint8_t* d_raw = raw;
+    if (device_resident && ((len && !device_readable(raw)) || !device_readable(offsets)))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "device_resident image with a host pointer");
     if (!device_resident && len) {
         uint8_t* d;
         ENSURE(b_payload, len, d);
@@ -1067,6 +1086,8 @@ static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, con
 static int sig_arrays(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t* s_hats, const uint8_t* r_hats,
                       const uint32_t** d_s_out, const uint8_t** d_r_out, poslo_error* err) {
     if (b->device_resident) {
+        if (b->n_epochs && (!device_readable(s_hats) || !device_readable(r_hats)))
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "device_resident batch with host signature arrays");
         *d_s_out = reinterpret_cast<const uint32_t*>(s_hats);
         *d_r_out = r_hats;
         return POSLO_OK;
@@ -1351,6 +1372,8 @@ static int fine_scalars_dev(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint
     EntryLayout lay{};
     lay.entry_len = fb->entry_len;
     if (fb->device_resident) {
+        if ((fb->payload_bytes && !device_readable(fb->payload)) || !device_readable(fb->offsets))
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "device_resident batch with a host pointer");
         lay.payload = fb->payload;
         lay.offsets = fb->offsets;
     } else {

@@ -508,3 +508,44 @@ def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
                        ctypes.c_void_p(r_dev.data_ptr()), verd, None)
         got = [bool(x) for x in verd.raw]
     assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
+
+
+def test_device_resident_host_pointers_rejected(verifier):
+    """A batch flagged device_resident that points at pageable host memory
+    (payload, or the per-epoch signature arrays) is refused with
+    INVALID_ARGUMENT instead of faulting in a kernel; the context keeps
+    working afterwards."""
+    import ctypes
+
+    import torch
+    from paper_2506_08781_b200 import _native as N
+    api = A()
+    cfg, batches, ds = _synthetic(1, 8, 64, 32, seed=3)
+    flat = b"".join(m for i in range(8) for m in batches[i])
+    host = np.frombuffer(flat, dtype=np.uint8).copy()
+    dsb = ds.serialize()
+    dsbuf = ctypes.create_string_buffer(dsb, len(dsb))
+    epochs = np.arange(8, dtype=np.uint32)
+
+    def batch(ptr):
+        b = N.PosloBatch()
+        b.suite, b.n2, b.payload, b.payload_bytes = 1, 64, ptr, len(flat)
+        b.offsets, b.entry_len, b.n_entries = None, 32, 8 * 64
+        b.epochs, b.epoch_starts, b.n_epochs = epochs.ctypes.data, None, 8
+        b.ds, b.ds_len, b.ds_capacity, b.device_resident = ctypes.addressof(dsbuf), len(dsb), ds.capacity, 1
+        return b
+
+    et, eh = ctypes.create_string_buffer(8 * 32), ctypes.create_string_buffer(32)
+    with pytest.raises(ValueError, match="host pointer"):
+        verifier._call(verifier._lib.poslo_gpu_agg_ekeys, ctypes.byref(batch(host.ctypes.data)), et, eh)
+    dev = torch.frombuffer(bytearray(flat), dtype=torch.uint8).cuda()
+    bd = batch(dev.data_ptr())
+    Y = verifier.exp_base((5).to_bytes(32, "little"))
+    s = ctypes.create_string_buffer(8 * 32)
+    r = ctypes.create_string_buffer(b"".join([Y] * 8), 8 * 32)
+    verd = ctypes.create_string_buffer(8)
+    with pytest.raises(ValueError, match="host signature arrays"):
+        verifier._call(verifier._lib.poslo_gpu_epoch_verify, ctypes.byref(bd), Y, s, r, verd, None)
+    verifier._call(verifier._lib.poslo_gpu_agg_ekeys, ctypes.byref(bd), et, eh)  # still healthy
+    parts, _ = verifier.agg_ekeys(cfg, batches, ds, 1)
+    assert [p[1] for p in parts] == [et.raw[32 * k:32 * k + 32] for k in range(8)]
