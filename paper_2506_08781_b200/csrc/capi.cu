@@ -75,6 +75,13 @@ struct poslo_gpu_ctx {
     uint32_t launches = 0;
 };
 
+extern "C" {  // defined with the batched-check entry points below
+static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
+                        poslo_error* err);
+static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
+                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err);
+}
+
 namespace {
 
 constexpr uint64_t kChunkBytes = 64ull << 20;
@@ -728,10 +735,14 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
     return POSLO_OK;
 }
 
-// The batched 8-lane checks on the widest tables ensure_tables built.
+// The batched checks on the widest tables ensure_tables built: with decoded
+// R-hat (d_pts, d_ok), 8 lanes per check (radix 256 or 2^16); without, one
+// thread per check on the radix-2^16 combs comparing encodings (d_r).
 void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
-                   const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st) {
-    if (xwide)
+                   const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st) {
+    if (xwide && !d_pts)
+        launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, nullptr, d_verdict, st);
+    else if (xwide)
         launch_check_split16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
     else
         launch_check_split(ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
@@ -746,12 +757,16 @@ int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const u
     uint8_t* d_enc = nullptr;
     ENSURE(b_flags, 4, d_flags);
     CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
-    int rc = ensure_tables(ctx, y, d_flags, err, n > kCtaCheckMax);
+    const bool xwide = n > kCtaCheckMax && n >= comb16_min();  // radix-2^16 combs, thread per check
+    int rc = ensure_tables(ctx, y, d_flags, err, n > kCtaCheckMax, xwide);
     if (rc) return rc;
     if (h_verdict) ENSURE(b_verdict, n, d_verdict);
     if (h_enc) ENSURE(b_enc, (size_t)n * 32, d_enc);
-    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_r, d_enc,
-                            d_verdict, ctx->stream);
+    if (xwide)
+        launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, d_enc, d_verdict, ctx->stream);
+    else
+        launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_r, d_enc,
+                                d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     int ybad = 0;
@@ -762,6 +777,7 @@ int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const u
     if (ybad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
     return POSLO_OK;
 }
+
 
 // LE 32-byte scalar -> 8 limbs (identical memory image on little-endian hosts).
 bool scalar_canonical(const uint8_t* s) {
@@ -1072,10 +1088,10 @@ static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void
     return POSLO_OK;
 }
 
-static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const void* d_pts,
-                        const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err) {
-    CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
-    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_pts, d_ok, d_verdict, ctx->stream);
+static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
+                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err) {
+    if (d_pts) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode
+    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_r, d_pts, d_ok, d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     return POSLO_OK;
@@ -1127,8 +1143,10 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         if (rc) return rc;
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
-        rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
-        if (rc) return rc;
+        if (n < comb16_min()) {  // radix 256: 8-lane checks against R-hat decoded here
+            rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
+            if (rc) return rc;
+        }  // radix 2^16: thread per check, encode compare (cheaper than decode + 8 lanes)
     }
     Prepared P;
     uint8_t* d_vpipe = nullptr;
@@ -1138,9 +1156,10 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
             CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));  // side: after the decode, then this piece
-            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0,
-                               d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
-                               d_ok + e0, d_vpipe + e0, ctx->side);
+            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
+                          d_r + 32 * (size_t)e0,
+                          d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
+                          d_ok ? d_ok + e0 : nullptr, d_vpipe + e0, ctx->side);
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1170,7 +1189,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     } else if (split) {
         uint8_t* d_verdict;
         ENSURE(b_verdict, n, d_verdict);
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
         if (rc) return rc;
         CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -1279,9 +1298,10 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
             CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
-            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0,
-                               d_s + 8 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
-                               d_ok + e0, d_verdict + e0, ctx->side);
+            launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
+                          d_r + 32 * (size_t)e0,
+                          d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
+                          d_ok ? d_ok + e0 : nullptr, d_verdict + e0, ctx->side);
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1300,7 +1320,7 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
     } else if (split) {
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
         if (rc) return rc;
     } else {
         launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s,

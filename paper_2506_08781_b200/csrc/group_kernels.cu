@@ -223,6 +223,38 @@ __global__ void __launch_bounds__(128) k_check_cta(const gcached* __restrict__ t
 
 // One thread per check (throughput mode, e.g. 2^20 per-epoch checks), on
 // the radix-256 combs: 64 mixed additions + one encode per check.
+// Thread per check on the radix-2^16 combs: 32 mixed additions + the encode
+// compare (for batches of >= POSLO_COMB16_MIN checks).
+__global__ void __launch_bounds__(128) k_check_thread16(const gcached* __restrict__ tabY,
+                                                        const gcached* __restrict__ tabB, uint32_t n,
+                                                        const uint32_t* __restrict__ e,
+                                                        const uint32_t* __restrict__ s,
+                                                        const uint8_t* __restrict__ r,
+                                                        uint8_t* __restrict__ enc,
+                                                        uint8_t* __restrict__ verdict) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t v[8];
+    gpt acc = pt_identity();
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = e[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabY, v);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = s[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabB, v);
+    uint8_t out[32];
+    rist_encode(acc, out);
+    if (enc)
+#pragma unroll
+        for (int k = 0; k < 32; k++) enc[(size_t)i * 32 + k] = out[k];
+    if (r && verdict) {
+        uint32_t diff = 0;
+#pragma unroll
+        for (int k = 0; k < 32; k++) diff |= out[k] ^ r[(size_t)i * 32 + k];
+        verdict[i] = diff == 0;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict__ tabY,
                                                       const gcached* __restrict__ tabB, uint32_t n,
                                                       const uint32_t* __restrict__ e,
@@ -533,6 +565,15 @@ void launch_check_split(const void* d_tabY256, const void* d_tabB256, uint32_t n
     k_check_split<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
         static_cast<const gcached*>(d_tabY256), static_cast<const gcached*>(d_tabB256), n, d_e, d_s,
         static_cast<const gpt*>(d_pts), d_ok, d_verdict);
+}
+
+void launch_check_thread16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                           const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
+                           cudaStream_t s) {
+    if (!n) return;
+    k_check_thread16<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
+                                                     static_cast<const gcached*>(d_tabB16), n, d_e, d_s, d_r, d_enc,
+                                                     d_verdict);
 }
 
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,

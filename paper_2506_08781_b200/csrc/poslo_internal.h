@@ -160,6 +160,9 @@ constexpr size_t kPointBytes = kGptBytes;
 void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s);
 // Radix-2^16 tables (kComb16TableBytes) and the 8-lane check on them.
 void launch_build_table65536(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s);
+void launch_check_thread16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                           const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
+                           cudaStream_t s);
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
                           const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
                           cudaStream_t s);

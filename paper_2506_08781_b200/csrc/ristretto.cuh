@@ -531,6 +531,23 @@ PHD gpt comb256_mul_add(gpt acc, const gcached* tab, const uint32_t s[8]) {
     return acc;
 }
 
+// acc + s * P on a radix-2^16 comb of P (16 windows x 32768 affine Niels
+// points): signed 16-bit digits, 16 mixed additions. s < 2^253, so the top
+// digit never carries out.
+PHD gpt comb65536_mul_add(gpt acc, const gcached* tab, const uint32_t s[8]) {
+    int carry = 0;
+    for (int k = 0; k < 16; k++) {
+        const int a = (int)((s[k >> 1] >> (16 * (k & 1))) & 0xffffu) + carry;
+        carry = (a + 32768) >> 16;
+        const int dig = a - (carry << 16);
+        if (!dig) continue;
+        const int m = dig < 0 ? -dig : dig;
+        const gcached c = tab[32768 * k + m - 1];
+        acc = pt_add_cached(acc, dig < 0 ? cached_neg(c) : c);
+    }
+    return acc;
+}
+
 // Ristretto equality of classes (RFC 9496 §4.3.3): X1*Y2 == Y1*X2 or
 // Y1*Y2 == X1*X2. Equal classes <=> equal canonical encodings, so comparing
 // against a decoded R replaces encoding P (the reference's byte compare).

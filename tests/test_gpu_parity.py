@@ -119,16 +119,21 @@ def test_commit_check_batched(verifier, kat):
         assert g == R.commit_check(Y, e, s)
 
 
-def test_commit_check_radix256_path(verifier, kat):
-    """n > 1024 checks run thread-per-check on the radix-256 combs; they must
-    agree with the CTA path (radix-16 combs, n <= 1024) and the oracle,
-    including edge scalars (0, 1, l - 1, digits that carry)."""
+@pytest.mark.parametrize("comb16", [False, True])
+def test_commit_check_radix256_path(verifier, kat, comb16, monkeypatch):
+    """n > 1024 checks run thread-per-check on the radix-256 combs (or, with
+    POSLO_COMB16_MIN = 1, on the radix-2^16 combs large batches take by
+    default); they must agree with the CTA path (radix-16 combs, n <= 1024)
+    and the oracle, including edge scalars (0, 1, l - 1, digits that carry,
+    2^16-digit boundaries)."""
     import random
+    monkeypatch.setenv("POSLO_COMB16_MIN", "1" if comb16 else "4294967295")
     from oracle import ristretto as R
     rng = random.Random(256)
     Y = bytes.fromhex(kat["commit_check"][5][0])
     L = R.L if hasattr(R, "L") else 2**252 + 27742317777372353535851937790883648493
-    edge = [0, 1, 2, 127, 128, 255, 256, 0x80 * 0x0101010101, L - 1, L - 128, 2**252]
+    edge = [0, 1, 2, 127, 128, 255, 256, 0x80 * 0x0101010101, L - 1, L - 128, 2**252,
+            32767, 32768, 32769, 65535, 65536, 0x8000 * (1 + 2**16 + 2**32 + 2**48), 2**240 - 1]
     vals = edge + [rng.randrange(L) for _ in range(1100 - len(edge))]
     es = [v.to_bytes(32, "little") for v in vals]
     ss = [rng.randrange(L).to_bytes(32, "little") for _ in vals]
