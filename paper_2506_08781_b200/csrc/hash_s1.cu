@@ -4,6 +4,10 @@
 #include "entry_hash.cuh"
 #include "tile_common.cuh"
 
+#ifndef POSLO_OTS_SPEC
+#define POSLO_OTS_SPEC 1  // onetime_seed-specialised schedule in the lean kernel (12.15 vs 12.34 ms)
+#endif
+
 namespace poslo_gpu {
 
 namespace {
@@ -85,6 +89,9 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
     static_assert(T == kLeanStride, "accumulator column stride");
     constexpr int TPE = T / EPC;  // threads per epoch (multiple of 32)
     __shared__ uint32_t s_pre[EPC][8], s_x0w[EPC][4];
+#if POSLO_OTS_SPEC
+    __shared__ OtsEpoch s_ots[EPC];
+#endif
     __shared__ uint32_t s_acc[18 * T];  // rows 0..8: sum of H1 words, rows 9..17: sum of H0 words
     __shared__ uint32_t red[(T / 32) * 17];
     const uint32_t le = threadIdx.x / TPE, lt = threadIdx.x % TPE;
@@ -99,6 +106,9 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
         for (int k = 0; k < 8; k++) s_pre[le][k] = pre[k];
 #pragma unroll
         for (int k = 0; k < 4; k++) s_x0w[le][k] = x0w[k];
+#if POSLO_OTS_SPEC
+        s_ots[le] = ots_epoch_consts(x0w);
+#endif
     }
     uint32_t* acc = s_acc + threadIdx.x;
 #pragma unroll
@@ -145,7 +155,21 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
                     }
                     sha256_init(st);
                 }
+#if POSLO_OTS_SPEC
+                // onetime_seed: rounds 4-31 on the per-epoch-constant schedule, the
+                // 16-round loop (rounds 32-63, or 16-63 for the entry hashes) shared
+                int blk0 = 16;
+                if (c == 0) {
+                    ots_head_rounds<FMA>(st, W, j, s_ots[le], pk);
+                    blk0 = 32;
+                } else {
+                    sha256_rounds_head<FMA>(st, W, 0, pk);
+                }
+                sha256_rounds_loop<FMA>(st, W, blk0, pk);
+                (void)r0;
+#else
                 sha256_rounds_compact<FMA>(st, W, r0, pk);
+#endif
                 const uint32_t iv[8] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3, SHA_IV4, SHA_IV5, SHA_IV6, SHA_IV7};
                 if (c == 0) {
 #pragma unroll
@@ -223,6 +247,9 @@ static void launch_tiled(uint32_t n_tiles, const uint4* pay, const TileMap& tm, 
                                                   tm.tile_begin, pipek_host());
 }
 
+#ifndef POSLO_S1_MINB
+#define POSLO_S1_MINB 4  // __launch_bounds__ min CTAs/SM of the lean kernel (48 regs: 5 fit anyway)
+#endif
 #ifndef POSLO_S1_FMA
 #define POSLO_S1_FMA 2  // pipe assignment of the lean kernel's SHA rounds (sha256.cuh SHA_RND_SEL)
 #endif
@@ -237,9 +264,9 @@ void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
         const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;
         const PipeK pk = pipek_host();
         if (tm.n2 <= 128)
-            k_hash_s1_l32r<256, 8, POSLO_S1_FMA, 4><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
+            k_hash_s1_l32r<256, 8, POSLO_S1_FMA, POSLO_S1_MINB><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         else
-            k_hash_s1_l32r<256, 4, POSLO_S1_FMA, 4><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
+            k_hash_s1_l32r<256, 4, POSLO_S1_FMA, POSLO_S1_MINB><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         return;
     }
     if (tm.tile_entries == 256 * 4)
