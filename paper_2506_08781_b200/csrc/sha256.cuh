@@ -504,6 +504,40 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const Pip
     sha256_rounds_loop<FMA>(st, W, 16, pk);
 }
 
+// ---- entry-hash specialisation: one-block messages with W13 = W14 = 0 --------
+// Both entry hashes of a 32-byte entry (m || x: W12 = 0x80000000, W15 = 384;
+// 0x01 || m || x: W12 varies, W15 = 392) have W13 = W14 = 0 and a constant
+// W15, so sigma1(W14), sigma0(W13), sigma0(W14) vanish and sigma1(W15),
+// sigma0(W15) are constants (s1w15, s0w15) in W16..W31. Runs rounds 0..31
+// and leaves W = W16..W31 for sha256_rounds_loop(.., 32, ..).
+template <int FMA = 2>
+PHD void entry_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t s1w15, uint32_t s0w15, const PipeK& pk) {
+    const uint32_t one = pk.one;
+    (void)one;
+    sha256_rounds_head<FMA>(st, W, 0, pk);
+    const uint32_t w0 = W[0], w1 = W[1], w2 = W[2], w3 = W[3], w4 = W[4], w5 = W[5], w6 = W[6], w7 = W[7];
+    const uint32_t w8 = W[8], w9 = W[9], w10 = W[10], w11 = W[11], w12 = W[12], w15 = W[15];
+    W[0] = fadd(sha_s0(w1), fadd(w9, w0, one), one);                                   // W16
+    W[1] = fadd(sha_s0(w2), fadd(w10, fadd(w1, s1w15, one), one), one);              // W17
+    W[2] = fadd(sha_s1(W[0]), fadd(sha_s0(w3), fadd(w11, w2, one), one), one);       // W18
+    W[3] = fadd(sha_s1(W[1]), fadd(sha_s0(w4), fadd(w12, w3, one), one), one);       // W19
+    W[4] = fadd(sha_s1(W[2]), fadd(sha_s0(w5), w4, one), one);                       // W20 (W13 = 0)
+    W[5] = fadd(sha_s1(W[3]), fadd(sha_s0(w6), w5, one), one);                       // W21 (W14 = 0)
+    W[6] = fadd(sha_s1(W[4]), fadd(sha_s0(w7), fadd(w15, w6, one), one), one);       // W22
+    W[7] = fadd(sha_s1(W[5]), fadd(sha_s0(w8), fadd(W[0], w7, one), one), one);      // W23
+    W[8] = fadd(sha_s1(W[6]), fadd(sha_s0(w9), fadd(W[1], w8, one), one), one);      // W24
+    W[9] = fadd(sha_s1(W[7]), fadd(sha_s0(w10), fadd(W[2], w9, one), one), one);     // W25
+    W[10] = fadd(sha_s1(W[8]), fadd(sha_s0(w11), fadd(W[3], w10, one), one), one);   // W26
+    W[11] = fadd(sha_s1(W[9]), fadd(sha_s0(w12), fadd(W[4], w11, one), one), one);   // W27
+    W[12] = fadd(sha_s1(W[10]), fadd(W[5], w12, one), one);                          // W28 (sigma0(W13) = 0)
+    W[13] = fadd(sha_s1(W[11]), W[6], one);                                          // W29 (W13 = W14 = 0)
+    W[14] = fadd(sha_s1(W[12]), fadd(W[7], s0w15, one), one);                        // W30 (W14 = 0)
+    W[15] = fadd(sha_s1(W[13]), fadd(sha_s0(W[0]), fadd(W[8], w15, one), one), one); // W31
+    uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+    SHA_16_ROUNDS(sha_k, 16);
+    st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
+}
+
 // ---- onetime_seed specialisation: F(x0 || be32 j) for all j of an epoch ----
 // The message is x0 (4 words, per epoch), W4 = j and the constants
 // W5 = 0x80000000, W6..W14 = 0, W15 = 160. Hence W16..W18 are per-epoch
