@@ -148,3 +148,33 @@ def test_image_batch_pipelined_matches_offsets_path(verifier):
         verifier.agg_ekeys_packed(ImageBatch(img[:int(hdr[-2])], 1, n2, n1, ds))
     with pytest.raises(ValueError, match="epochs"):
         verifier.agg_ekeys_packed(ImageBatch(img[:int(hdr[n2 * (n1 - 1)])], 1, n2, n1, ds))
+
+
+@pytest.mark.gpu
+def test_image_batch_pipelined_huge_records(verifier):
+    """Pipelined ingestion with records spanning several 64 MiB copy chunks
+    (a 70 MB and a 66 MB record among small ones), empty records and a
+    record ending exactly on a chunk boundary: e~ equal the two-step path."""
+    import numpy as np
+    from paper_2506_08781_b200 import api
+    from paper_2506_08781_b200.logfile import ImageBatch, RecordLog
+    rng = np.random.default_rng(3)
+    lens = [int(x) for x in rng.integers(0, 900, 100)] + [70_000_000] + [0, 0, 5] + \
+           [int(x) for x in rng.integers(1, 300, 20)] + [66_000_000] + [17, 0, 1]
+    n2 = 32
+    assert len(lens) % n2 == 0
+    # make record 50 end exactly at the first 64 MiB boundary: pad the one before it
+    pos = sum(4 + L for L in lens[:50])
+    lens[49] += (1 << 26) - (pos + 4 + lens[50]) if pos + 4 + lens[50] < (1 << 26) else 0
+    img = bytearray()
+    for L in lens:
+        img += L.to_bytes(4, "little")
+        img += rng.integers(32, 127, L, dtype=np.uint8).tobytes()
+    img = bytes(img)
+    assert len(img) > (2 << 26)
+    n1 = len(lens) // n2
+    D = max(1, (n1 - 1).bit_length())
+    ds = api.SeedStack(D, [api.SeedNode(D, 0, bytes(range(16)))])
+    want = verifier.agg_ekeys_log(RecordLog(img, verifier).batch(1, n2, ds))
+    got = verifier.agg_ekeys_packed(ImageBatch(img, 1, n2, n1, ds))
+    assert got == want
