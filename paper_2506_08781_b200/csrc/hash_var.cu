@@ -13,6 +13,10 @@
 #include "entry_hash.cuh"
 #include "tile_common.cuh"
 
+#ifndef POSLO_VAR_FMA
+#define POSLO_VAR_FMA 2  // pipe assignment of the SHA rounds (sha256.cuh SHA_RND_SEL)
+#endif
+
 namespace poslo_gpu {
 
 namespace {
@@ -104,7 +108,7 @@ __device__ __forceinline__ void compress_into(uint32_t H[8], uint32_t W[16], con
     uint32_t st[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) st[i] = H[i];
-    sha256_rounds_compact<2>(st, W, 0, pk);
+    sha256_rounds_compact<POSLO_VAR_FMA>(st, W, 0, pk);
 #pragma unroll
     for (int i = 0; i < 8; i++) H[i] += st[i];
 }
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileM
                     for (int k = 0; k < 8; k++) st[k] = 0;
                 }
             }
-            if (active) sha256_rounds_compact<2>(st, W, r0, pk);
+            if (active) sha256_rounds_compact<POSLO_VAR_FMA>(st, W, r0, pk);
             if (job == 0) {  // x kept in the slot tail (bytes in stream order) for the suffix writes
                 const uint32_t iv[4] = {SHA_IV0, SHA_IV1, SHA_IV2, SHA_IV3};
 #pragma unroll
