@@ -257,6 +257,9 @@ static void launch_tiled(uint32_t n_tiles, const uint4* pay, const TileMap& tm, 
                                                   tm.tile_begin, pipek_host());
 }
 
+#ifndef POSLO_LEAN_EPC8_MAX
+#define POSLO_LEAN_EPC8_MAX 256  // largest n2 run 8 epochs per 256-thread CTA (else 4)
+#endif
 #ifndef POSLO_S1_MINB
 #define POSLO_S1_MINB 4  // __launch_bounds__ min CTAs/SM of the lean kernel (48 regs: 5 fit anyway)
 #endif
@@ -273,7 +276,11 @@ void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* 
         // whole epochs per CTA (tile == epoch): register-lean kernel, raw epoch sums
         const uint32_t e0 = tm.tile_begin, ne = e0 + n_tiles;
         const PipeK pk = pipek_host();
-        if (tm.n2 <= 128)
+        // 8 epochs per CTA (a warp per epoch) up to n2 = POSLO_LEAN_EPC8_MAX: the
+        // per-epoch prologue amortised over more entries per thread (config 2,
+        // n2 = 256: 12.04 vs 12.10 ms); 4 epochs per CTA above (config 3,
+        // n2 = 1024: equal within noise)
+        if (tm.n2 <= POSLO_LEAN_EPC8_MAX)
             k_hash_s1_l32r<256, 8, POSLO_S1_FMA, POSLO_S1_MINB><<<(n_tiles + 7) / 8, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
         else
             k_hash_s1_l32r<256, 4, POSLO_S1_FMA, POSLO_S1_MINB><<<(n_tiles + 3) / 4, 256, 0, s>>>(pay, tm.n2, ne, e0, d_x0, d_partial, pk);
