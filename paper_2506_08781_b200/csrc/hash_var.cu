@@ -13,6 +13,9 @@
 #include "entry_hash.cuh"
 #include "tile_common.cuh"
 
+#ifndef POSLO_VAR_MINB
+#define POSLO_VAR_MINB 6  // min CTAs/SM of k_hash_s1_var (register cap 65536 / (128 x MINB))
+#endif
 #ifndef POSLO_VAR_FMA
 #define POSLO_VAR_FMA 2  // pipe assignment of the SHA rounds (sha256.cuh SHA_RND_SEL)
 #endif
@@ -133,7 +136,7 @@ PD void smem_acc9_add8v(uint32_t* s, int stride, const uint32_t v[8]) {
     for (int k = 0; k < 9; k++) s[k * stride] = a[k];
 }
 
-__global__ void __launch_bounds__(kVarT, 6) k_hash_s1_var(EntryLayout lay, TileMap tm,
+__global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayout lay, TileMap tm,
                                                           const uint4* __restrict__ x0,
                                                           uint32_t* __restrict__ partial, const PipeK pk) {
     __shared__ uint32_t red[(kVarT / 32) * 17];
