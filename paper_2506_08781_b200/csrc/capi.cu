@@ -1285,7 +1285,11 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
     }
-    if (split) {  // R-hat decoded once, on the side stream during hashing, for the checks AND the fold
+    // R-hat decoded once, on the side stream during hashing, for the fold (and
+    // the 8-lane radix-256 checks); radix-2^16 batches check thread per check
+    // (encode compare), cheaper than 8 lanes on the decoded point
+    const bool xw = split && n >= comb16_min();
+    if (split) {
         rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
         if (rc) return rc;
     }
@@ -1300,8 +1304,8 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
                           d_r + 32 * (size_t)e0,
-                          d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
-                          d_ok ? d_ok + e0 : nullptr, d_verdict + e0, ctx->side);
+                          !xw ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
+                          !xw ? d_ok + e0 : nullptr, d_verdict + e0, ctx->side);
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1320,7 +1324,7 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
     } else if (split) {
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, xw ? nullptr : d_pts, d_ok, d_verdict, err);
         if (rc) return rc;
     } else {
         launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s,
@@ -1339,6 +1343,7 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
             uint8_t* d_out;
             UPLOAD(b_seg32, seg, (size_t)(n_seg + 1) * 4, d_seg);
             ENSURE(b_out_r, (size_t)n_seg * 32, d_out);
+            CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode (side stream)
             launch_segfold_decoded(d_pts, d_seg, n_seg, d_verdict, d_out, ctx->stream);
             ctx->launches += 1;
             CU(cudaMemcpyAsync(seg_r, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, ctx->stream));
