@@ -555,6 +555,14 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             }
             cut.push_back(e1);
         }
+        // the hashing of the last chunk is the exposed tail behind the copy:
+        // land it as four quarter chunks (fixed-length logs; a variable-length
+        // tail is bounded by the latency of one 1024-entry tile instead)
+        if (!b->offsets && cut.size() >= 3 && cut.back() - cut[cut.size() - 2] >= 8) {
+            const uint32_t a = cut[cut.size() - 2], z = cut.back();
+            cut.pop_back();
+            for (uint32_t q = 1; q <= 4; q++) cut.push_back(a + (uint32_t)((uint64_t)(z - a) * q / 4));
+        }
         const uint32_t n_chunks = (uint32_t)cut.size() - 1;
         while (ctx->chunk_ev.size() < n_chunks + 1) {
             cudaEvent_t ev;
