@@ -1,4 +1,5 @@
-"""Parity at BASELINE sizes (SURVEY §8d "sampled"): the device verifies the
+"""Parity at BASELINE sizes: config 1 in full (2^20 x 32 B,
+every epoch against the oracle); "sampled" above it: the device verifies the
 full synthetic log of config 2 (2^26 x 32 B, n2 = 256), a per-epoch config-3
 slice (2^24 x 32 B, n2 = 1024), a config-4 slice (2^20 syslog entries) and a
 config-5 slice (tamper localisation over 2^22 signed entries);
@@ -74,6 +75,12 @@ def _run(verifier, log2n, n2, varlen, samples, seed):
     rc, _, ref = O.agg_ekeys_packed(1, b"".join(flat), o, 0, pick, starts, dsb, D)
     assert rc == 0
     assert [raw[32 * i:32 * i + 32] for i in pick] == ref
+
+
+def test_config1_full_parity(verifier):
+    """Config 1 (2^20 x 32 B, n2 = 256, the reference's CPU-runnable case):
+    EVERY epoch's e~ (all 4096) against the oracle, not a sample."""
+    _run(verifier, 20, 256, False, 4096, 11)
 
 
 def test_config2_full_size_sampled_parity(verifier):
