@@ -93,6 +93,17 @@ typedef struct poslo_batch {
                                       FormatError "truncated log record" (read_log), "record count
                                       must be a nonzero multiple of n2" (epochs_of), then
                                       INVALID_ARGUMENT when the count names other epochs. */
+    /* Optional host producer of the entry bytes, for callers whose entries are not
+     * contiguous in memory (the reference's std::map<u32, vector<Bytes>>): with
+     * payload == NULL and device_resident == 0, the library calls
+     * fill(fill_user, first, count, dst) to write entries [first, first + count)
+     * back to back into dst (pinned staging of up to 64 MiB for fixed-length
+     * entries: whole epochs per call, ascending, from the calling thread), and copies
+     * and hashes each chunk while the next one is being produced. payload_bytes
+     * (and offsets, for variable lengths) still describe the packed layout. A
+     * nonzero return aborts the call with POSLO_INVALID_ARGUMENT. */
+    int (*fill)(void* fill_user, uint64_t first, uint64_t count, uint8_t* dst);
+    void* fill_user;
 } poslo_batch;
 
 /* Scheme F (POSLO-F, include/poslo/poslo_f.hpp) entries: each entry t has a
@@ -138,6 +149,22 @@ int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int
 
 /* ---- context -------------------------------------------------------------- */
 int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err);
+/* Multi-device context (SURVEY §8b "select GPU count", §8e): one member
+ * context per entry of `devices` (a device may repeat: members then share
+ * it, which exercises the sharded path on one GPU). agg_ekeys, paver,
+ * epoch_verify and distill_coarse shard the queried epochs into contiguous
+ * ranges balanced by entry bytes, one range per member, run the members
+ * concurrently (one host thread and stream per member) and combine on member
+ * 0: e-hat partials folded mod l in member order, R-hat partials with the
+ * group law, per-epoch outputs concatenated, umbrella pieces that a shard cut
+ * splits folded back together — byte-identical to the single-device result.
+ * Device-resident batches run on the member owning the memory; raw images
+ * without offsets and every other call run on member 0. */
+int poslo_gpu_create_multi(const int* devices, int n_devices, poslo_gpu_ctx** out, poslo_error* err);
+/* Members of a context (1 for a single-device context). */
+int poslo_gpu_member_count(const poslo_gpu_ctx* ctx);
+/* Visible CUDA devices (0 without a driver / device). */
+int poslo_gpu_device_count(void);
 void poslo_gpu_destroy(poslo_gpu_ctx* ctx);
 /* Run subsequent work on this cudaStream_t (NULL = the context's own stream,
  * a blocking stream: ordered after work on the legacy default stream). */
@@ -168,6 +195,31 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t 
                     const uint8_t s_hat[32], const uint8_t* r_hat_agg, const uint8_t* r_hats,
                     uint8_t* verdict, poslo_error* err);
 
+/* ---- multi-rank coarse PAVer (one process per GPU) ---------------
+ * agg_ekeys_partial: e-hat of this shard (sum of its e~ mod l) written to
+ * d_e_part, a 32-byte DEVICE pointer on the context's device, in stream order
+ * on the context's stream (so a collective queued on the same stream after
+ * the call gathers it without a host round trip). Errors as agg_ekeys.
+ * combine_check: e-hat = sum of the n_parts partials mod l (in the given =
+ * rank order), *verdict = (commit_check(Y, e-hat, s-hat) == r_hat) — the
+ * fold and final check of paver (batch_verify.cpp:83-86). parts_on_device:
+ * e_parts is a device pointer (e.g. the output of an all-gather). */
+int poslo_gpu_agg_ekeys_partial(poslo_gpu_ctx* ctx, const poslo_batch* batch, uint8_t* d_e_part, poslo_error* err);
+int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t* e_parts, int32_t parts_on_device,
+                            const uint8_t y[32], const uint8_t s_hat[32], const uint8_t r_hat[32], uint8_t* verdict,
+                            poslo_error* err);
+
+/* ---- group operation counters (group.hpp:86-97 GroupOpCounts) ------------------
+ * Process-wide counts of the group operations the device performed, in the
+ * reference's units: double_exp = commit_check evaluations (one per checked
+ * group: 1 per coarse paver, n per per-epoch batch), exp_base = fixed-base
+ * exponentiations (kg commitments), exp_var = 0 (never used on the path),
+ * combine = group_combine folds of caller-supplied points (one per folded
+ * element, as the reference's fold from the identity counts them). Relaxed
+ * atomics; out = {exp_base, exp_var, double_exp, combine}. */
+void poslo_gpu_group_op_counts(uint64_t out[4]);
+void poslo_gpu_reset_group_op_counts(void);
+
 /* ---- per-epoch verification (distill_epoch verdicts, distiller.cpp:60-89) ---
  * verdicts[k] = (commit_check(Y, e~_k, s_hats[k]) == r_hats[k]) for every
  * queried epoch; e_tilde_out optional (n_epochs x 32 B). When the batch is
@@ -178,7 +230,11 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* batch, const u
                            uint8_t* e_tilde_out, poslo_error* err);
 
 /* ---- SeBVer (distiller.cpp:156-233) over a coarse CCD --------------------------
- * The batch holds epochs 0..n_epochs-1 (all distilled epochs, n2 each).
+ * The batch holds the epochs SeBVer hashes (verify_range / the mode-I lookup
+ * read no others), any ascending subset of the distilled epochs, n2 each;
+ * seeds are derived only for them. A group's e-sum runs over the batch
+ * epochs in its range that are not in the invalid list; an I record's epoch
+ * must be in the batch (else FormatError "messages for invalid epoch missing").
  * invalid: n_invalid ascending epoch indices (CCD invalid list).
  * Mode V: v_s/v_r = CCD valid aggregate -> *v_bit.
  * Mode U: n_umb umbrella records (index u, s, r; width w = n1/n_u) -> u_bits.
@@ -207,6 +263,14 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* batch, const
                              const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg,
                              uint32_t n_seg, uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r,
                              poslo_error* err);
+/* The same with one more per-segment output (NULL to skip): seg_e[g] = sum of
+ * e~ mod l over the segment's VALID epochs — the e-sum SeBVer mode U checks
+ * against the umbrella record (distiller.cpp:156-179), so a sharded caller can
+ * fold umbrella pieces of e, s and R-hat across shards without rehashing. */
+int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                                const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg,
+                                uint32_t n_seg, uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r,
+                                uint8_t* seg_e, poslo_error* err);
 
 /* Masked segmented folds on the device: for g < n_seg, over items k in
  * [seg[g], seg[g+1]) with mask[k] != 0 (mask NULL = all): out_s[g] = sum of

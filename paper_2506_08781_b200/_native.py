@@ -37,7 +37,13 @@ class PosloBatch(ctypes.Structure):
         ("device_resident", ctypes.c_int32),
         ("ds_offsets", ctypes.c_void_p),
         ("record_header", ctypes.c_uint32),
+        ("fill", ctypes.c_void_p),       # int (*)(void*, uint64_t, uint64_t, uint8_t*) or NULL
+        ("fill_user", ctypes.c_void_p),
     ]
+
+
+# poslo_batch.fill: int fill(void* user, uint64_t first, uint64_t count, uint8_t* dst)
+FILL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p)
 
 
 class PosloFineBatch(ctypes.Structure):
@@ -69,7 +75,9 @@ EXPORTS = [
     "poslo_gpu_entry_scalars", "poslo_gpu_group_check", "poslo_gpu_scalar_sum", "poslo_gpu_synth_log",
     "poslo_gpu_synth_varlog", "poslo_gpu_distill_coarse", "poslo_gpu_segfold", "poslo_gpu_fine_scalars",
     "poslo_gpu_fine_verify", "poslo_gpu_aver_f_batch", "poslo_log_scan", "poslo_gpu_kg_commitments",
-    "poslo_gpu_sig_epochs", "poslo_gpu_log_scan",
+    "poslo_gpu_sig_epochs", "poslo_gpu_log_scan", "poslo_gpu_create_multi", "poslo_gpu_member_count",
+    "poslo_gpu_device_count", "poslo_gpu_agg_ekeys_partial", "poslo_gpu_combine_check",
+    "poslo_gpu_group_op_counts", "poslo_gpu_reset_group_op_counts", "poslo_gpu_distill_coarse_ex",
 ]
 
 _lib = None
@@ -122,6 +130,14 @@ def load():
         "poslo_gpu_kg_commitments": ([P, c.c_uint8, P, P, c.c_uint32, c.c_uint32, P, P, E], c.c_int),
         "poslo_gpu_sig_epochs": ([P, B, P, P, P, E], c.c_int),
         "poslo_gpu_log_scan": ([P, P, c.c_uint64, c.c_int32, P, c.c_uint64, c.POINTER(c.c_uint64), E], c.c_int),
+        "poslo_gpu_create_multi": ([c.POINTER(c.c_int), c.c_int, c.POINTER(c.c_void_p), E], c.c_int),
+        "poslo_gpu_member_count": ([P], c.c_int),
+        "poslo_gpu_device_count": ([], c.c_int),
+        "poslo_gpu_agg_ekeys_partial": ([P, B, P, E], c.c_int),
+        "poslo_gpu_combine_check": ([P, c.c_uint32, P, c.c_int32, P, P, P, P, E], c.c_int),
+        "poslo_gpu_group_op_counts": ([c.POINTER(c.c_uint64)], None),
+        "poslo_gpu_reset_group_op_counts": ([], None),
+        "poslo_gpu_distill_coarse_ex": ([P, B, P, P, P, P, c.c_uint32, P, P, P, P, E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

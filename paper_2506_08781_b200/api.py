@@ -286,16 +286,31 @@ def _buf(b: Optional[bytes]):
 
 # ---------------------------------------------------------------- verifier
 class Verifier:
-    """One device context (re-entrant; calls on one context serialise)."""
+    """One device context (re-entrant; calls on one context serialise).
 
-    def __init__(self, device: int = 0):
+    devices: several device indices -> a multi-device context
+    (poslo_gpu_create_multi): agg_ekeys / paver / epoch_verify / distillation
+    shard their epochs over the members and combine on the first; a device may
+    repeat (members sharing one GPU)."""
+
+    def __init__(self, device: int = 0, devices: Optional[Sequence[int]] = None):
         self._lib = N.load()
         self._ctx = ctypes.c_void_p()
         err = N.PosloError()
-        rc = self._lib.poslo_gpu_create(device, ctypes.byref(self._ctx), ctypes.byref(err))
+        if devices is not None and len(devices) > 1:
+            arr = (ctypes.c_int * len(devices))(*devices)
+            rc = self._lib.poslo_gpu_create_multi(arr, len(devices), ctypes.byref(self._ctx), ctypes.byref(err))
+            device = devices[0]
+        else:
+            if devices:
+                device = devices[0]
+            rc = self._lib.poslo_gpu_create(device, ctypes.byref(self._ctx), ctypes.byref(err))
         if rc:
             _raise(rc, err)
         self.device = device
+
+    def members(self) -> int:
+        return int(self._lib.poslo_gpu_member_count(self._ctx))
 
     def close(self):
         if self._ctx:
@@ -327,6 +342,31 @@ class Verifier:
 
     def last_launches(self) -> int:
         return int(self._lib.poslo_gpu_last_launches(self._ctx))
+
+    # -- group operation counters (group.hpp:86-97), process-wide
+    def group_op_counts(self) -> Dict[str, int]:
+        arr = (ctypes.c_uint64 * 4)()
+        self._lib.poslo_gpu_group_op_counts(arr)
+        return dict(zip(["exp_base", "exp_var", "double_exp", "combine"], [int(x) for x in arr]))
+
+    def reset_group_op_counts(self):
+        self._lib.poslo_gpu_reset_group_op_counts()
+
+    # -- multi-rank coarse PAVer: partial e-hat into device memory, rank-ordered fold + check
+    def agg_ekeys_partial(self, cb: "N.PosloBatch", d_out: int):
+        """e-hat of this shard's batch (a filled N.PosloBatch) into 32 bytes of device memory."""
+        self._call(self._lib.poslo_gpu_agg_ekeys_partial, ctypes.byref(cb), ctypes.c_void_p(d_out))
+
+    def combine_check(self, parts, y: bytes, s_hat: bytes, r_hat: bytes, n_parts: Optional[int] = None) -> bool:
+        """parts: bytes (host, n x 32) or an int device pointer (then n_parts is required)."""
+        v = ctypes.c_uint8(0)
+        if isinstance(parts, int):
+            self._call(self._lib.poslo_gpu_combine_check, n_parts, ctypes.c_void_p(parts), 1, _buf(y), _buf(s_hat),
+                       _buf(r_hat), ctypes.byref(v))
+        else:
+            self._call(self._lib.poslo_gpu_combine_check, len(parts) // 32, _buf(parts), 0, _buf(y), _buf(s_hat),
+                       _buf(r_hat), ctypes.byref(v))
+        return bool(v.value)
 
     # -- agg_ekeys / aggregate_ekey (batch_verify.cpp:11-62, poslo_c.cpp:177-190)
     def agg_ekeys(self, suite: SuiteConfig, batches: Dict[int, Sequence[bytes]], ds: SeedStack,
@@ -431,10 +471,11 @@ class Verifier:
 
     # -- batched coarse distillation (distiller.cpp:60-89): verdicts + masked umbrella folds
     def distill_coarse(self, pk: PoslocPublicKey, batches, sigs: Dict[int, "EpochSignature"],
-                       seg: Sequence[int]):
+                       seg: Sequence[int], want_e: bool = False):
         """Epochs of `batches` (consecutive, n2 entries each) verified against
         their own signatures (s_hat, pk.r_hats[i], sig.ds). seg: batch-position
-        boundaries (len n_seg + 1). Returns (verdicts, [(s_le, r)] per segment)."""
+        boundaries (len n_seg + 1). Returns (verdicts, [(s_le, r)] per segment),
+        with want_e (verdicts, [(s_le, r, e_le)]): e = sum of the segment's valid e~."""
         ds_any = next(iter(sigs.values())).ds if sigs else SeedStack(pk.suite.depth())
         pb = PackedBatch(pk.suite.suite, pk.suite.n2, batches, ds_any,
                          epoch_ds={i: sigs[i].ds for i in batches})
@@ -446,10 +487,15 @@ class Verifier:
         verd = ctypes.create_string_buffer(max(len(eps), 1))
         out_s = ctypes.create_string_buffer(max(ng, 1) * 32)
         out_r = ctypes.create_string_buffer(max(ng, 1) * 32)
+        out_e = ctypes.create_string_buffer(max(ng, 1) * 32)
         cb = pb.cstruct()
-        self._call(self._lib.poslo_gpu_distill_coarse, ctypes.byref(cb), _buf(pk.y), _buf(s) if s else None,
-                   _buf(r) if r else None, segs.ctypes.data if ng else None, ng, verd, out_s, out_r)
-        vr, sr_, rr = verd.raw, out_s.raw, out_r.raw
+        self._call(self._lib.poslo_gpu_distill_coarse_ex, ctypes.byref(cb), _buf(pk.y), _buf(s) if s else None,
+                   _buf(r) if r else None, segs.ctypes.data if ng else None, ng, verd, out_s, out_r,
+                   out_e if want_e else None)
+        vr, sr_, rr, er = verd.raw, out_s.raw, out_r.raw, out_e.raw
+        if want_e:
+            return ([bool(vr[k]) for k in range(len(eps))],
+                    [(sr_[32 * g:32 * g + 32], rr[32 * g:32 * g + 32], er[32 * g:32 * g + 32]) for g in range(ng)])
         return ([bool(vr[k]) for k in range(len(eps))],
                 [(sr_[32 * g:32 * g + 32], rr[32 * g:32 * g + 32]) for g in range(ng)])
 
@@ -470,10 +516,12 @@ class Verifier:
 
     # -- SeBVer over a coarse CCD (distiller.cpp:181-233)
     def sebver(self, y: bytes, suite: SuiteConfig, all_msgs, ds: SeedStack, epochs_distilled: int,
-               invalid: Sequence, umbrellas: Sequence, valid=None):
+               invalid: Sequence, umbrellas: Sequence, valid=None, hashed: Optional[Sequence[int]] = None):
         """invalid: [(epoch, s_le, r)], umbrellas: [(u, s_le, r)], valid: (s_le, r) or None.
-        Returns dict with keys V (list, only when valid given), U, I."""
-        batches = {i: all_msgs[i] for i in range(epochs_distilled)}
+        hashed: the epochs to hash (default: every distilled epoch); the C-ABI derives
+        seeds and hashes only those. Returns dict with keys V (list, only when valid given), U, I."""
+        eps = range(epochs_distilled) if hashed is None else hashed
+        batches = {i: all_msgs[i] for i in eps}
         pb = PackedBatch(suite.suite, suite.n2, batches, ds)
         cb = pb.cstruct()
         inv = np.array([x[0] for x in invalid], dtype=np.uint32)

@@ -24,56 +24,7 @@
 
 using namespace poslo_gpu;
 
-namespace {
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-};
-
-}  // namespace
-
-struct PinnedStage {  // pinned host landing zone for the per-call small D2H copies
-    unsigned long long err_key;
-    unsigned long long err_init;  // H2D: error word seeded with host-detected seed failures
-    int flags[4];
-    uint8_t verdict;
-    unsigned long long scan[3];  // raw-image scan state {next record, records so far} + sentinel
-};
-
-struct poslo_gpu_ctx {
-    int device = 0;
-    cudaStream_t own = nullptr;
-    cudaStream_t stream = nullptr;
-    cudaStream_t copy = nullptr;  // H2D of host-resident logs, overlapped with hashing
-    cudaStream_t side = nullptr;  // e-hat-independent part of the group check, overlapped with hashing
-    cudaEvent_t ev_side[2] = {};
-    std::vector<cudaEvent_t> chunk_ev;
-    std::mutex mtx;
-    uint32_t* d_t0 = nullptr;
-    DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
-        b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state;
-    // fixed-base comb tables: generator (built once) and the last Y seen
-    void* d_tabB = nullptr;
-    void* d_tabY = nullptr;
-    void* d_tabB256 = nullptr;  // radix-256 combs for batched checks (built on first use)
-    void* d_tabY256 = nullptr;
-    void* d_pk = nullptr;
-    uint8_t tabY_key[32] = {};
-    bool tabY_valid = false;
-    uint8_t tabY256_key[32] = {};
-    bool tabY256_valid = false;
-    void* d_tabB16 = nullptr;  // radix-2^16 combs (60 MiB each) for large check batches
-    void* d_tabY16 = nullptr;
-    uint8_t tabY16_key[32] = {};
-    bool tabY16_valid = false;
-    PinnedStage* stage = nullptr;
-    bool timing = false;
-    cudaEvent_t ev[7] = {};
-    float last_ms[6] = {};
-    uint32_t launches = 0;
-};
+#include "capi_ctx.h"
 
 extern "C" {  // defined with the batched-check entry points below
 static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
@@ -108,6 +59,8 @@ int set_err(poslo_error* err, int code, uint32_t epoch, const char* fmt, ...) {
     }
     return code;
 }
+
+std::atomic<uint64_t> g_ops[4];  // poslo_gpu_group_op_counts
 
 int ok(poslo_error* err) {
     if (err) {
@@ -321,8 +274,26 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "epoch_starts[0] must be 0");
     if (n_entries > b->n_entries && !raw_image)
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "batch describes more entries than given");
-    if (n_entries && !b->payload && !(b->offsets == nullptr && b->entry_len == 0))
+    // a producer callback stands in for a host payload (poslo_batch.fill)
+    const bool has_fill = b->fill && !b->payload && !b->device_resident;
+    if (has_fill && raw_image)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "a fill producer needs entry offsets or a fixed length");
+    if (n_entries && !b->payload && !has_fill && !(b->offsets == nullptr && b->entry_len == 0))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null payload");
+    // layout bounds: the kernels read payload[offsets[t] + header .. offsets[t+1]) or
+    // payload[t L .. (t+1) L); a batch whose layout leaves the payload is refused
+    // before any copy or kernel touches it (host offsets: the ends here and the
+    // monotonicity on the device below; device offsets: all on the device)
+    if (!raw_image && !b->offsets && n_entries && (uint64_t)b->entry_len * n_entries > b->payload_bytes)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "n_entries x entry_len exceeds payload_bytes");
+    uint64_t off_lo = 0, off_hi = b->payload_bytes;  // byte span of the described entries
+    if (!b->offsets && !raw_image) off_hi = (uint64_t)b->entry_len * n_entries;
+    if (b->offsets && !b->device_resident) {
+        off_lo = b->offsets[0];
+        off_hi = b->offsets[n_entries];
+        if (off_lo > off_hi || off_hi > b->payload_bytes)
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "entry offsets outside the payload");
+    }
 
     cudaStream_t s = ctx->stream;
     uint32_t n_ep = b->n_epochs;
@@ -345,7 +316,7 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     // Host-resident uniform logs (fixed length, or byte offsets / raw record
     // images) stream in epoch-aligned chunks of <= 64 MiB on the copy stream.
     const bool chunked = !raw_image && !b->device_resident && P.uniform && (b->offsets || epoch_bytes > 0) &&
-                         b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
+                         ((b->payload_bytes >= 2 * kChunkBytes && n_ep > 1) || (has_fill && n_ep > 0));
     const bool raw_chunked = raw_image && !b->device_resident && b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
     auto epoch_byte = [&](uint32_t e) -> uint64_t {  // first payload byte of the e-th queried epoch
         return b->offsets ? b->offsets[(uint64_t)e * b->n2] : (uint64_t)e * epoch_bytes;
@@ -356,18 +327,59 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         P.lay.payload = b->payload;
         P.lay.offsets = b->offsets;
     } else {
+        // only the described entries' bytes travel: [off_lo, off_hi) lands at
+        // d_pay, and the kernels index it through the shifted base d_pay - off_lo
+        // with the caller's absolute offsets (a sub-range of a larger log, e.g.
+        // one shard of a multi-device call, copies only its own bytes)
         uint8_t* d_pay;
-        ENSURE(b_payload, b->payload_bytes, d_pay);
-        if (b->payload_bytes && !chunked && !raw_chunked)
-            CU(cudaMemcpyAsync(d_pay, b->payload, b->payload_bytes, cudaMemcpyHostToDevice, s));
-        P.lay.payload = d_pay;
+        const uint64_t span = off_hi - off_lo;
+        ENSURE(b_payload, span, d_pay);
+        if (span && !chunked && !raw_chunked) {
+            if (has_fill) {
+                const size_t need = (size_t)span;
+                if (!ctx->fill_slot[0] || ctx->fill_cap < need) {
+                    CU(cudaStreamSynchronize(s));
+                    CU(cudaStreamSynchronize(ctx->copy));
+                    for (auto& p : ctx->fill_slot)
+                        if (p) {
+                            cudaFreeHost(p);
+                            p = nullptr;
+                        }
+                    ctx->fill_cap = 0;
+                    for (auto& p : ctx->fill_slot) CU(cudaMallocHost(&p, need));
+                    ctx->fill_cap = need;
+                }
+                CU(cudaEventSynchronize(ctx->fill_ev[0]));
+                if (b->fill(b->fill_user, 0, n_entries, ctx->fill_slot[0]) != 0)
+                    return set_err(err, POSLO_INVALID_ARGUMENT, 0, "fill producer failed");
+                CU(cudaMemcpyAsync(d_pay, ctx->fill_slot[0], span, cudaMemcpyHostToDevice, s));
+                CU(cudaEventRecord(ctx->fill_ev[0], s));
+            } else {
+                CU(cudaMemcpyAsync(d_pay, b->payload + off_lo, span, cudaMemcpyHostToDevice, s));
+            }
+        }
+        P.lay.payload = d_pay - off_lo;
         P.lay.offsets = nullptr;
         if (b->offsets) {
             uint64_t* d_off;
-            ENSURE(b_offsets, b->n_entries + 1, d_off);
-            CU(cudaMemcpyAsync(d_off, b->offsets, (b->n_entries + 1) * 8, cudaMemcpyHostToDevice, s));
+            ENSURE(b_offsets, n_entries + 1, d_off);
+            CU(cudaMemcpyAsync(d_off, b->offsets, (n_entries + 1) * 8, cudaMemcpyHostToDevice, s));
             P.lay.offsets = d_off;
         }
+    }
+    // offsets must be non-decreasing with room for each record header and stay
+    // inside [off_lo, off_hi] (device-resident: inside the payload), checked on
+    // the device before the first hashing kernel reads through them
+    if (P.lay.offsets && !raw_image && n_entries) {
+        int* d_bad;
+        ENSURE(b_flags, 4, d_bad);
+        CU(cudaMemsetAsync(d_bad, 0, 16, s));
+        launch_check_offsets(P.lay.offsets, n_entries, b->record_header, off_lo, off_hi, d_bad, s);
+        ctx->launches += 1;
+        CU(cudaMemcpyAsync(ctx->stage->flags, d_bad, 4, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (ctx->stage->flags[0])
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "entry offsets not ascending or outside the payload");
     }
 
     // raw image: record offsets found on the device
@@ -569,6 +581,23 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             ctx->chunk_ev.push_back(ev);
         }
+        if (has_fill) {  // pinned ring for the producer: kFillSlots chunks in flight
+            size_t need = 0;
+            for (uint32_t c = 0; c < n_chunks; c++)
+                need = std::max<size_t>(need, epoch_byte(cut[c + 1]) - epoch_byte(cut[c]));
+            if (!ctx->fill_slot[0] || ctx->fill_cap < need) {
+                CU(cudaStreamSynchronize(s));
+                CU(cudaStreamSynchronize(ctx->copy));
+                for (auto& p : ctx->fill_slot)
+                    if (p) {
+                        cudaFreeHost(p);
+                        p = nullptr;
+                    }
+                ctx->fill_cap = 0;
+                for (auto& p : ctx->fill_slot) CU(cudaMallocHost(&p, std::max<size_t>(need, 1)));
+                ctx->fill_cap = std::max<size_t>(need, 1);
+            }
+        }
         // the copy stream must not overwrite the buffer before earlier work on s is done
         CU(cudaEventRecord(ctx->chunk_ev[n_chunks], s));
         CU(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[n_chunks], 0));
@@ -576,7 +605,20 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         for (uint32_t c = 0; c < n_chunks; c++) {
             const uint32_t e0 = cut[c], e1 = cut[c + 1];
             const uint64_t off = epoch_byte(e0), bytes = epoch_byte(e1) - off;
-            CU(cudaMemcpyAsync(d_pay + off, b->payload + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
+            if (has_fill) {
+                // produce chunk c into a free slot while chunks c-1, c-2 copy and hash
+                const int sl = (int)(c % poslo_gpu_ctx::kFillSlots);
+                CU(cudaEventSynchronize(ctx->fill_ev[sl]));
+                if (b->fill(b->fill_user, (uint64_t)e0 * b->n2, (uint64_t)(e1 - e0) * b->n2, ctx->fill_slot[sl]) != 0) {
+                    cudaStreamSynchronize(ctx->copy);
+                    cudaStreamSynchronize(s);
+                    return set_err(err, POSLO_INVALID_ARGUMENT, 0, "fill producer failed");
+                }
+                CU(cudaMemcpyAsync(d_pay + off, ctx->fill_slot[sl], bytes, cudaMemcpyHostToDevice, ctx->copy));
+                CU(cudaEventRecord(ctx->fill_ev[sl], ctx->copy));
+            } else {
+                CU(cudaMemcpyAsync(d_pay + off, b->payload + off, bytes, cudaMemcpyHostToDevice, ctx->copy));
+            }
             CU(cudaEventRecord(ctx->chunk_ev[c], ctx->copy));
             CU(cudaStreamWaitEvent(s, ctx->chunk_ev[c], 0));
             TileMap t = tm;
@@ -648,13 +690,26 @@ void finish_timing(poslo_gpu_ctx* ctx) {
     cudaEventElapsedTime(&ctx->last_ms[5], ctx->ev[kEvSeed], ctx->ev[kEvEnd]);
 }
 
+// Serialises the calls on one context and makes its device current for the
+// call; the caller's current device is restored on exit (a torch thread on
+// cuda:0 calling a context on device 1 keeps allocating on cuda:0).
 struct Guard {
     poslo_gpu_ctx* ctx;
     std::lock_guard<std::mutex> lk;
+    int prev = -1;
     explicit Guard(poslo_gpu_ctx* c) : ctx(c), lk(c->mtx) {
-        cudaSetDevice(c->device);
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != c->device) cudaSetDevice(c->device);
         c->launches = 0;
     }
+    ~Guard() {
+        if (prev >= 0 && prev != ctx->device) cudaSetDevice(prev);
+    }
+    Guard(const Guard&) = delete;
+    Guard& operator=(const Guard&) = delete;
 };
 
 int upload(poslo_gpu_ctx* ctx, DevBuf& buf, const void* src, size_t bytes, void** out, poslo_error* err) {
@@ -684,13 +739,47 @@ uint32_t comb16_min() {
     return e ? (uint32_t)std::strtoul(e, nullptr, 10) : (1u << 17);
 }
 
+// The generator's tables depend on nothing but the device: built once per
+// process and device (on the first context's stream, then synchronised so
+// every later context and stream can read them) and shared by all contexts.
+struct GenTables {
+    void* tab[3] = {};  // radix 16, radix 256, radix 2^16
+};
+std::mutex g_gen_mtx;
+GenTables g_gen[64];
+
+int gen_table(poslo_gpu_ctx* ctx, int kind, int* d_flags, void** out, poslo_error* err) {
+    std::lock_guard<std::mutex> lk(g_gen_mtx);
+    if (ctx->device < 0 || ctx->device >= 64) return set_err(err, POSLO_CUDA_ERROR, 0, "device index out of range");
+    void*& t = g_gen[ctx->device].tab[kind];
+    if (!t) {
+        const size_t bytes = kind == 0 ? kCombTableBytes : kind == 1 ? kComb256TableBytes : kComb16TableBytes;
+        void* p = nullptr;
+        CU(cudaMalloc(&p, bytes));
+        if (kind == 0)
+            launch_build_table(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
+        else if (kind == 1)
+            launch_build_table256(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
+        else
+            launch_build_table65536(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
+        ctx->launches += 2;
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return set_err(err, POSLO_CUDA_ERROR, 0, "generator table: %s", cudaGetErrorString(e));
+        }
+        t = p;
+    }
+    *out = t;
+    return POSLO_OK;
+}
+
 int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false,
                   bool xwide = false) {
     if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * kGptBytes));
     if (!ctx->d_tabB) {
-        CU(cudaMalloc(&ctx->d_tabB, kCombTableBytes));
-        launch_build_table(nullptr, ctx->d_pk, ctx->d_tabB, d_flags, ctx->stream);
-        ctx->launches += 2;
+        int rc = gen_table(ctx, 0, d_flags, &ctx->d_tabB, err);
+        if (rc) return rc;
     }
     if (!ctx->d_tabY) CU(cudaMalloc(&ctx->d_tabY, kCombTableBytes));
     if (!ctx->tabY_valid || std::memcmp(ctx->tabY_key, y, 32) != 0) {
@@ -710,9 +799,8 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
     }
     if (wide) {
         if (!ctx->d_tabB256) {
-            CU(cudaMalloc(&ctx->d_tabB256, kComb256TableBytes));
-            launch_build_table256(nullptr, ctx->d_pk, ctx->d_tabB256, d_flags, ctx->stream);
-            ctx->launches += 2;
+            int rc = gen_table(ctx, 1, d_flags, &ctx->d_tabB256, err);
+            if (rc) return rc;
         }
         if (!ctx->d_tabY256) CU(cudaMalloc(&ctx->d_tabY256, kComb256TableBytes));
         if (!ctx->tabY256_valid || std::memcmp(ctx->tabY256_key, y, 32) != 0) {
@@ -726,9 +814,8 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
     }
     if (xwide) {
         if (!ctx->d_tabB16) {
-            CU(cudaMalloc(&ctx->d_tabB16, kComb16TableBytes));
-            launch_build_table65536(nullptr, ctx->d_pk, ctx->d_tabB16, d_flags, ctx->stream);
-            ctx->launches += 2;
+            int rc = gen_table(ctx, 2, d_flags, &ctx->d_tabB16, err);
+            if (rc) return rc;
         }
         if (!ctx->d_tabY16) CU(cudaMalloc(&ctx->d_tabY16, kComb16TableBytes));
         if (!ctx->tabY16_valid || std::memcmp(ctx->tabY16_key, y, 32) != 0) {
@@ -801,7 +888,24 @@ bool scalar_canonical(const uint8_t* s) {
 
 }  // namespace
 
+void poslo_gpu_detail::count_op(const poslo_gpu_ctx* ctx, int which, uint64_t n) {
+    if (ctx->count_ops && n) g_ops[which].fetch_add(n, std::memory_order_relaxed);
+}
+using poslo_gpu_detail::count_op;
+using poslo_gpu_detail::kOpCombine;
+using poslo_gpu_detail::kOpDoubleExp;
+using poslo_gpu_detail::kOpExpBase;
+
 extern "C" {
+
+void poslo_gpu_group_op_counts(uint64_t out[4]) {
+    if (!out) return;
+    for (int i = 0; i < 4; i++) out[i] = g_ops[i].load(std::memory_order_relaxed);
+}
+
+void poslo_gpu_reset_group_op_counts(void) {
+    for (auto& c : g_ops) c.store(0, std::memory_order_relaxed);
+}
 
 const char* poslo_gpu_version(void) { return "poslo-b200 0.1 (sm_100a)"; }
 
@@ -843,6 +947,8 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     e = cudaMalloc(&ctx->d_t0, sizeof t0);
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_t0, t0, sizeof t0, cudaMemcpyHostToDevice);
     for (int i = 0; i < 7 && e == cudaSuccess; i++) e = cudaEventCreate(&ctx->ev[i]);
+    for (int i = 0; i < poslo_gpu_ctx::kFillSlots && e == cudaSuccess; i++)
+        e = cudaEventCreateWithFlags(&ctx->fill_ev[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->stage, sizeof(PinnedStage));
     if (e != cudaSuccess) {
         poslo_gpu_destroy(ctx);
@@ -852,8 +958,51 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     return ok(err);
 }
 
+int poslo_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int poslo_gpu_create_multi(const int* devices, int n_devices, poslo_gpu_ctx** out, poslo_error* err) {
+    if (!out || !devices || n_devices < 1) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    *out = nullptr;
+    if (n_devices == 1) return poslo_gpu_create(devices[0], out, err);
+    poslo_gpu_ctx* ctx = new poslo_gpu_ctx();
+    ctx->device = devices[0];
+    for (int k = 0; k < n_devices; k++) {
+        poslo_gpu_ctx* m = nullptr;
+        int rc = poslo_gpu_create(devices[k], &m, err);
+        if (rc) {
+            poslo_gpu_destroy(ctx);
+            return rc;
+        }
+        ctx->members.push_back(m);
+    }
+    *out = ctx;
+    return ok(err);
+}
+
+int poslo_gpu_member_count(const poslo_gpu_ctx* ctx) {
+    if (!ctx) return 0;
+    return ctx->members.empty() ? 1 : (int)ctx->members.size();
+}
+
 void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
     if (!ctx) return;
+    if (!ctx->members.empty()) {  // a multi-device context owns only its members
+        for (poslo_gpu_ctx* m : ctx->members) poslo_gpu_destroy(m);
+        delete ctx;
+        return;
+    }
+    int prev = -1;
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+        cudaGetLastError();
+        prev = -1;
+    }
     cudaSetDevice(ctx->device);
     DevBuf* bufs[] = {&ctx->b_epochs, &ctx->b_x0, &ctx->b_partial, &ctx->b_etilde, &ctx->b_sum,
                       &ctx->b_scratch, &ctx->b_tiles, &ctx->b_starts, &ctx->b_tbegin, &ctx->b_err,
@@ -862,13 +1011,18 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
                       &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok,
                       &ctx->b_scan_exit, &ctx->b_scan_cnt, &ctx->b_scan_start, &ctx->b_scan_base,
-                      &ctx->b_scan_off, &ctx->b_scan_state};
+                      &ctx->b_scan_off, &ctx->b_scan_state, &ctx->b_seg_e, &ctx->b_out_e};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
     if (ctx->stage) cudaFreeHost(ctx->stage);
-    for (void* p : {ctx->d_tabB, ctx->d_tabY, ctx->d_tabB256, ctx->d_tabY256, ctx->d_tabB16, ctx->d_tabY16, ctx->d_pk})
+    // (the generator tables d_tabB* are the process's, shared: not freed here)
+    for (void* p : {ctx->d_tabY, ctx->d_tabY256, ctx->d_tabY16, ctx->d_pk})
         if (p) cudaFree(p);
+    for (auto* p : ctx->fill_slot)
+        if (p) cudaFreeHost(p);
+    for (auto& ev : ctx->fill_ev)
+        if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->chunk_ev) cudaEventDestroy(ev);
@@ -878,10 +1032,12 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
+    if (prev >= 0) cudaSetDevice(prev);
 }
 
 int poslo_gpu_set_stream(poslo_gpu_ctx* ctx, void* stream) {
     if (!ctx) return POSLO_INVALID_ARGUMENT;
+    if (!ctx->members.empty()) ctx = ctx->members[0];  // a stream belongs to one device: member 0's
     std::lock_guard<std::mutex> lk(ctx->mtx);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
     return POSLO_OK;
@@ -889,12 +1045,19 @@ int poslo_gpu_set_stream(poslo_gpu_ctx* ctx, void* stream) {
 
 int poslo_gpu_enable_timing(poslo_gpu_ctx* ctx, int on) {
     if (!ctx) return POSLO_INVALID_ARGUMENT;
+    for (poslo_gpu_ctx* m : ctx->members) m->timing = on != 0;
     ctx->timing = on != 0;
     return POSLO_OK;
 }
 
 int poslo_gpu_last_timings(poslo_gpu_ctx* ctx, float out_ms[6]) {
     if (!ctx || !out_ms) return POSLO_INVALID_ARGUMENT;
+    if (!ctx->members.empty()) {  // the slowest member's stages
+        std::memset(out_ms, 0, 6 * sizeof(float));
+        for (poslo_gpu_ctx* m : ctx->members)
+            for (int i = 0; i < 6; i++) out_ms[i] = std::max(out_ms[i], m->last_ms[i]);
+        return POSLO_OK;
+    }
     std::memcpy(out_ms, ctx->last_ms, sizeof ctx->last_ms);
     return POSLO_OK;
 }
@@ -926,6 +1089,7 @@ int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int
                        uint64_t* offsets, uint64_t cap, uint64_t* n_records, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!n_records || (len && !raw)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     cudaStream_t s = ctx->stream;
     const uint8_t* d_raw = raw;
@@ -972,11 +1136,17 @@ int poslo_gpu_log_scan(poslo_gpu_ctx* ctx, const uint8_t* raw, uint64_t len, int
     return ok(err);
 }
 
-uint32_t poslo_gpu_last_launches(poslo_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint32_t poslo_gpu_last_launches(poslo_gpu_ctx* ctx) {
+    if (!ctx) return 0;
+    uint32_t n = ctx->launches;
+    for (poslo_gpu_ctx* m : ctx->members) n += m->launches;
+    return n;
+}
 
 int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_tilde_out,
                         uint8_t* e_hat_out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!ctx->members.empty()) return multi_agg_ekeys(ctx, b, e_tilde_out, e_hat_out, err);
     Guard g(ctx);
     Prepared P;
     P.want_etilde = e_tilde_out != nullptr;
@@ -1002,11 +1172,96 @@ int poslo_gpu_agg_ekeys(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_til
     return ok(err);
 }
 
+int poslo_gpu_agg_ekeys_partial(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* d_e_part, poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!d_e_part) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) {  // fold of the members' shards, left on member 0's device
+        uint8_t part[32];
+        int rc = multi_agg_ekeys(ctx, b, nullptr, part, err);
+        if (rc) return rc;
+        poslo_gpu_ctx* m0 = ctx->members[0];
+        Guard g(m0);
+        CU(cudaMemcpyAsync(d_e_part, part, 32, cudaMemcpyHostToDevice, m0->stream));
+        CU(cudaStreamSynchronize(m0->stream));
+        return ok(err);
+    }
+    if (!device_readable(d_e_part)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "d_e_part is not device memory");
+    Guard g(ctx);
+    Prepared P;
+    P.want_etilde = false;
+    int rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    mark(ctx, kEvSum);
+    uint32_t* d_scr;
+    ENSURE(b_scratch, 17 * 1024, d_scr);
+    launch_sum_mod_l(P.sum_src, P.sum_limbs, b->n_epochs, nullptr, reinterpret_cast<uint32_t*>(d_e_part), d_scr,
+                     ctx->stream);
+    ctx->launches += 2;
+    mark(ctx, kEvGroup);
+    rc = check_hash_errors(ctx, b, err);
+    if (rc) return rc;
+    finish_timing(ctx);
+    return ok(err);
+}
+
+int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t* e_parts, int32_t parts_on_device,
+                            const uint8_t y[32], const uint8_t s_hat[32], const uint8_t r_hat[32], uint8_t* verdict,
+                            poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!y || !s_hat || !r_hat || !verdict || (n_parts && !e_parts))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
+    if (!scalar_canonical(s_hat)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    if (parts_on_device) {
+        if (n_parts && !device_readable(e_parts))
+            return set_err(err, POSLO_INVALID_ARGUMENT, 0, "parts_on_device with a host pointer");
+    } else {
+        for (uint32_t k = 0; k < n_parts; k++)
+            if (!scalar_canonical(e_parts + 32 * (size_t)k))
+                return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    }
+    Guard g(ctx);
+    int* d_flags;
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    int rc = ensure_tables(ctx, y, d_flags, err);  // validates Y (syncs only when Y changed)
+    if (rc) return rc;
+    const uint32_t* d_parts;
+    if (parts_on_device) {
+        d_parts = reinterpret_cast<const uint32_t*>(e_parts);
+    } else {
+        uint32_t* d_up;
+        UPLOAD(b_e, e_parts, (size_t)n_parts * 32, d_up);
+        d_parts = d_up;
+    }
+    uint32_t *d_sum, *d_scr, *d_s;
+    uint8_t *d_rhat, *d_verdict;
+    void* d_pre;
+    ENSURE(b_sum, 8, d_sum);
+    ENSURE(b_scratch, 17 * 1024, d_scr);
+    UPLOAD(b_s, s_hat, 32, d_s);
+    UPLOAD(b_rhat, r_hat, 32, d_rhat);
+    ENSURE(b_pre, 256, d_pre);
+    ENSURE(b_verdict, 1, d_verdict);
+    // the rank-ordered fold mod l (batch_verify.cpp:83-85), then the one check (:86)
+    launch_sum_mod_l(d_parts, 8, n_parts, nullptr, d_sum, d_scr, ctx->stream);
+    launch_check_pre(ctx->d_tabB, d_s, d_rhat, d_pre, ctx->stream);
+    launch_check_post(ctx->d_tabY, d_sum, d_pre, d_verdict, ctx->stream);
+    ctx->launches += 4;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&ctx->stage->verdict, d_verdict, 1, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *verdict = ctx->stage->verdict;
+    count_op(ctx, kOpDoubleExp, 1);
+    return ok(err);
+}
+
 int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
                     const uint8_t s_hat[32], const uint8_t* r_hat_agg, const uint8_t* r_hats,
                     uint8_t* verdict, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!b || !y || !s_hat || !verdict) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) return multi_paver(ctx, b, y, s_hat, r_hat_agg, r_hats, verdict, err);
     Guard g(ctx);
     // 1. every batch holds exactly n2 entries (batch_verify.cpp:68-70)
     if (b->epoch_starts)
@@ -1077,6 +1332,9 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     if (rc) return rc;
     if (!r_hat_agg && hs->flags[1]) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
     *verdict = hs->verdict;
+    // batch_verify.cpp:80 (one group_combine per folded epoch) and :86 (one commit_check)
+    if (!r_hat_agg) count_op(ctx, kOpCombine, b->n_epochs);
+    count_op(ctx, kOpDoubleExp, 1);
     finish_timing(ctx);
     return ok(err);
 }
@@ -1131,6 +1389,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!b || !y || (b->n_epochs && (!s_hats || !r_hats || !verdicts)))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) return multi_epoch_verify(ctx, b, y, s_hats, r_hats, verdicts, e_tilde_out, err);
     Guard g(ctx);
     if (!b->device_resident)  // device-resident signature arrays were validated when parsed
         for (uint32_t k = 0; k < b->n_epochs; k++)
@@ -1207,6 +1466,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     }
     if (e_tilde_out && b->n_epochs)
         CU(cudaMemcpy(e_tilde_out, P.d_etilde, (size_t)b->n_epochs * 32, cudaMemcpyDeviceToHost));
+    count_op(ctx, kOpDoubleExp, n);  // one commit_check per epoch
     finish_timing(ctx);
     return ok(err);
 }
@@ -1254,6 +1514,7 @@ int poslo_gpu_segfold(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* scalars, co
                       poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (n_seg && !seg) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null segments");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     uint32_t* d_s = nullptr;
     uint8_t* d_r = nullptr;
@@ -1263,13 +1524,27 @@ int poslo_gpu_segfold(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* scalars, co
     if (mask) UPLOAD(b_mask, mask, std::max<uint32_t>(n, 1), d_mask);
     int rc = segfold_dev(ctx, n, d_s, d_r, d_mask, seg, n_seg, out_s, out_r, err);
     if (rc) return rc;
+    if (points && out_r) {  // group_combine per folded point
+        uint64_t kept = 0;
+        for (uint32_t g2 = 0; g2 < n_seg; g2++)
+            for (uint32_t k = seg[g2]; k < seg[g2 + 1]; k++) kept += !mask || mask[k];
+        count_op(ctx, kOpCombine, kept);
+    }
     return ok(err);
 }
 
 int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
                              const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg, uint32_t n_seg,
                              uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r, poslo_error* err) {
+    return poslo_gpu_distill_coarse_ex(ctx, b, y, s_hats, r_hats, seg, n_seg, verdicts, seg_s, seg_r, nullptr, err);
+}
+
+int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32],
+                                const uint8_t* s_hats, const uint8_t* r_hats, const uint32_t* seg, uint32_t n_seg,
+                                uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r, uint8_t* seg_e, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!ctx->members.empty())
+        return multi_distill_coarse(ctx, b, y, s_hats, r_hats, seg, n_seg, verdicts, seg_s, seg_r, seg_e, err);
     if (!b || !y || (b->n_epochs && (!s_hats || !r_hats || !verdicts)) || (n_seg && !seg))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
     Guard g(ctx);
@@ -1340,6 +1615,19 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         ctx->launches += 1;
     }
     CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (seg_e && n_seg) {  // e-sums of the valid epochs per segment (SeBVer mode U's operand)
+        for (uint32_t g2 = 0; g2 < n_seg; g2++)
+            if (seg[g2] > seg[g2 + 1] || seg[g2 + 1] > n)
+                return set_err(err, POSLO_INVALID_ARGUMENT, 0, "segments must be non-decreasing within [0, n]");
+        std::vector<uint64_t> seg64(seg, seg + n_seg + 1);
+        uint64_t* d_seg;
+        uint32_t* d_out;
+        UPLOAD(b_seg_e, seg64.data(), seg64.size() * 8, d_seg);
+        ENSURE(b_out_e, (size_t)n_seg * 8, d_out);
+        launch_segsum_mod_l(P.d_etilde, d_seg, n_seg, d_verdict, d_out, ctx->stream, /*skip_val=*/0);
+        ctx->launches += 1;
+        CU(cudaMemcpyAsync(seg_e, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     if (split) {  // scalars as before; points from the decoded R-hats (no second decode)
         rc = segfold_dev(ctx, n, d_s, nullptr, d_verdict, seg, n_seg, seg_s, nullptr, err);
         if (rc) return rc;
@@ -1361,6 +1649,13 @@ int poslo_gpu_distill_coarse(poslo_gpu_ctx* ctx, const poslo_batch* b, const uin
         rc = segfold_dev(ctx, n, d_s, d_r, d_verdict, seg, n_seg, seg_s, seg_r, err);
         if (rc) return rc;
     }
+    CU(cudaStreamSynchronize(ctx->stream));
+    // per epoch, aver (poslo_c.cpp:199-212: one R-hat combine, one commit_check),
+    // then fold_valid (distiller.cpp:45-53: two combines per valid epoch)
+    uint64_t n_valid = 0;
+    for (uint32_t k = 0; k < n; k++) n_valid += verdicts[k] != 0;
+    count_op(ctx, kOpDoubleExp, n);
+    count_op(ctx, kOpCombine, n + 2 * n_valid);
     finish_timing(ctx);
     return ok(err);
 }
@@ -1455,6 +1750,7 @@ static int fine_scalars_dev(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint
 int poslo_gpu_fine_scalars(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint8_t* e_out, uint8_t* e_sum,
                            poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     uint32_t* d_e;
     int rc = fine_scalars_dev(ctx, fb, &d_e, err);
@@ -1479,12 +1775,17 @@ int poslo_gpu_fine_verify(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const 
     if (!fb || !y || (fb->n_entries && (!s || !r || !verdicts)))
         return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
     if (fb->n_entries > 0xFFFFFFFFull) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "too many entries");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
+    // FineSignature::s was parsed with Scalar::from_be_bytes (< l): refuse others
+    for (uint64_t t = 0; t < fb->n_entries; t++)
+        if (!scalar_canonical(s + 32 * t)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
     Guard g(ctx);
     uint32_t* d_e;
     int rc = fine_scalars_dev(ctx, fb, &d_e, err);
     if (rc) return rc;
     const uint32_t n = (uint32_t)fb->n_entries;
     if (!n) return ok(err);
+    count_op(ctx, kOpDoubleExp, n);
     uint32_t* d_s;
     uint8_t* d_r;
     UPLOAD(b_s, s, (size_t)n * 32, d_s);
@@ -1498,10 +1799,13 @@ int poslo_gpu_aver_f_batch(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, const
                            const uint8_t r[32], uint8_t* verdict, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!fb || !y || !s || !r || !verdict) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
+    if (!scalar_canonical(s)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
     Guard g(ctx);
     uint32_t* d_e;
     int rc = fine_scalars_dev(ctx, fb, &d_e, err);
     if (rc) return rc;
+    count_op(ctx, kOpDoubleExp, 1);
     uint32_t *d_sum, *d_scr, *d_s;
     uint8_t* d_r;
     ENSURE(b_sum, 8, d_sum);
@@ -1522,51 +1826,66 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[3
                      const uint8_t* umb_s, const uint8_t* umb_r, uint32_t n_umb, uint8_t* u_bits,
                      uint8_t* i_bits, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     if (!b || !y || n_u == 0 || n1 % n_u) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "bad argument");
+    if ((n_invalid && (!invalid || (i_bits && (!invalid_s || !invalid_r)))) || (v_bit && (!v_s || !v_r)) ||
+        (u_bits && n_umb && (!umb_index || !umb_s || !umb_r)))
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    // CCD scalars were parsed with Scalar::from_be_bytes (< l); the comb digit
+    // recoding relies on it, so a C-ABI caller's non-canonical scalar is refused
+    auto canon = [](const uint8_t* p, uint32_t cnt) {
+        for (uint32_t k = 0; k < cnt; k++)
+            if (!scalar_canonical(p + 32 * (size_t)k)) return false;
+        return true;
+    };
+    if ((i_bits && !canon(invalid_s, n_invalid)) || (v_bit && !canon(v_s, 1)) || (u_bits && !canon(umb_s, n_umb)))
+        return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
     Guard g(ctx);
-    for (uint32_t k = 0; k < b->n_epochs; k++)
-        if (b->epochs[k] != k) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "sebver batch must hold epochs 0..n-1");
     Prepared P;
-    int rc = run_hash(ctx, b, P, err);
+    int rc = run_hash(ctx, b, P, err);  // only the epochs SeBVer reads are in the batch
     if (rc) return rc;
     rc = check_hash_errors(ctx, b, err);
     if (rc) return rc;
     cudaStream_t s = ctx->stream;
-    uint32_t n_ep = b->n_epochs;
-    std::vector<uint8_t> mask(std::max<uint32_t>(n_ep, 1), 0);
-    for (uint32_t k = 0; k < n_invalid; k++)
-        if (invalid[k] < n_ep) mask[invalid[k]] = 1;
+    const uint32_t n_ep = b->n_epochs;
+    const uint32_t* ep = b->epochs;
+    // batch position of the first epoch >= e (the batch is ascending)
+    auto pos = [&](uint64_t e) -> uint64_t {
+        if (e > 0xFFFFFFFFull) return n_ep;
+        return (uint64_t)(std::lower_bound(ep, ep + n_ep, (uint32_t)e) - ep);
+    };
+    std::vector<uint8_t> mask(std::max<uint32_t>(n_ep, 1), 0);  // 1 = invalid epoch: left out of every e-sum
+    for (uint32_t k = 0; k < n_invalid; k++) {
+        const uint64_t q = pos(invalid[k]);
+        if (q < n_ep && ep[q] == invalid[k]) mask[q] = 1;
+    }
     uint8_t* d_mask;
     UPLOAD(b_mask, mask.data(), mask.size(), d_mask);
-    uint32_t w = n1 / n_u;
+    const uint32_t w = n1 / n_u;
     // groups: [V] + U umbrellas + I records, e per group on device
-    uint32_t nV = v_bit ? 1 : 0, nU = u_bits ? n_umb : 0, nI = i_bits ? n_invalid : 0;
-    uint32_t ng = nV + nU + nI;
+    const uint32_t nV = v_bit ? 1 : 0, nU = u_bits ? n_umb : 0, nI = i_bits ? n_invalid : 0;
+    const uint32_t ng = nV + nU + nI;
     if (!ng) return ok(err);
     std::vector<uint64_t> seg;
     std::vector<uint8_t> hs((size_t)ng * 32), hr((size_t)ng * 32);
     uint32_t gi = 0;
-    auto clip = [&](uint64_t v) { return std::min<uint64_t>(v, n_ep); };
-    if (nV) {
+    if (nV) {  // every batch epoch (the distilled ones that SeBVer hashes)
         seg.push_back(0);
         seg.push_back(n_ep);
         std::memcpy(&hs[0], v_s, 32);
         std::memcpy(&hr[0], v_r, 32);
         gi++;
     }
-    for (uint32_t u = 0; u < nU; u++, gi++) {
-        seg.push_back(clip((uint64_t)umb_index[u] * w));
-        seg.push_back(clip((uint64_t)(umb_index[u] + 1) * w));
+    for (uint32_t u = 0; u < nU; u++, gi++) {  // batch epochs in [u w, (u + 1) w)
+        seg.push_back(pos((uint64_t)umb_index[u] * w));
+        seg.push_back(pos((uint64_t)(umb_index[u] + 1) * w));
         std::memcpy(&hs[32 * gi], umb_s + 32 * (size_t)u, 32);
         std::memcpy(&hr[32 * gi], umb_r + 32 * (size_t)u, 32);
     }
-    // segsum takes [seg[g], seg[g+1]) over consecutive pairs; use a flat
-    // pair list with a stride-2 view by summing per group separately.
     uint32_t* d_e;
     ENSURE(b_e, (size_t)ng * 8, d_e);
-    uint32_t n_seg_groups = nV + nU;
-    if (n_seg_groups) {
-        // pair list -> launch one segsum per pair via seg array of 2 per group
+    const uint32_t n_seg_groups = nV + nU;
+    if (n_seg_groups) {  // one masked sum per [lo, hi) pair
         uint64_t* d_seg;
         UPLOAD(b_seg, seg.data(), seg.size() * 8, d_seg);
         for (uint32_t g2 = 0; g2 < n_seg_groups; g2++) {
@@ -1575,9 +1894,10 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[3
         }
     }
     for (uint32_t k = 0; k < nI; k++, gi++) {
-        uint32_t ep = invalid[k];
-        if (ep >= n_ep) return set_err(err, POSLO_FORMAT_ERROR, ep, "messages for invalid epoch missing");
-        CU(cudaMemcpyAsync(d_e + 8 * (size_t)gi, P.d_etilde + 8 * (size_t)ep, 32, cudaMemcpyDeviceToDevice, s));
+        const uint32_t e = invalid[k];
+        const uint64_t q = pos(e);
+        if (q >= n_ep || ep[q] != e) return set_err(err, POSLO_FORMAT_ERROR, e, "messages for invalid epoch missing");
+        CU(cudaMemcpyAsync(d_e + 8 * (size_t)gi, P.d_etilde + 8 * q, 32, cudaMemcpyDeviceToDevice, s));
         std::memcpy(&hs[32 * gi], invalid_s + 32 * (size_t)k, 32);
         std::memcpy(&hr[32 * gi], invalid_r + 32 * (size_t)k, 32);
     }
@@ -1588,6 +1908,7 @@ int poslo_gpu_sebver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[3
     std::vector<uint8_t> bits(ng);
     rc = group_check_dev(ctx, y, ng, d_e, d_s, d_r, bits.data(), nullptr, err);
     if (rc) return rc;
+    count_op(ctx, kOpDoubleExp, ng);  // verify_range / the mode-I check: one commit_check each
     gi = 0;
     if (nV) *v_bit = bits[gi++];
     for (uint32_t u = 0; u < nU; u++) u_bits[u] = bits[gi++];
@@ -1601,6 +1922,7 @@ int poslo_gpu_kg_commitments(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t r_
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (suite < 1 || suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
     if (!r_seed || (n && (!epochs || !r_hats_out))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     if (!n) return ok(err);
     uint32_t rw[4];
@@ -1616,6 +1938,7 @@ int poslo_gpu_kg_commitments(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t r_
     static const uint8_t identity[32] = {0};
     int rc = group_check_dev(ctx, identity, n, d_zero, d_r, nullptr, nullptr, r_hats_out, err);
     if (rc) return rc;
+    count_op(ctx, kOpExpBase, n);  // kg: one exp_base per epoch (poslo_c.cpp:91-113)
     if (r_scalars_out) {
         CU(cudaMemcpyAsync(r_scalars_out, d_r, (size_t)n * 32, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -1628,6 +1951,7 @@ int poslo_gpu_sig_epochs(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!b || !r_seed || !y || (b->n_epochs && !s_hats_out)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
     if (!scalar_canonical(y)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     // sig_epoch (poslo_c.cpp:117-118): every epoch batch holds exactly n2 entries
     if (b->epoch_starts)
@@ -1660,6 +1984,7 @@ int poslo_gpu_commit_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], 
                            const uint8_t* s, uint8_t* out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!y || (n && (!e || !s || !out))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     for (uint32_t i = 0; i < n; i++)
         if (!scalar_canonical(e + 32 * (size_t)i) || !scalar_canonical(s + 32 * (size_t)i))
@@ -1669,6 +1994,9 @@ int poslo_gpu_commit_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], 
     UPLOAD(b_s, s, (size_t)n * 32, d_s);
     int rc = group_check_dev(ctx, y, n, d_e, d_s, nullptr, nullptr, out, err);
     if (rc) return rc;
+    bool y_id = true;
+    for (int k = 0; k < 32; k++) y_id &= y[k] == 0;
+    count_op(ctx, y_id ? kOpExpBase : kOpDoubleExp, n);
     return ok(err);
 }
 
@@ -1676,6 +2004,7 @@ int poslo_gpu_group_fold(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* pts, uin
                          poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!out || (n && !pts)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     uint8_t *d_pts, *d_out;
     void* d_fs;
@@ -1693,6 +2022,7 @@ int poslo_gpu_group_fold(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* pts, uin
     CU(cudaMemcpyAsync(out, d_out, 32, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (bad) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    count_op(ctx, kOpCombine, n);  // agg_elements: one group_combine per element (poslo_c.cpp:170-174)
     return ok(err);
 }
 
@@ -1700,6 +2030,7 @@ int poslo_gpu_point_valid(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* pts, ui
                           poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (n && (!pts || !okv)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     uint8_t *d_pts, *d_ok;
     UPLOAD(b_pts, pts, (size_t)n * 32, d_pts);
@@ -1718,6 +2049,7 @@ int poslo_gpu_seed_retrieve(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t* ds
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (n && (!epochs || !x0_out)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
     if (suite < 1 || suite > 3) return set_err(err, POSLO_FORMAT_ERROR, 0, "unknown suite id");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     DsParam dsp;
     int rc = parse_ds(ds, ds_len, ds_capacity, dsp, err);
@@ -1747,6 +2079,7 @@ int poslo_gpu_seed_retrieve(poslo_gpu_ctx* ctx, uint8_t suite, const uint8_t* ds
 int poslo_gpu_entry_scalars(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_t* e_out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!b || !e_out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     // Force the generic path with per-entry output.
     Prepared P;
@@ -1777,6 +2110,7 @@ int poslo_gpu_scalar_sum(poslo_gpu_ctx* ctx, uint64_t n, const uint8_t* scalars,
                          poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!out || (n && !scalars)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     for (uint64_t i = 0; i < n; i++)
         if (!scalar_canonical(scalars + 32 * i)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
@@ -1796,6 +2130,7 @@ int poslo_gpu_group_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], c
                           const uint8_t* s, const uint8_t* r, uint8_t* verdicts, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (!y || (n && (!e || !s || !r || !verdicts))) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     for (uint32_t i = 0; i < n; i++)
         if (!scalar_canonical(e + 32 * (size_t)i) || !scalar_canonical(s + 32 * (size_t)i))
@@ -1807,6 +2142,7 @@ int poslo_gpu_group_check(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t y[32], c
     UPLOAD(b_r, r, (size_t)n * 32, d_r);
     int rc = group_check_dev(ctx, y, n, d_e, d_s, d_r, verdicts, nullptr, err);
     if (rc) return rc;
+    count_op(ctx, kOpDoubleExp, n);
     return ok(err);
 }
 
@@ -1814,6 +2150,7 @@ int poslo_gpu_synth_log(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, uint6
                         uint32_t entry_len, void* d_out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (n && !d_out) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     launch_synth_fixed(seed, first, n, entry_len, static_cast<uint8_t*>(d_out), ctx->stream);
     ctx->launches += n ? 1 : 0;
@@ -1826,6 +2163,7 @@ int poslo_gpu_synth_varlog(poslo_gpu_ctx* ctx, uint64_t seed, uint64_t first, ui
                            const uint64_t* d_offsets, void* d_out, poslo_error* err) {
     if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
     if (n && (!d_out || !d_offsets)) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
     Guard g(ctx);
     launch_synth_var(seed, first, n, d_offsets, static_cast<uint8_t*>(d_out), ctx->stream);
     ctx->launches += n ? 1 : 0;

@@ -91,6 +91,11 @@ void launch_hash_generic(int suite, const EntryLayout& lay, const TileMap& tm, c
 void launch_hash_s1_var(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0, uint32_t* d_partial,
                         cudaStream_t s);
 
+// Layout check of caller-supplied entry offsets (n entries, n + 1 offsets):
+// *d_bad = 1 unless lo <= off[0], off[t] + header <= off[t+1] and off[n] <= hi.
+void launch_check_offsets(const uint64_t* d_off, uint64_t n, uint32_t header, uint64_t lo, uint64_t hi, int* d_bad,
+                          cudaStream_t s);
+
 // Per-epoch e~ from tile partials (skipped when tiles_per_epoch == 1 on the
 // fast paths, which finalise in the hashing kernel).
 void launch_epoch_finalize(const TileMap& tm, const uint32_t* d_partial, uint32_t* d_etilde,

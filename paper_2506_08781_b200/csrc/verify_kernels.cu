@@ -398,6 +398,26 @@ __global__ void k_synth_var(uint64_t seed, uint64_t first, uint64_t n, const uin
 }  // namespace
 
 // ---------------------------------------------------------------- launchers
+// One thread per gap, grid-strided: a read of 8 bytes per entry (~10 us per
+// 2^22 offsets), run once per call before any hashing kernel.
+__global__ void __launch_bounds__(256) k_check_offsets(const uint64_t* __restrict__ off, uint64_t n, uint32_t header,
+                                                       uint64_t lo, uint64_t hi, int* bad) {
+    bool ok = true;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = off[t], z = off[t + 1];
+        ok &= z >= a && z - a >= header;
+        if (t == 0) ok &= a >= lo;
+        if (t == n - 1) ok &= z <= hi;
+    }
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+void launch_check_offsets(const uint64_t* d_off, uint64_t n, uint32_t header, uint64_t lo, uint64_t hi, int* d_bad,
+                          cudaStream_t s) {
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 8);
+    k_check_offsets<<<(unsigned)std::max<uint64_t>(blocks, 1), 256, 0, s>>>(d_off, n, header, lo, hi, d_bad);
+}
+
 void launch_seed_derive(int suite, const DsParam& ds, const uint32_t* d_epochs, uint32_t epoch0, uint32_t n_epochs,
                         uint4* d_x0, unsigned long long* d_err, const uint32_t* d_t0, cudaStream_t s) {
     if (n_epochs == 0) return;

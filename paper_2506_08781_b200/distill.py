@@ -212,21 +212,44 @@ class ColdCryptoData:
         if self.scheme == FINE:
             return self._sebver_fine(y, all_msgs, mode)
         w = self.umbrella_width()
+        bad = {i for i, _, _ in self.invalid}
+        # the groups SeBVer checks, in its order, with the epochs each one reads
+        # (collect_epochs, :140-154, or the mode-I lookup, :208-210) and hashes
+        # (verify_range skips invalid epochs, :161-162)
         if mode == "I":
-            need = [i for i, _, _ in self.invalid]
+            groups = [([i], [i]) for i, _, _ in self.invalid]
         elif mode == "V":
-            need = list(range(self.next_epoch))
+            rng = list(range(self.next_epoch))
+            groups = [(rng, [i for i in rng if i not in bad])]
         else:
-            need = sorted({i for u, _, _ in self.umbrellas for i in range(u * w, min((u + 1) * w, self.next_epoch))})
-        for i in need:  # collect_epochs (:140-154) / the mode-I lookup (:208-210)
-            if i not in all_msgs:
-                raise FormatError("messages for invalid epoch missing" if mode == "I"
-                                  else f"messages for epoch {i} missing")
-            if mode != "I" and len(all_msgs[i]) != self.suite.n2:
-                raise FormatError("epoch batch size mismatch")
-        res = self.v.sebver(y, self.suite, all_msgs, self.ds, self.next_epoch, self.invalid,
-                            self.umbrellas if mode == "U" else [],
-                            self.valid_ if mode == "V" else None)
+            groups = []
+            for u, _, _ in self.umbrellas:
+                rng = list(range(u * w, min((u + 1) * w, self.next_epoch)))
+                groups.append((rng, [i for i in rng if i not in bad]))
+        # the reference raises at the first group whose messages are missing, after
+        # hashing (and raising the hashing errors of) every group before it
+        hashed, missing, live = set(), None, len(groups)
+        for k, (read, hash_) in enumerate(groups):
+            for i in read:
+                if i not in all_msgs:
+                    missing = FormatError("messages for invalid epoch missing" if mode == "I"
+                                          else f"messages for epoch {i} missing")
+                    break
+                if mode != "I" and len(all_msgs[i]) != self.suite.n2:
+                    missing = FormatError("epoch batch size mismatch")
+                    break
+            if missing is not None:
+                live = k
+                break
+            hashed.update(hash_)
+        if missing is not None and live == 0:
+            raise missing
+        res = self.v.sebver(y, self.suite, all_msgs, self.ds, self.next_epoch,
+                            self.invalid[:live] if mode == "I" else self.invalid,
+                            self.umbrellas[:live] if mode == "U" else [],
+                            self.valid_ if mode == "V" else None, hashed=sorted(hashed))
+        if missing is not None:
+            raise missing
         return res[mode]
 
     def _sebver_fine(self, y, all_msgs, mode):

@@ -5,14 +5,28 @@
 // include/poslo_gpu.h. Compiled against the reference's own headers in place
 // of src/batch_verify.cpp; see INTEGRATION.md.
 //
-// The std::map<uint32_t, std::vector<Bytes>> batches are packed into one
-// payload (+ byte offsets when lengths differ) and epoch ranges; all hashing,
-// modular sums and the group check run on the device. `workers` keeps its
-// reference meaning only as a parameter check (0 -> StateError).
+// `workers` keeps its reference meaning as the degree of parallelism: the
+// call runs on min(workers, #GPUs) devices (batch_verify.cpp:51-59 spawns
+// min(workers, #epochs) threads), sharded by contiguous epoch ranges inside
+// one C-ABI call (poslo_gpu_create_multi); workers == 0 -> StateError.
+// POSLO_GPU_DEVICES=0,1,... lists the devices (a device may repeat: members
+// then share it), default every visible device; POSLO_GPU_DEVICE=k pins one.
+//
+// The std::map<uint32_t, std::vector<Bytes>> is not copied up front: the C-ABI
+// pulls the entries chunk by chunk through poslo_batch.fill, and each chunk is
+// gathered into pinned staging by all host cores (a persistent worker pool)
+// while the previous chunks are copied to the device and hashed.
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "poslo/batch_verify.hpp"
 #include "poslo_gpu.h"
@@ -21,25 +35,137 @@ namespace poslo {
 
 namespace {
 
-// One device context per host thread: the C-ABI serialises calls per
-// context, so thread-local contexts keep concurrent callers independent
-// ("externally a pure, thread-safe function").
-struct DeviceContext {
-    poslo_gpu_ctx* ctx = nullptr;
-    DeviceContext() {
-        poslo_error err{};
-        int dev = 0;
-        if (const char* e = std::getenv("POSLO_GPU_DEVICE")) dev = std::atoi(e);
-        if (poslo_gpu_create(dev, &ctx, &err) != POSLO_OK)
-            throw std::runtime_error(std::string("poslo_gpu: ") + err.message);
+// Persistent host workers for the gather/sizing loops: parallel_for(n, f)
+// runs f(0..n-1) on every core (the caller included); one loop at a time.
+class Pool {
+public:
+    Pool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned n = std::min(hw, 64u) - 1;
+        for (unsigned i = 0; i < n; i++) th_.emplace_back([this] { work(); });
     }
-    ~DeviceContext() { poslo_gpu_destroy(ctx); }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void parallel_for(int64_t n, const std::function<void(int64_t)>& f) {
+        if (n <= 0) return;
+        std::lock_guard<std::mutex> one(call_);
+        if (th_.empty() || n == 1) {
+            for (int64_t i = 0; i < n; i++) f(i);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            job_ = &f;
+            n_ = n;
+            next_.store(0);
+            busy_ = (int)th_.size();
+            gen_++;
+        }
+        cv_.notify_all();
+        run();
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return busy_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void run() {
+        for (int64_t i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*job_)(i);
+    }
+    void work() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            run();
+            std::lock_guard<std::mutex> lk(m_);
+            if (--busy_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_, call_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int64_t)>* job_ = nullptr;
+    int64_t n_ = 0;
+    std::atomic<int64_t> next_{0};
+    int busy_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
 };
 
-poslo_gpu_ctx* device() {
-    thread_local std::unique_ptr<DeviceContext> dc;
-    if (!dc) dc = std::make_unique<DeviceContext>();
-    return dc->ctx;
+Pool& pool() {
+    static Pool p;
+    return p;
+}
+
+// f over [0, n) in blocks of `grain` on the pool
+void parallel_blocks(int64_t n, int64_t grain, const std::function<void(int64_t, int64_t)>& f) {
+    const int64_t nb = (n + grain - 1) / grain;
+    pool().parallel_for(nb, [&](int64_t blk) { f(blk * grain, std::min(n, (blk + 1) * grain)); });
+}
+
+std::vector<int> parse_devices() {
+    std::vector<int> out;
+    if (const char* e = std::getenv("POSLO_GPU_DEVICES")) {
+        const std::string s(e);
+        size_t p = 0;
+        while (p < s.size()) {
+            size_t q = s.find(',', p);
+            if (q == std::string::npos) q = s.size();
+            if (q > p) out.push_back(std::atoi(s.substr(p, q - p).c_str()));
+            p = q + 1;
+        }
+    } else if (const char* e1 = std::getenv("POSLO_GPU_DEVICE")) {
+        out.push_back(std::atoi(e1));
+    } else {
+        const int n = poslo_gpu_device_count();
+        for (int d = 0; d < n; d++) out.push_back(d);
+    }
+    if (out.empty()) out.push_back(0);
+    return out;
+}
+
+const std::vector<int>& device_list() {
+    static const std::vector<int> list = parse_devices();
+    return list;
+}
+
+// Device contexts of one host thread, one per GPU count: the C-ABI serialises
+// calls per context, so thread-local contexts keep concurrent callers
+// independent ("externally a pure, thread-safe function").
+struct DeviceContexts {
+    std::map<size_t, poslo_gpu_ctx*> by_count;
+    ~DeviceContexts() {
+        for (auto& [g, c] : by_count) poslo_gpu_destroy(c);
+    }
+    poslo_gpu_ctx* get(size_t g) {
+        auto it = by_count.find(g);
+        if (it != by_count.end()) return it->second;
+        poslo_gpu_ctx* c = nullptr;
+        poslo_error err{};
+        const std::vector<int>& L = device_list();
+        const int rc = g > 1 ? poslo_gpu_create_multi(L.data(), static_cast<int>(g), &c, &err)
+                             : poslo_gpu_create(L[0], &c, &err);
+        if (rc != POSLO_OK) throw std::runtime_error(std::string("poslo_gpu: ") + err.message);
+        by_count[g] = c;
+        return c;
+    }
+};
+
+poslo_gpu_ctx* device(unsigned workers) {
+    thread_local DeviceContexts dc;
+    const size_t g = std::min<size_t>(std::max(1u, workers), device_list().size());
+    return dc.get(g);
 }
 
 [[noreturn]] void rethrow(const poslo_error& e) {
@@ -51,60 +177,119 @@ poslo_gpu_ctx* device() {
     }
 }
 
+// The batches as the C-ABI sees them: epoch list, entry ranges, byte
+// offsets for variable-length entries, and a producer that gathers any entry
+// range into a packed buffer.
 struct Packed {
-    std::vector<uint8_t> payload;
-    std::vector<uint64_t> offsets;
+    std::vector<const std::vector<Bytes>*> msgs;  // per queried epoch, map order
     std::vector<uint32_t> epochs;
-    std::vector<uint64_t> starts;
+    std::vector<uint64_t> starts;   // n_epochs + 1 entry indices
+    std::vector<uint64_t> offsets;  // n_entries + 1 byte offsets (variable lengths only)
+    bool fixed = true, uniform = true;
+    uint32_t len0 = 0;
     Bytes ds;
     poslo_batch b{};
 };
 
+uint64_t byte_at(const Packed& p, uint64_t t) { return p.fixed ? t * p.len0 : p.offsets[t]; }
+
+// poslo_batch.fill: entries [first, first + count) back to back into dst,
+// epochs spread over the host cores.
+int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
+    const Packed& p = *static_cast<const Packed*>(user);
+    const uint64_t last = first + count;
+    const int64_t k0 = std::upper_bound(p.starts.begin(), p.starts.end(), first) - p.starts.begin() - 1;
+    const int64_t k1 = std::lower_bound(p.starts.begin(), p.starts.end(), last) - p.starts.begin();
+    const uint64_t base = byte_at(p, first);
+    const int64_t kb = std::max<int64_t>(k0, 0);
+    parallel_blocks(k1 - kb, 16, [&](int64_t a, int64_t z) {
+        for (int64_t k = kb + a; k < kb + z; k++) {
+            const std::vector<Bytes>& ms = *p.msgs[k];
+            const uint64_t s0 = p.starts[k];
+            const uint64_t t0 = std::max(s0, first), t1 = std::min(p.starts[k + 1], last);
+            if (p.fixed) {
+                uint8_t* d = dst + (t0 * p.len0 - base);
+                for (uint64_t t = t0; t < t1; t++, d += p.len0) std::memcpy(d, ms[t - s0].data(), p.len0);
+            } else {
+                for (uint64_t t = t0; t < t1; t++) {
+                    const Bytes& m = ms[t - s0];
+                    if (!m.empty()) std::memcpy(dst + (p.offsets[t] - base), m.data(), m.size());
+                }
+            }
+        }
+    });
+    return 0;
+}
+
 void pack(const SuiteConfig& suite, const std::map<uint32_t, std::vector<Bytes>>& batches,
           const SeedStack& ds, Packed& p) {
-    size_t total = 0, n = 0;
-    bool fixed = true, uniform = true;
-    size_t len0 = SIZE_MAX;
-    for (const auto& [i, msgs] : batches) {
-        p.epochs.push_back(i);
-        if (msgs.size() != suite.n2) uniform = false;
-        for (const auto& m : msgs) {
-            if (len0 == SIZE_MAX) len0 = m.size();
-            if (m.size() != len0) fixed = false;
-            total += m.size();
-            n++;
-        }
-    }
-    p.payload.reserve(total);
-    if (!fixed) p.offsets.reserve(n + 1);
-    if (!uniform) p.starts.reserve(batches.size() + 1);
+    const size_t ne = batches.size();
+    p.msgs.reserve(ne);
+    p.epochs.reserve(ne);
+    p.starts.reserve(ne + 1);
     uint64_t t = 0;
     for (const auto& [i, msgs] : batches) {
-        if (!uniform) p.starts.push_back(t);
-        for (const auto& m : msgs) {
-            if (!fixed) p.offsets.push_back(p.payload.size());
-            p.payload.insert(p.payload.end(), m.begin(), m.end());
-            t++;
-        }
+        p.epochs.push_back(i);
+        p.msgs.push_back(&msgs);
+        p.starts.push_back(t);
+        t += msgs.size();
+        if (msgs.size() != suite.n2) p.uniform = false;
     }
-    if (!fixed) p.offsets.push_back(p.payload.size());
-    if (!uniform) p.starts.push_back(t);
+    p.starts.push_back(t);
+    const uint64_t n = t;
+    // sizing pass over the entry headers, in parallel: one length, or offsets
+    for (size_t k = 0; k < ne && p.len0 == 0 && n; k++)
+        if (!p.msgs[k]->empty()) p.len0 = static_cast<uint32_t>((*p.msgs[k])[0].size());
+    std::atomic<bool> fixed{true};
+    parallel_blocks((int64_t)ne, 256, [&](int64_t a, int64_t z) {
+        bool f = true;
+        for (int64_t k = a; k < z && f; k++)
+            for (const Bytes& m : *p.msgs[k]) f = f && m.size() == p.len0;
+        if (!f) fixed.store(false, std::memory_order_relaxed);
+    });
+    p.fixed = fixed.load();
+    uint64_t total = n * p.len0;
+    if (!p.fixed) {
+        std::vector<uint64_t> ep_bytes(ne + 1, 0);
+        parallel_blocks((int64_t)ne, 256, [&](int64_t a, int64_t z) {
+            for (int64_t k = a; k < z; k++) {
+                uint64_t s = 0;
+                for (const Bytes& m : *p.msgs[k]) s += m.size();
+                ep_bytes[k + 1] = s;
+            }
+        });
+        for (size_t k = 0; k < ne; k++) ep_bytes[k + 1] += ep_bytes[k];
+        p.offsets.resize(n + 1);
+        parallel_blocks((int64_t)ne, 256, [&](int64_t a, int64_t z) {
+            for (int64_t k = a; k < z; k++) {
+                uint64_t o = ep_bytes[k], tt = p.starts[k];
+                for (const Bytes& m : *p.msgs[k]) {
+                    p.offsets[tt++] = o;
+                    o += m.size();
+                }
+            }
+        });
+        p.offsets[n] = ep_bytes[ne];
+        total = ep_bytes[ne];
+    }
     ds.serialize(p.ds);
     poslo_batch& b = p.b;
     b.suite = static_cast<uint8_t>(suite.suite);
     b.n2 = suite.n2;
-    b.payload = p.payload.data();
-    b.payload_bytes = p.payload.size();
-    b.offsets = fixed ? nullptr : p.offsets.data();
-    b.entry_len = fixed && len0 != SIZE_MAX ? static_cast<uint32_t>(len0) : 0;
+    b.payload = nullptr;  // produced on demand by gather()
+    b.payload_bytes = total;
+    b.offsets = p.fixed ? nullptr : p.offsets.data();
+    b.entry_len = p.fixed ? p.len0 : 0;
     b.n_entries = n;
     b.epochs = p.epochs.data();
-    b.epoch_starts = uniform ? nullptr : p.starts.data();
+    b.epoch_starts = p.uniform ? nullptr : p.starts.data();
     b.n_epochs = static_cast<uint32_t>(p.epochs.size());
     b.ds = p.ds.data();
     b.ds_len = static_cast<uint32_t>(p.ds.size());
     b.ds_capacity = ds.capacity();
     b.device_resident = 0;
+    b.fill = n ? gather : nullptr;
+    b.fill_user = &p;
 }
 
 }  // namespace
@@ -117,7 +302,7 @@ std::vector<EpochKeyAggregate> agg_ekeys(const SuiteConfig& suite,
     pack(suite, batches, ds, p);
     std::vector<uint8_t> et(32 * std::max<size_t>(p.epochs.size(), 1));
     poslo_error err{};
-    if (poslo_gpu_agg_ekeys(device(), &p.b, et.data(), nullptr, &err) != POSLO_OK) rethrow(err);
+    if (poslo_gpu_agg_ekeys(device(workers), &p.b, et.data(), nullptr, &err) != POSLO_OK) rethrow(err);
     std::vector<EpochKeyAggregate> out(p.epochs.size());
     for (size_t k = 0; k < p.epochs.size(); k++)
         out[k] = EpochKeyAggregate{p.epochs[k], Scalar::from_canonical_le(et.data() + 32 * k)};
@@ -131,13 +316,15 @@ bool paver(const PoslocPublicKey& pk, const std::map<uint32_t, std::vector<Bytes
     for (const auto& [i, msgs] : batches)
         if (msgs.size() != pk.suite.n2) throw StateError("every batch must hold exactly n2 entries");
     std::vector<uint8_t> r_hats;
-    if (!r_hat_agg) {
-        r_hats.reserve(32 * batches.size());
+    if (!r_hat_agg) {  // both maps are ordered: one merge walk finds every commitment
+        r_hats.resize(32 * batches.size());
+        auto it = pk.r_hats.begin();
+        size_t k = 0;
         for (const auto& [i, msgs] : batches) {
-            auto it = pk.r_hats.find(i);
-            if (it == pk.r_hats.end())
+            while (it != pk.r_hats.end() && it->first < i) ++it;
+            if (it == pk.r_hats.end() || it->first != i)
                 throw StateError("commitment for epoch " + std::to_string(i) + " no longer in public key");
-            r_hats.insert(r_hats.end(), it->second.bytes().begin(), it->second.bytes().end());
+            std::memcpy(&r_hats[32 * k++], it->second.bytes().data(), 32);
         }
     }
     if (workers == 0) throw StateError("worker count must be at least 1");
@@ -145,7 +332,7 @@ bool paver(const PoslocPublicKey& pk, const std::map<uint32_t, std::vector<Bytes
     pack(pk.suite, batches, ds, p);
     uint8_t verdict = 0;
     poslo_error err{};
-    int rc = poslo_gpu_paver(device(), &p.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
+    int rc = poslo_gpu_paver(device(workers), &p.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
                              r_hat_agg ? r_hat_agg->bytes().data() : nullptr,
                              r_hat_agg ? nullptr : r_hats.data(), &verdict, &err);
     if (rc != POSLO_OK) rethrow(err);

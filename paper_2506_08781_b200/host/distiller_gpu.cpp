@@ -288,27 +288,60 @@ std::vector<bool> ColdCryptoData::sebver(const GroupElement& y,
     if (mode == SebverMode::V) ranges.push_back({0, next_epoch_});
     if (mode == SebverMode::U)
         for (const auto& u : umbrellas_) ranges.push_back({u.index * w, (u.index + 1) * w});
-    for (const auto& [lo, hi] : ranges) collect_epochs(all_msgs, lo, hi);
-    if (mode == SebverMode::I)
-        for (const auto& rec : invalid_) {
-            const uint32_t i = scheme_ == CcdScheme::Coarse ? rec.index : rec.index / suite_.n2;
-            auto it = all_msgs.find(i);
-            if (it == all_msgs.end() || (scheme_ == CcdScheme::Fine && it->second.size() <= rec.index % suite_.n2))
-                throw FormatError(scheme_ == CcdScheme::Coarse ? "messages for invalid epoch missing"
-                                                               : "message for invalid entry missing");
-        }
     Bytes dsw;
     ds_.serialize(dsw);
     poslo_error err{};
     if (scheme_ == CcdScheme::Coarse) {
-        // the device verifier takes epochs 0..next-1 and every record at once
+        // groups in the reference's order: each reads its epochs (collect_epochs or the
+        // mode-I lookup) and hashes the non-invalid ones (verify_range, :161-162). The
+        // reference raises at the first group with missing messages, after hashing
+        // every group before it; the device hashes exactly those epochs (seeds are
+        // derived for no other epoch), then the missing-message error is raised.
+        std::set<uint32_t> bad_ep;
+        for (const auto& rec : invalid_) bad_ep.insert(rec.index);
+        std::set<uint32_t> hashed;
+        size_t live = mode == SebverMode::I ? invalid_.size() : ranges.size();
+        std::string missing;
+        auto read_ok = [&](uint32_t i, bool need_n2) -> bool {
+            auto it = all_msgs.find(i);
+            if (it == all_msgs.end()) {
+                missing = mode == SebverMode::I ? "messages for invalid epoch missing"
+                                                : "messages for epoch " + std::to_string(i) + " missing";
+                return false;
+            }
+            if (need_n2 && it->second.size() != suite_.n2) {
+                missing = "epoch batch size mismatch";
+                return false;
+            }
+            return true;
+        };
+        if (mode == SebverMode::I) {
+            for (size_t k = 0; k < invalid_.size(); k++) {
+                if (!read_ok(invalid_[k].index, false)) {
+                    live = k;
+                    break;
+                }
+                hashed.insert(invalid_[k].index);
+            }
+        } else {
+            for (size_t k = 0; k < ranges.size(); k++) {
+                bool ok = true;
+                for (uint32_t i = ranges[k].first; i < std::min(ranges[k].second, next_epoch_) && ok; i++)
+                    ok = read_ok(i, true);
+                if (!ok) {
+                    live = k;
+                    break;
+                }
+                for (uint32_t i = ranges[k].first; i < std::min(ranges[k].second, next_epoch_); i++)
+                    if (!bad_ep.count(i)) hashed.insert(i);
+            }
+        }
+        if (!missing.empty() && live == 0) throw FormatError(missing);
         Entries e;
         std::vector<uint32_t> epochs;
         std::vector<uint64_t> starts{0};
-        for (uint32_t i = 0; i < next_epoch_; i++) {
-            auto it = all_msgs.find(i);
-            if (it != all_msgs.end())
-                for (const auto& m : it->second) e.add(m);
+        for (uint32_t i : hashed) {
+            for (const auto& m : all_msgs.at(i)) e.add(m);
             epochs.push_back(i);
             starts.push_back(e.n());
         }
@@ -321,18 +354,21 @@ std::vector<bool> ColdCryptoData::sebver(const GroupElement& y,
         b.n_entries = e.n();
         b.epochs = epochs.data();
         b.epoch_starts = starts.data();
-        b.n_epochs = next_epoch_;
+        b.n_epochs = static_cast<uint32_t>(epochs.size());
         b.ds = dsw.data();
         b.ds_len = static_cast<uint32_t>(dsw.size());
         b.ds_capacity = suite_.depth();
         std::vector<uint32_t> inv, ui;
         std::vector<uint8_t> is, ir, us, ur;
-        for (const auto& rec : invalid_) {
+        for (size_t k = 0; k < invalid_.size(); k++) {
+            const auto& rec = invalid_[k];
+            if (mode == SebverMode::I && k >= live) break;
             inv.push_back(rec.index);
             append(is, rec.sig.s.le_bytes().data(), kScalarBytes);
             append(ir, rec.sig.r.bytes().data(), kPointBytes);
         }
-        for (const auto& u : umbrellas_) {
+        for (size_t k = 0; k < umbrellas_.size() && (mode != SebverMode::U || k < live); k++) {
+            const auto& u = umbrellas_[k];
             ui.push_back(u.index);
             append(us, u.sig.s.le_bytes().data(), kScalarBytes);
             append(ur, u.sig.r.bytes().data(), kPointBytes);
@@ -346,12 +382,21 @@ std::vector<bool> ColdCryptoData::sebver(const GroupElement& y,
                                us.data(), ur.data(), want_u ? static_cast<uint32_t>(ui.size()) : 0,
                                want_u ? ubits.data() : nullptr, want_i ? ibits.data() : nullptr, &err),
               err);
+        if (!missing.empty()) throw FormatError(missing);
         if (want_v) return {vbit != 0};
         std::vector<bool> bits;
         const size_t n = want_u ? ui.size() : inv.size();
         for (size_t k = 0; k < n; k++) bits.push_back((want_u ? ubits[k] : ibits[k]) != 0);
         return bits;
     }
+    // fine scheme: the reads of collect_epochs / the mode-I lookup, in order
+    for (const auto& [lo, hi] : ranges) collect_epochs(all_msgs, lo, hi);
+    if (mode == SebverMode::I)
+        for (const auto& rec : invalid_) {
+            auto it = all_msgs.find(rec.index / suite_.n2);
+            if (it == all_msgs.end() || it->second.size() <= rec.index % suite_.n2)
+                throw FormatError("message for invalid entry missing");
+        }
     // fine scheme: entry scalars from the disclosed stack, on the device
     std::set<uint32_t> bad;
     for (const auto& rec : invalid_) bad.insert(rec.index);

@@ -1,24 +1,36 @@
-"""Multi-GPU sharding of the batch verifier.
+"""Multi-rank sharding of the batch verifier: one process per
+GPU, torch.distributed for the plumbing (NCCL over NVLink on the box; gloo
+works too, e.g. several ranks sharing one device in tests).
 
-One process per GPU. The log is sharded by contiguous, epoch-aligned entry
-ranges; each rank runs stages 0-2 on its own epochs and produces a partial
-e-hat (32 bytes). Coarse mode needs ONE exchange: an all-gather of the
-partials (NCCL over NVLink on the box; any torch.distributed backend works),
-then a rank-ordered fold mod l and a single group check. NCCL all-reduce is
-never used: there is no mod-l reduction operator and limb-wise sums drop
-carries. Per-epoch verdicts need no exchange except gathering the verdict
-bits to rank 0.
-
-`backend` is anything with agg_ekeys_packed / scalar_sum / group_check: the
-Verifier (device) in production; tests/test_multi_gloo.py drives the same
-host logic on CPU with world_size 2 over gloo.
+The log is sharded by contiguous, epoch-aligned entry ranges (rank r owns
+epochs shard_range(n1, world, r)); each rank hashes and checks its own epochs
+on its GPU. The only data exchanges are the ones SURVEY §8e names:
+  coarse PAVer   the 32-byte partial e-hat of every rank, all-gathered straight
+                 from device memory, folded mod l in rank order and checked
+                 once on rank 0 (batch_verify.cpp:83-86);
+  per-epoch      verdict bytes gathered to every rank in epoch order;
+  distillation   verdicts -> the ascending invalid-epoch list; umbrella pieces
+                 (sum of valid s-hat, e~ and the R-hat fold) of umbrellas a
+                 shard cut splits, folded in rank order on rank 0
+                 (distiller.cpp:45-53, 82-88), then one check per umbrella
+                 (SeBVer mode U, :156-179).
+NCCL all-reduce is never used: there is no mod-l operator and limb-wise sums
+drop carries. Before every exchange of results the ranks exchange a status
+record, so an error on one rank (SeedNotDisclosed, FormatError, ...) is
+raised on every rank — the lowest failing rank's error, i.e. the lowest
+epoch's — instead of leaving the others blocked in a collective.
 """
 from __future__ import annotations
 
-from typing import Sequence, Tuple
+import ctypes
+import struct
+from typing import Dict, List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import api
 
 
 def shard_range(n_epochs: int, world: int, rank: int) -> Tuple[int, int]:
@@ -51,11 +63,12 @@ def _device_for(group):
     return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
 
 
-def all_gather_bytes(blob: bytes, group=None) -> list:
+def all_gather_bytes(blob: bytes, group=None) -> List[bytes]:
     """All-gather one fixed-size byte string per rank, returned in rank order."""
     world = dist.get_world_size(group)
     dev = _device_for(group)
-    t = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    t = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev) if blob else torch.zeros(0, dtype=torch.uint8,
+                                                                                              device=dev)
     out = torch.empty(world * len(blob), dtype=torch.uint8, device=dev)
     dist.all_gather_into_tensor(out, t, group=group)
     raw = out.cpu().numpy().tobytes()
@@ -63,31 +76,178 @@ def all_gather_bytes(blob: bytes, group=None) -> list:
     return [raw[r * n:(r + 1) * n] for r in range(world)]
 
 
-def sharded_paver(backend, packed_shard, y: bytes, s_hat: bytes, r_hat: bytes, group=None) -> bool:
-    """Coarse PAVer over a sharded log: every rank passes ITS shard; all ranks
-    return the same verdict (broadcast from rank 0)."""
-    _, e_part = backend.agg_ekeys_packed(packed_shard)
-    parts = all_gather_bytes(e_part, group)
-    verdict = torch.zeros(1, dtype=torch.uint8, device=_device_for(group))
-    if dist.get_rank(group) == 0:
-        e_hat = backend.scalar_sum(parts)          # rank-ordered fold mod l on the device
-        verdict[0] = int(backend.group_check(y, [e_hat], [s_hat], [r_hat])[0])
-    dist.broadcast(verdict, src=0, group=group)
-    return bool(verdict.item())
+def all_gather_var(blob: bytes, group=None) -> List[bytes]:
+    """All-gather byte strings of differing lengths (padded to the longest)."""
+    sizes = [struct.unpack("<Q", x)[0] for x in all_gather_bytes(struct.pack("<Q", len(blob)), group)]
+    width = max(sizes) if sizes else 0
+    parts = all_gather_bytes(blob + bytes(width - len(blob)), group) if width else [b""] * len(sizes)
+    return [p[:s] for p, s in zip(parts, sizes)]
 
 
-def sharded_epoch_verdicts(backend, pk, shard_batches, s_hats, ds, group=None) -> list:
-    """Per-epoch verdicts: each rank checks its own epochs; verdict bits are
-    gathered to every rank in epoch order (ranks hold ascending shards)."""
-    local = backend.epoch_verify(pk, shard_batches, s_hats, ds)
-    world = dist.get_world_size(group)
-    n = torch.tensor([len(local)], dtype=torch.int64, device=_device_for(group))
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    width = int(max(s.item() for s in sizes))
-    blob = bytes(int(x) for x in local) + bytes(width - len(local))
-    parts = all_gather_bytes(blob, group)
-    out = []
-    for r, p in enumerate(parts):
-        out += [bool(b) for b in p[:int(sizes[r].item())]]
-    return out
+# ---------------------------------------------------------------- error agreement
+_KIND = {api.FormatError: 1, api.StateError: 2, api.SeedNotDisclosed: 3, ValueError: 5}
+
+
+def _status(exc: Optional[BaseException]) -> bytes:
+    if exc is None:
+        return bytes(128)
+    kind = next((k for cls, k in _KIND.items() if isinstance(exc, cls)), 4)
+    epoch = int(getattr(exc, "epoch", 0) or 0)
+    msg = str(exc).encode(errors="replace")[:119]
+    return struct.pack("<BI", kind, epoch & 0xFFFFFFFF) + bytes([len(msg)]) + msg + bytes(122 - len(msg))
+
+
+def agree(exc: Optional[BaseException], group=None):
+    """Every rank contributes its status; if any rank failed, every rank raises
+    the lowest failing rank's error (ranks hold ascending epochs)."""
+    recs = all_gather_bytes(_status(exc), group)
+    for r, rec in enumerate(recs):
+        kind = rec[0]
+        if not kind:
+            continue
+        if r == dist.get_rank(group) and exc is not None:
+            raise exc
+        epoch = struct.unpack("<I", rec[1:5])[0]
+        msg = rec[6:6 + rec[5]].decode(errors="replace")
+        if kind == 3:
+            raise api.SeedNotDisclosed(epoch)
+        cls = {1: api.FormatError, 2: api.StateError, 5: ValueError}.get(kind, api.DeviceError)
+        e = cls(f"rank {r}: {msg}")
+        e.epoch = epoch
+        raise e
+
+
+def _guard(fn):
+    try:
+        return fn(), None
+    except (api.FormatError, api.StateError, api.SeedNotDisclosed, api.DeviceError, ValueError) as e:
+        return None, e
+
+
+def _root(group) -> int:
+    return dist.get_global_rank(group, 0) if group is not None else 0
+
+
+# ---------------------------------------------------------------- coarse PAVer
+class ShardedPaver:
+    """Coarse PAVer over a sharded log: partial e-hat into device memory, an
+    all-gather of the partials (NCCL: device to device, no host hop), the
+    rank-ordered fold mod l and ONE check on rank 0, whose verdict every rank
+    receives. Buffers are allocated once and reused across steps."""
+
+    def __init__(self, v: api.Verifier, group=None):
+        self.v, self.group = v, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.part = torch.zeros(32, dtype=torch.uint8, device=dev)
+        self.parts = torch.zeros(32 * self.world, dtype=torch.uint8, device=dev if self.nccl else "cpu")
+        self.flag = torch.zeros(1, dtype=torch.uint8, device=dev if self.nccl else "cpu")
+        self.status = torch.zeros(self.world, dtype=torch.uint8, device=dev if self.nccl else "cpu")
+
+    def __call__(self, cb, y: bytes, s_hat: bytes, r_hat: bytes) -> bool:
+        _, exc = _guard(lambda: self.v.agg_ekeys_partial(cb, self.part.data_ptr()))
+        # one status byte per rank; the full error record only when someone failed
+        self.flag[0] = 0 if exc is None else 1
+        dist.all_gather_into_tensor(self.status, self.flag, group=self.group)
+        if int(self.status.max().item()):
+            agree(exc, self.group)
+        if self.nccl:
+            dist.all_gather_into_tensor(self.parts, self.part, group=self.group)
+        else:
+            dist.all_gather_into_tensor(self.parts, self.part.cpu(), group=self.group)
+        ok, exc = None, None
+        if self.rank == 0:
+            if self.nccl:
+                ok, exc = _guard(lambda: self.v.combine_check(self.parts.data_ptr(), y, s_hat, r_hat,
+                                                              n_parts=self.world))
+            else:
+                ok, exc = _guard(lambda: self.v.combine_check(self.parts.numpy().tobytes(), y, s_hat, r_hat))
+        self.flag[0] = (2 if exc is not None else (1 if ok else 0)) if self.rank == 0 else 0
+        dist.broadcast(self.flag, src=_root(self.group), group=self.group)
+        res = int(self.flag.item())
+        if res == 2:
+            agree(exc if self.rank == 0 else None, self.group)
+        return res == 1
+
+
+def sharded_paver(v: api.Verifier, cb, y: bytes, s_hat: bytes, r_hat: bytes, group=None) -> bool:
+    """One-shot form of ShardedPaver: every rank passes ITS shard's batch."""
+    return ShardedPaver(v, group)(cb, y, s_hat, r_hat)
+
+
+def sharded_e_tilde(v: api.Verifier, cb, group=None) -> List[bytes]:
+    """agg_ekeys over a sharded log: every rank gets every e~ in epoch order."""
+    n = cb.n_epochs
+    out = ctypes.create_string_buffer(max(n, 1) * 32)
+    _, exc = _guard(lambda: v._call(v._lib.poslo_gpu_agg_ekeys, ctypes.byref(cb), out, None))
+    agree(exc, group)
+    raw = b"".join(all_gather_var(out.raw[:32 * n], group))
+    return [raw[32 * k:32 * k + 32] for k in range(len(raw) // 32)]
+
+
+# ---------------------------------------------------------------- per-epoch verdicts
+def sharded_epoch_verdicts(v: api.Verifier, cb, y: bytes, s_hats, r_hats, group=None) -> bytes:
+    """Per-epoch verdicts: each rank checks its own epochs (no exchange) and the
+    verdict bytes are gathered to every rank in epoch order. s_hats / r_hats:
+    host bytes, or device pointers for a device-resident batch."""
+    n = cb.n_epochs
+    verd = ctypes.create_string_buffer(max(n, 1))
+    args = [ctypes.c_void_p(x) if isinstance(x, int) else api._buf(x) for x in (s_hats, r_hats)]
+    _, exc = _guard(lambda: v._call(v._lib.poslo_gpu_epoch_verify, ctypes.byref(cb), api._buf(y), *args, verd,
+                                    None))
+    agree(exc, group)
+    return b"".join(all_gather_var(verd.raw[:n], group))
+
+
+# ---------------------------------------------------------------- distillation
+def umbrella_cuts(first_epoch: int, n_epochs: int, w: int) -> List[int]:
+    """Batch positions where this shard's epochs cross an umbrella boundary."""
+    return [0] + [k for k in range(1, n_epochs) if (first_epoch + k) % w == 0] + [n_epochs]
+
+
+def sharded_distill(v: api.Verifier, cb, first_epoch: int, y: bytes, s_hats, r_hats, w: int, group=None,
+                    check_umbrellas: bool = True) -> Optional[Dict]:
+    """Coarse distillation of a sharded log (distill_epoch over every epoch,
+    distiller.cpp:60-89): on rank 0 returns {"verdicts": bytes (epoch order),
+    "invalid": ascending invalid epochs, "umbrellas": [(u, s, R, e)] with the
+    valid epochs of umbrella u folded across shards, "u_bits": SeBVer mode U
+    (one commit_check per umbrella)}; None on other ranks."""
+    n = cb.n_epochs
+    cuts = umbrella_cuts(first_epoch, n, w)
+    seg = np.array(cuts, dtype=np.uint32)
+    ng = len(cuts) - 1
+    verd = ctypes.create_string_buffer(max(n, 1))
+    out_s, out_r, out_e = (ctypes.create_string_buffer(max(ng, 1) * 32) for _ in range(3))
+    args = [ctypes.c_void_p(x) if isinstance(x, int) else api._buf(x) for x in (s_hats, r_hats)]
+    _, exc = _guard(lambda: v._call(v._lib.poslo_gpu_distill_coarse_ex, ctypes.byref(cb), api._buf(y), *args,
+                                    ctypes.c_void_p(seg.ctypes.data), ng, verd, out_s, out_r, out_e))
+    agree(exc, group)
+    # pieces: (umbrella index, s, R, e) of this shard, in epoch order
+    pieces = b"".join(struct.pack("<I", (first_epoch + cuts[g]) // w) + out_s.raw[32 * g:32 * g + 32] +
+                      out_r.raw[32 * g:32 * g + 32] + out_e.raw[32 * g:32 * g + 32] for g in range(ng))
+    verd_all = all_gather_var(verd.raw[:n], group)
+    piece_all = all_gather_var(pieces, group)
+    if dist.get_rank(group) != 0:
+        return None
+    verdicts = b"".join(verd_all)
+    invalid = [first_epoch + i for i, x in enumerate(verdicts) if not x]  # rank 0 holds the first shard
+    # fold the pieces of each umbrella in rank order (one segmented fold on the device)
+    recs = [(struct.unpack("<I", p[k:k + 4])[0], p[k + 4:k + 36], p[k + 36:k + 68], p[k + 68:k + 100])
+            for p in piece_all for k in range(0, len(p), 100)]
+    us = sorted({u for u, _, _, _ in recs})
+    bounds, sc, pt, es = [0], [], [], []
+    for u in us:
+        for uu, s_, r_, e_ in recs:
+            if uu == u:
+                sc.append(s_)
+                pt.append(r_)
+                es.append(e_)
+        bounds.append(len(sc))
+    folded = v.segfold(sc, pt, None, bounds)
+    efold = v.segfold(es, [], None, bounds)
+    umbrellas = [(u, folded[k][0], folded[k][1], efold[k][0]) for k, u in enumerate(us)]
+    u_bits = v.group_check(y, [e for _, _, _, e in umbrellas], [s for _, s, _, _ in umbrellas],
+                           [r for _, _, r, _ in umbrellas]) if (check_umbrellas and umbrellas) else []
+    return {"verdicts": verdicts, "invalid": invalid, "umbrellas": umbrellas, "u_bits": u_bits}
