@@ -516,10 +516,12 @@ class Verifier:
 
     # -- SeBVer over a coarse CCD (distiller.cpp:181-233)
     def sebver(self, y: bytes, suite: SuiteConfig, all_msgs, ds: SeedStack, epochs_distilled: int,
-               invalid: Sequence, umbrellas: Sequence, valid=None, hashed: Optional[Sequence[int]] = None):
+               invalid: Sequence, umbrellas: Sequence, valid=None, hashed: Optional[Sequence[int]] = None,
+               want: str = "VUI"):
         """invalid: [(epoch, s_le, r)], umbrellas: [(u, s_le, r)], valid: (s_le, r) or None.
         hashed: the epochs to hash (default: every distilled epoch); the C-ABI derives
-        seeds and hashes only those. Returns dict with keys V (list, only when valid given), U, I."""
+        seeds and hashes only those. want: the modes to evaluate. Returns dict with
+        keys V (list, only when valid given), U, I."""
         eps = range(epochs_distilled) if hashed is None else hashed
         batches = {i: all_msgs[i] for i in eps}
         pb = PackedBatch(suite.suite, suite.n2, batches, ds)
@@ -537,8 +539,9 @@ class Verifier:
                    inv.ctypes.data if len(inv) else None, _buf(inv_s) if inv_s else None,
                    _buf(inv_r) if inv_r else None, len(invalid),
                    _buf(valid[0]) if valid else None, _buf(valid[1]) if valid else None,
-                   ctypes.byref(vbit) if valid else None, ui.ctypes.data if len(ui) else None,
-                   _buf(us) if us else None, _buf(ur) if ur else None, len(umbrellas), ubits, ibits)
+                   ctypes.byref(vbit) if (valid and "V" in want) else None, ui.ctypes.data if len(ui) else None,
+                   _buf(us) if us else None, _buf(ur) if ur else None, len(umbrellas),
+                   ubits if "U" in want else None, ibits if "I" in want else None)
         ub, ib = ubits.raw, ibits.raw
         res = {"U": [bool(ub[k]) for k in range(len(umbrellas))],
                "I": [bool(ib[k]) for k in range(len(invalid))]}

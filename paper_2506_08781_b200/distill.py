@@ -247,7 +247,7 @@ class ColdCryptoData:
         res = self.v.sebver(y, self.suite, all_msgs, self.ds, self.next_epoch,
                             self.invalid[:live] if mode == "I" else self.invalid,
                             self.umbrellas[:live] if mode == "U" else [],
-                            self.valid_ if mode == "V" else None, hashed=sorted(hashed))
+                            self.valid_ if mode == "V" else None, hashed=sorted(hashed), want=mode)
         if missing is not None:
             raise missing
         return res[mode]

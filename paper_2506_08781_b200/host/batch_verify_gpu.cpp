@@ -16,8 +16,14 @@
 // pulls the entries chunk by chunk through poslo_batch.fill, and each chunk is
 // gathered into pinned staging by all host cores (a persistent worker pool)
 // while the previous chunks are copied to the device and hashed.
+#if defined(__SSE2__)
+#include <immintrin.h>
+#endif
+
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -187,16 +193,45 @@ struct Packed {
     std::vector<uint64_t> offsets;  // n_entries + 1 byte offsets (variable lengths only)
     bool fixed = true, uniform = true;
     uint32_t len0 = 0;
+    std::atomic<bool> mismatch{false};  // gather met an entry of another length (fixed layout assumed)
     Bytes ds;
     poslo_batch b{};
 };
 
 uint64_t byte_at(const Packed& p, uint64_t t) { return p.fixed ? t * p.len0 : p.offsets[t]; }
 
+// Fixed-length copy of entries [t0, t1) of one epoch; L a compile-time
+// constant for the common sizes (inlined moves), the data of later entries
+// prefetched (their heap blocks are scattered); false on a length mismatch.
+// The staging writes are non-temporal: the chunk goes to the device by DMA,
+// never back through this core's caches (no read-for-ownership of dst).
+template <uint32_t L>
+bool copy_fixed(const std::vector<Bytes>& ms, uint64_t s0, uint64_t t0, uint64_t t1, uint8_t* d, uint32_t len) {
+    const uint32_t n = L ? L : len;
+    constexpr uint64_t kAhead = 8;
+    for (uint64_t t = t0; t < t1; t++, d += n) {
+        if (t + kAhead < t1) __builtin_prefetch(ms[t + kAhead - s0].data());
+        const Bytes& m = ms[t - s0];
+        if (m.size() != n) return false;
+#if defined(__SSE2__)
+        if constexpr (L != 0 && L % 16 == 0) {
+            if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+                const __m128i* src = reinterpret_cast<const __m128i*>(m.data());
+                __m128i* dd = reinterpret_cast<__m128i*>(d);
+                for (uint32_t q = 0; q < L / 16; q++) _mm_stream_si128(dd + q, _mm_loadu_si128(src + q));
+                continue;
+            }
+        }
+#endif
+        std::memcpy(d, m.data(), L ? L : len);
+    }
+    return true;
+}
+
 // poslo_batch.fill: entries [first, first + count) back to back into dst,
 // epochs spread over the host cores.
 int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
-    const Packed& p = *static_cast<const Packed*>(user);
+    Packed& p = *static_cast<Packed*>(user);
     const uint64_t last = first + count;
     const int64_t k0 = std::upper_bound(p.starts.begin(), p.starts.end(), first) - p.starts.begin() - 1;
     const int64_t k1 = std::lower_bound(p.starts.begin(), p.starts.end(), last) - p.starts.begin();
@@ -209,7 +244,13 @@ int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
             const uint64_t t0 = std::max(s0, first), t1 = std::min(p.starts[k + 1], last);
             if (p.fixed) {
                 uint8_t* d = dst + (t0 * p.len0 - base);
-                for (uint64_t t = t0; t < t1; t++, d += p.len0) std::memcpy(d, ms[t - s0].data(), p.len0);
+                const bool ok = p.len0 == 32   ? copy_fixed<32>(ms, s0, t0, t1, d, 32)
+                                : p.len0 == 64 ? copy_fixed<64>(ms, s0, t0, t1, d, 64)
+                                               : copy_fixed<0>(ms, s0, t0, t1, d, p.len0);
+                if (!ok) p.mismatch.store(true, std::memory_order_relaxed);
+#if defined(__SSE2__)
+                _mm_sfence();  // the streaming stores are visible before the DMA reads the slot
+#endif
             } else {
                 for (uint64_t t = t0; t < t1; t++) {
                     const Bytes& m = ms[t - s0];
@@ -218,11 +259,14 @@ int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
             }
         }
     });
-    return 0;
+    return p.mismatch.load() ? 1 : 0;  // a mismatch aborts the call; the caller re-packs with offsets
 }
 
+// fixed_guess: assume one entry length (checked entry by entry while the
+// chunks are gathered, so the common case reads each entry header once);
+// false: the sizing pass computes byte offsets for mixed lengths.
 void pack(const SuiteConfig& suite, const std::map<uint32_t, std::vector<Bytes>>& batches,
-          const SeedStack& ds, Packed& p) {
+          const SeedStack& ds, Packed& p, bool fixed_guess) {
     const size_t ne = batches.size();
     p.msgs.reserve(ne);
     p.epochs.reserve(ne);
@@ -240,14 +284,7 @@ void pack(const SuiteConfig& suite, const std::map<uint32_t, std::vector<Bytes>>
     // sizing pass over the entry headers, in parallel: one length, or offsets
     for (size_t k = 0; k < ne && p.len0 == 0 && n; k++)
         if (!p.msgs[k]->empty()) p.len0 = static_cast<uint32_t>((*p.msgs[k])[0].size());
-    std::atomic<bool> fixed{true};
-    parallel_blocks((int64_t)ne, 256, [&](int64_t a, int64_t z) {
-        bool f = true;
-        for (int64_t k = a; k < z && f; k++)
-            for (const Bytes& m : *p.msgs[k]) f = f && m.size() == p.len0;
-        if (!f) fixed.store(false, std::memory_order_relaxed);
-    });
-    p.fixed = fixed.load();
+    p.fixed = fixed_guess;
     uint64_t total = n * p.len0;
     if (!p.fixed) {
         std::vector<uint64_t> ep_bytes(ne + 1, 0);
@@ -299,10 +336,16 @@ std::vector<EpochKeyAggregate> agg_ekeys(const SuiteConfig& suite,
                                          const SeedStack& ds, unsigned workers) {
     if (workers == 0) throw StateError("worker count must be at least 1");
     Packed p;
-    pack(suite, batches, ds, p);
+    pack(suite, batches, ds, p, true);
     std::vector<uint8_t> et(32 * std::max<size_t>(p.epochs.size(), 1));
     poslo_error err{};
-    if (poslo_gpu_agg_ekeys(device(workers), &p.b, et.data(), nullptr, &err) != POSLO_OK) rethrow(err);
+    int rc = poslo_gpu_agg_ekeys(device(workers), &p.b, et.data(), nullptr, &err);
+    if (rc != POSLO_OK && p.mismatch.load()) {  // mixed entry lengths: again with byte offsets
+        Packed q;
+        pack(suite, batches, ds, q, false);
+        rc = poslo_gpu_agg_ekeys(device(workers), &q.b, et.data(), nullptr, &err);
+    }
+    if (rc != POSLO_OK) rethrow(err);
     std::vector<EpochKeyAggregate> out(p.epochs.size());
     for (size_t k = 0; k < p.epochs.size(); k++)
         out[k] = EpochKeyAggregate{p.epochs[k], Scalar::from_canonical_le(et.data() + 32 * k)};
@@ -328,13 +371,20 @@ bool paver(const PoslocPublicKey& pk, const std::map<uint32_t, std::vector<Bytes
         }
     }
     if (workers == 0) throw StateError("worker count must be at least 1");
-    Packed p;
-    pack(pk.suite, batches, ds, p);
     uint8_t verdict = 0;
     poslo_error err{};
-    int rc = poslo_gpu_paver(device(workers), &p.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
-                             r_hat_agg ? r_hat_agg->bytes().data() : nullptr,
-                             r_hat_agg ? nullptr : r_hats.data(), &verdict, &err);
+    auto run = [&](bool fixed_guess, Packed& p) {
+        pack(pk.suite, batches, ds, p, fixed_guess);
+        return poslo_gpu_paver(device(workers), &p.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
+                               r_hat_agg ? r_hat_agg->bytes().data() : nullptr, r_hat_agg ? nullptr : r_hats.data(),
+                               &verdict, &err);
+    };
+    Packed p;
+    int rc = run(true, p);
+    if (rc != POSLO_OK && p.mismatch.load()) {  // mixed entry lengths: again with byte offsets
+        Packed q;
+        rc = run(false, q);
+    }
     if (rc != POSLO_OK) rethrow(err);
     return verdict != 0;
 }

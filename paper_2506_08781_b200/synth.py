@@ -86,8 +86,9 @@ class SignedLog:
         b.suite, b.n2 = self.suite, self.n2
         b.payload = payload_ptr if payload_ptr is not None else self.log.data_ptr()
         b.payload_bytes = self.payload_bytes
-        if self.offsets is not None:
-            b.offsets = offsets_ptr if offsets_ptr is not None else self.offsets.data_ptr()
+        if self.offsets is not None:  # device offsets for a device batch, else the host copy
+            b.offsets = offsets_ptr if offsets_ptr is not None else (
+                self.offsets.data_ptr() if device_resident else self.offsets_host.ctypes.data)
         else:
             b.offsets = None
         b.entry_len, b.n_entries = self.entry_len, self.n

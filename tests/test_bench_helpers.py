@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_synth_varlen_numpy_port_matches_c():
-    import bench
+    from paper_2506_08781_b200 import synth as bench
     src = ('#include "poslo_synth.h"\n'
            'uint32_t vl(uint64_t s, uint64_t k) { return poslo_synth_varlen(s, k); }\n'
            'uint8_t ab(uint64_t s, uint64_t k, uint32_t b) { return poslo_synth_ascii(s, k, b); }\n')

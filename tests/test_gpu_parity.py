@@ -427,7 +427,7 @@ def test_chunked_varlen_host_path_matches_device_resident(verifier):
     import ctypes
 
     import torch
-    import bench
+    from paper_2506_08781_b200 import synth as bench
     from paper_2506_08781_b200 import _native as N
     api = A()
     n2, n = 1024, 1 << 18  # ~143 MB of syslog-style entries: > 2 chunks

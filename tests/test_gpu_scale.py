@@ -32,7 +32,7 @@ def _run(verifier, log2n, n2, varlen, samples, seed):
     err = N.PosloError()
     offs_dev = None
     if varlen:
-        import bench
+        from paper_2506_08781_b200 import synth as bench
         lens = bench.synth_varlen(seed, 0, n)
         offs = np.zeros(n + 1, dtype=np.uint64)
         np.cumsum(lens, out=offs[1:])

@@ -7,7 +7,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-import bench  # noqa: E402
+from paper_2506_08781_b200 import synth as bench  # noqa: E402
 from paper_2506_08781_b200 import _native as N  # noqa: E402
 from paper_2506_08781_b200 import api  # noqa: E402
 
