@@ -184,10 +184,10 @@ struct Prepared {
     const uint32_t* sum_src = nullptr;  // what e-hat sums: e~ (8 limbs) or raw epoch sums (17 limbs)
     int sum_limbs = 8;
     // Pipelining hook: when set (and the log is device-resident), the hash is
-    // launched in epoch pieces and on_piece(e0, e1) runs after each piece's
-    // e~ are final on the stream, so the caller can start its per-epoch
+    // launched in epoch pieces and on_piece(e0, e1, st) runs after each piece's
+    // e~ are final on stream st, so the caller can start its per-epoch
     // checks for that piece while the next one hashes.
-    std::function<int(uint32_t, uint32_t)> on_piece;
+    std::function<int(uint32_t, uint32_t, cudaStream_t)> on_piece;
 };
 
 // Entries per tile of the generic / variable-length kernels (<= 1024, the
@@ -490,16 +490,16 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         P.sum_src = d_partial;
         P.sum_limbs = 17;
     }
-    auto launch_hash = [&](const TileMap& t) {
+    auto launch_hash = [&](const TileMap& t, cudaStream_t hs) {
         if (P.fast) {
             if (b->suite == 1)
-                launch_hash_s1_l32(P.lay, t, d_x0, d_partial, P.d_etilde, s);
+                launch_hash_s1_l32(P.lay, t, d_x0, d_partial, P.d_etilde, hs);
             else
-                launch_hash_s2_l32(P.lay, t, d_x0, d_partial, P.d_etilde, ctx->d_t0, s);
+                launch_hash_s2_l32(P.lay, t, d_x0, d_partial, P.d_etilde, ctx->d_t0, hs);
         } else if (b->suite == 1) {
-            launch_hash_s1_var(P.lay, t, d_x0, d_partial, s);
+            launch_hash_s1_var(P.lay, t, d_x0, d_partial, hs);
         } else {
-            launch_hash_generic(b->suite, P.lay, t, d_x0, d_partial, nullptr, d_err, ctx->d_t0, s);
+            launch_hash_generic(b->suite, P.lay, t, d_x0, d_partial, nullptr, d_err, ctx->d_t0, hs);
         }
         ctx->launches += 1;
     };
@@ -550,7 +550,7 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
                 TileMap t = tm;
                 t.tile_begin = e_done * tm.tiles_per_epoch;
                 t.tile_count = (e_ready - e_done) * tm.tiles_per_epoch;
-                launch_hash(t);
+                launch_hash(t, s);
                 e_done = e_ready;
             }
         }
@@ -624,28 +624,39 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             TileMap t = tm;
             t.tile_begin = e0 * tm.tiles_per_epoch;
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
-            if (t.tile_count) launch_hash(t);
+            if (t.tile_count) launch_hash(t, s);
         }
     } else if (tm.n_tiles && P.on_piece && need_finalize && tm.tiles == nullptr && pipe_pieces() > 1 &&
                n_ep >= 2 * pipe_pieces() && tm.n_tiles >= 2 * kPipeMinTiles) {
         // device-resident, uniform: epoch pieces, each finalised and handed to the caller;
         // every piece keeps >= kPipeMinTiles CTAs so no piece runs the GPU part-full
+        // Pieces alternate between the context stream and hash2, so piece q+1's
+        // CTAs fill the SMs while piece q drains (a single stream would idle the
+        // tail wave of every piece at the kernel boundary).
         const uint32_t pieces = std::min<uint32_t>(pipe_pieces(), tm.n_tiles / kPipeMinTiles);
+        cudaStream_t hs[2] = {s, ctx->hash2};
+        CU(cudaEventRecord(ctx->ev_hash[0], s));
+        CU(cudaStreamWaitEvent(ctx->hash2, ctx->ev_hash[0], 0));
         for (uint32_t q = 0; q < pieces; q++) {
             const uint32_t e0 = (uint32_t)((uint64_t)n_ep * q / pieces);
             const uint32_t e1 = (uint32_t)((uint64_t)n_ep * (q + 1) / pieces);
             TileMap t = tm;
             t.tile_begin = e0 * tm.tiles_per_epoch;
             t.tile_count = (e1 - e0) * tm.tiles_per_epoch;
-            if (t.tile_count) launch_hash(t);
-            launch_epoch_finalize_range(tm, e0, e1, d_partial, P.d_etilde, s);
+            if (t.tile_count) launch_hash(t, hs[q & 1]);
+            launch_epoch_finalize_range(tm, e0, e1, d_partial, P.d_etilde, hs[q & 1]);
             ctx->launches += 1;
-            int rc2 = P.on_piece(e0, e1);
-            if (rc2) return rc2;
+            int rc2 = P.on_piece(e0, e1, hs[q & 1]);
+            if (rc2) {
+                cudaStreamSynchronize(ctx->hash2);
+                return rc2;
+            }
         }
+        CU(cudaEventRecord(ctx->ev_hash[1], ctx->hash2));
+        CU(cudaStreamWaitEvent(s, ctx->ev_hash[1], 0));
         need_finalize = false;
     } else if (tm.n_tiles) {
-        launch_hash(tm);
+        launch_hash(tm, s);
     }
     mark(ctx, kEvFin);
     if (need_finalize && n_ep) {
@@ -936,8 +947,11 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
     ctx->stream = ctx->own;
     e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->hash2, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; i++)
         e = cudaEventCreateWithFlags(&ctx->ev_side[i], cudaEventDisableTiming);
+    for (int i = 0; i < 2 && e == cudaSuccess; i++)
+        e = cudaEventCreateWithFlags(&ctx->ev_hash[i], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         poslo_gpu_destroy(ctx);
         return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
@@ -1028,7 +1042,10 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
     for (auto& ev : ctx->chunk_ev) cudaEventDestroy(ev);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->hash2) cudaStreamDestroy(ctx->hash2);
     for (auto& ev : ctx->ev_side)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : ctx->ev_hash)
         if (ev) cudaEventDestroy(ev);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
@@ -1420,8 +1437,8 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     bool piped = false;
     if (split && b->device_resident) {  // checks of piece q overlap the hashing of piece q + 1
         ENSURE(b_verdict, n, d_vpipe);
-        P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
-            CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+        P.on_piece = [&](uint32_t e0, uint32_t e1, cudaStream_t hs) -> int {
+            CU(cudaEventRecord(ctx->ev_side[0], hs));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));  // side: after the decode, then this piece
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
                           d_r + 32 * (size_t)e0,
@@ -1582,8 +1599,8 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
     ENSURE(b_verdict, std::max<uint32_t>(n, 1), d_verdict);
     bool piped = false;
     if (split && b->device_resident) {  // checks of piece q overlap the hashing of piece q + 1
-        P.on_piece = [&](uint32_t e0, uint32_t e1) -> int {
-            CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+        P.on_piece = [&](uint32_t e0, uint32_t e1, cudaStream_t hs) -> int {
+            CU(cudaEventRecord(ctx->ev_side[0], hs));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
                           d_r + 32 * (size_t)e0,

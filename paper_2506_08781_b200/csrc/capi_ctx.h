@@ -35,6 +35,8 @@ struct poslo_gpu_ctx {
     cudaStream_t copy = nullptr;  // H2D of host-resident logs, overlapped with hashing
     cudaStream_t side = nullptr;  // e-hat-independent part of the group check, overlapped with hashing
     cudaEvent_t ev_side[2] = {};
+    cudaStream_t hash2 = nullptr;  // second hash stream: epoch pieces alternate so one piece's tail
+    cudaEvent_t ev_hash[2] = {};   // overlaps the next piece instead of idling at a kernel boundary
     std::vector<cudaEvent_t> chunk_ev;
     std::mutex mtx;
     uint32_t* d_t0 = nullptr;

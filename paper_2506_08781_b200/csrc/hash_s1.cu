@@ -88,8 +88,10 @@ template <int T, int EPC, int FMA, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restrict__ pay, uint32_t n2,
                                                           uint32_t n_epochs, uint32_t epoch0,
                                                           const uint4* __restrict__ x0,
-                                                          uint32_t* __restrict__ epoch_sum, const PipeK pk) {
+                                                          uint32_t* __restrict__ epoch_sum, const PipeK pk_in) {
     static_assert(T == kLeanStride, "accumulator column stride");
+    const PipeK pk = pk_in;
+    if (FMA == 5) sha_k_smem_init();
     constexpr int TPE = T / EPC;  // threads per epoch (multiple of 32)
     __shared__ uint32_t s_pre[EPC][8], s_x0w[EPC][4];
 #if POSLO_OTS_SPEC

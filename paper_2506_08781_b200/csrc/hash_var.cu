@@ -17,7 +17,7 @@
 #define POSLO_VAR_MINB 6  // min CTAs/SM of k_hash_s1_var (register cap 65536 / (128 x MINB))
 #endif
 #ifndef POSLO_VAR_FMA
-#define POSLO_VAR_FMA 2  // pipe assignment of the SHA rounds (sha256.cuh SHA_RND_SEL)
+#define POSLO_VAR_FMA 5  // pipe assignment of the SHA rounds (sha256.cuh SHA_RND_SEL)
 #endif
 
 namespace poslo_gpu {
@@ -52,32 +52,43 @@ struct VarEntry {
     const uint8_t* m;  // entry bytes
     uint32_t L;
     uint32_t* slot;    // kSlotWords words of shared memory
-    uintptr_t base;    // 16-byte aligned global address of slot word 0 (window start)
 };
 
-__device__ __forceinline__ void stage_window(VarEntry& v, uint32_t b) {
-    const uintptr_t a = (uintptr_t)v.m;
-    const uintptr_t lo = a + 64ull * b - 4;
-    v.base = lo & ~(uintptr_t)15;
+// Per-entry, per-stream constants kept in shared memory (one LDS.128 per
+// block instead of re-deriving them on the ALU pipe every job): the shared
+// address of the stream's word 0 in the slot, the PRMT selector, the index of
+// its last block, and its message length in bits (low word; < 2^32 here).
+struct StreamDesc {
+    uint32_t word_addr, sel, last_b, bits;
+};
+
+// Edge block step (b = 0, or a window reaching past the entry): relative
+// 32-bit arithmetic on m positions. The window of block b covers m positions
+// [64b - d0, 64b - d0 + 96) (d0 = slot byte of m[0] in block 0, 4..19);
+// chunk c is loaded only if it holds a byte of the entry.
+__device__ __forceinline__ void stage_window(const VarEntry& v, uintptr_t base0, uint32_t d0, uint32_t b) {
+    const int r0 = (int)(64 * b) - (int)d0;  // m position of slot byte 0
+    const uint4* src = reinterpret_cast<const uint4*>(base0 + 64ull * b);
     uint4* s4 = reinterpret_cast<uint4*>(v.slot);
 #pragma unroll
     for (int c = 0; c < 6; c++) {
-        const uintptr_t cs = v.base + 16 * c;
+        const int rc = r0 + 16 * c;
         uint4 q = make_uint4(0, 0, 0, 0);
-        if (cs < a + v.L && cs + 16 > a) q = __ldg(reinterpret_cast<const uint4*>(cs));
+        // rc > -16 can only fail for chunk 0 of block 0 (d0 >= 16)
+        if (rc < (int)v.L && (c > 0 || rc > -16)) q = __ldg(src + c);
         s4[c] = q;
     }
-    const int64_t off = (int64_t)(a - v.base);  // slot byte of m position 0 (negative for b > 0)
+    const int off = -r0;  // slot byte of m position 0 (negative for b > 0)
     if (b == 0) reinterpret_cast<uint8_t*>(v.slot)[off - 1] = 0x01;  // tag byte of the second stream
     // Suffix x || 0x80 at m positions L .. L+16. Only those bytes need writing:
     // a chunk holding position >= L+16 starts past L and was not loaded
     // (zero), so the neighbour bytes a loaded chunk carries past the entry
     // all lie in L .. L+14. Five word writes at the suffix start's word
     // alignment, funnel-shifted out of the slot tail E = [0, x0..x3, 0x80, 0].
-    const int64_t sp = off + (int64_t)v.L;  // slot byte of position L
+    const int sp = off + (int)v.L;  // slot byte of position L
     if (sp < 4 * 24 && sp + 17 > 0) {
         const uint32_t c0 = (uint32_t)sp & 3;
-        const int w0 = (int)(sp >> 2);
+        const int w0 = sp >> 2;
         const uint32_t* E = v.slot + 24 + (c0 == 0);
         const uint32_t sh = ((4 - c0) & 3) * 8;
         const uint32_t keep = c0 ? (1u << (8 * c0)) - 1 : 0u;  // bytes of word w0 before position L
@@ -92,19 +103,31 @@ __device__ __forceinline__ void stage_window(VarEntry& v, uint32_t b) {
     }
 }
 
-// Message words of block b of one stream (tag = 0 or 1 prefix bytes).
-__device__ __forceinline__ void load_block(const VarEntry& v, uint32_t b, uint32_t tag, uint32_t W[16]) {
-    const uint32_t d = (uint32_t)((uintptr_t)v.m + 64ull * b - tag - v.base);  // slot byte of word 0
-    const uint32_t r = d & 3;
-    const uint32_t sel = (r + 3) | (r + 2) << 4 | (r + 1) << 8 | r << 12;
-    const uint32_t* s = v.slot + (d >> 2);
-    uint32_t lo = s[0];
+// Interior block step: the whole window lies inside the entry (b >= 1 and
+// 64b + 96 - d0 <= L), so it is six unconditional 16-byte loads at
+// base0 + 64b with nothing to patch (no tag, no suffix).
+__device__ __forceinline__ void stage_interior(const VarEntry& v, uintptr_t base0, uint32_t b) {
+    const uint4* src = reinterpret_cast<const uint4*>(base0 + 64ull * b);
+    uint4* s4 = reinterpret_cast<uint4*>(v.slot);
 #pragma unroll
-    for (int k = 0; k < 16; k++) {
-        const uint32_t hi = s[k + 1];
-        W[k] = __byte_perm(lo, hi, sel);
-        lo = hi;
-    }
+    for (int c = 0; c < 6; c++) s4[c] = __ldg(src + c);
+}
+
+// PRMT selector that funnels bytes r..r+3 of (lo, hi) into one big-endian word
+__device__ __forceinline__ uint32_t prmt_sel(uint32_t r) { return (r + 3) | (r + 2) << 4 | (r + 1) << 8 | r << 12; }
+
+// Message words of one stream's block: slot words from word_addr funnelled
+// by sel. The window of block b starts at base0 + 64b, so a stream's word 0
+// sits at the same slot byte d0 - tag in every block: per-entry constants.
+__device__ __forceinline__ void load_block(uint32_t word_addr, uint32_t sel, uint32_t W[16]) {
+    uint32_t w[17];
+#define POSLO_LDS_W(k) asm volatile("ld.shared.u32 %0, [%1+" #k "];" : "=r"(w[(k) / 4]) : "r"(word_addr))
+    POSLO_LDS_W(0); POSLO_LDS_W(4); POSLO_LDS_W(8); POSLO_LDS_W(12); POSLO_LDS_W(16); POSLO_LDS_W(20);
+    POSLO_LDS_W(24); POSLO_LDS_W(28); POSLO_LDS_W(32); POSLO_LDS_W(36); POSLO_LDS_W(40); POSLO_LDS_W(44);
+    POSLO_LDS_W(48); POSLO_LDS_W(52); POSLO_LDS_W(56); POSLO_LDS_W(60); POSLO_LDS_W(64);
+#undef POSLO_LDS_W
+#pragma unroll
+    for (int k = 0; k < 16; k++) W[k] = __byte_perm(w[k], w[k + 1], sel);
 }
 
 __device__ __forceinline__ void compress_into(uint32_t H[8], uint32_t W[16], const PipeK& pk) {
@@ -138,7 +161,8 @@ PD void smem_acc9_add8v(uint32_t* s, int stride, const uint32_t v[8]) {
 
 __global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayout lay, TileMap tm,
                                                           const uint4* __restrict__ x0,
-                                                          uint32_t* __restrict__ partial, const PipeK pk) {
+                                                          uint32_t* __restrict__ partial, const PipeK pk_in) {
+    const PipeK pk = POSLO_VAR_FMA == 5 ? pipek_vec(pk_in) : pk_in;
     __shared__ uint32_t red[(kVarT / 32) * 17];
     __shared__ uint16_t order[kVarTile];
     __shared__ uint32_t bucket_count[kVarBuckets];
@@ -146,6 +170,7 @@ __global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayo
     __shared__ __align__(16) uint32_t slots[kVarT * kSlotWords];
     __shared__ uint32_t s_acc[18 * kVarT];  // rows 0..8: sum of H1 digests, 9..17: sum of H0 digests
     __shared__ uint32_t s_pre[8], s_x0w[4];
+    __shared__ uint4 s_desc[2 * kVarT];  // StreamDesc of this thread's entry, streams 0 and 1
     const uint32_t tile = tm.tile_begin + blockIdx.x;
     uint32_t ep, j0, count;
     uint64_t ebase;
@@ -218,12 +243,22 @@ __global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayo
             L = lay.entry_len;
         }
         v.L = (uint32_t)L;
+        const uintptr_t base0 = ((uintptr_t)v.m - 4) & ~(uintptr_t)15;  // window of block 0
+        const uint32_t d0 = (uint32_t)((uintptr_t)v.m - base0);          // slot byte of m[0]: 4..19
+        const uint32_t fast_hi = v.L + d0 >= 96 ? (v.L + d0 - 96) >> 6 : 0u;  // interior blocks 1..fast_hi
         // One job loop shares ONE copy of the compression code (the kernel
         // stays inside the instruction cache): job 0 is x = onetime_seed(x0, j)
         // (resumed at round 4), then block b of stream 0 and of stream 1
         // alternate; Hc/Ho are the current/other stream's chaining values,
         // swapped after every job so both stay in registers.
         const uint32_t nb0 = nblocks(L + 16), nb1 = nblocks(L + 17);
+        {
+            const uint32_t slot_addr = (uint32_t)__cvta_generic_to_shared(v.slot);
+            s_desc[2 * threadIdx.x] = make_uint4(slot_addr + (d0 & ~3u), prmt_sel(d0 & 3), nb0 - 1,
+                                                 (uint32_t)((L + 16) * 8));
+            s_desc[2 * threadIdx.x + 1] = make_uint4(slot_addr + ((d0 - 1) & ~3u), prmt_sel((d0 - 1) & 3),
+                                                     nb1 - 1, (uint32_t)((L + 17) * 8));
+        }
         uint32_t Hc[8], Ho[8];
         sha256_init(Hc);
         sha256_init(Ho);
@@ -245,15 +280,17 @@ __global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayo
                 r0 = 4;
             } else {
                 const uint32_t b = (job - 1) >> 1, stream = (job - 1) & 1;
-                if (!stream) stage_window(v, b);
-                active = stream || b < nb0;
+                if (!stream) {
+                    if (b - 1u < fast_hi) stage_interior(v, base0, b);
+                    else stage_window(v, base0, d0, b);
+                }
+                const uint4 sd = s_desc[2 * threadIdx.x + stream];
+                active = b <= sd.z;  // stream 0 may end one block before stream 1
                 if (active) {
-                    load_block(v, b, stream, W);
-                    const uint32_t nb = stream ? nb1 : nb0;
-                    if (b == nb - 1) {
-                        const uint64_t bits = (L + 16 + stream) * 8;
-                        W[14] = (uint32_t)(bits >> 32);
-                        W[15] = (uint32_t)bits;
+                    load_block(sd.x, sd.y, W);
+                    if (b == sd.z) {  // entries < 512 MiB: the bit length fits one word
+                        W[14] = 0;
+                        W[15] = sd.w;
                     }
 #pragma unroll
                     for (int k = 0; k < 8; k++) st[k] = Hc[k];

@@ -9,6 +9,11 @@
 //   5  SHF.R.W funnel rotate (ALU pipe)       6  IMAD.HI immediate
 //   7  LOP3 + IMAD.HI immediate
 //   8  IMAD.WIDE.U32, 64-bit addend          9  LOP3 + IMAD.WIDE.U32
+//  11  LOP3 + IMAD with a per-thread REGISTER multiplier (R-R-R operands)
+//  12  LOP3 + two-input add, register addend (ptxas: VIADD R, R, R?)
+//  13  LOP3 + two-input add, uniform addend (VIADD R, R, UR)
+//  14  LOP3 on three vector registers + IMAD R-R-R (register-read pressure)
+//  15  LOP3 on three vector registers + IMAD R-UR-R
 //  10  shared-memory table lookups: data-dependent 32-bit LDS from a
 //      bank-replicated 256-entry table ([x][lane], the AES T-table layout of
 //      tile_common.cuh SmemT0), i.e. the suite-2 kernel's bound
@@ -16,6 +21,8 @@
 // Not part of the verifier ABI (separate library libposlo_microbench.so).
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+static __device__ uint32_t g_mb_mult = 0x9e3779b9u;  // the `a` multiplier, read opaquely
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uint32_t b, int iters) {
@@ -25,6 +32,7 @@ __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uin
         x[k] = threadIdx.x * (k + 1) ^ a;
         y[k] = blockIdx.x + k * b + threadIdx.x * 0x10001u;  // per-lane: keeps IMADs off the uniform datapath
     }
+    const uint32_t mreg = *reinterpret_cast<volatile const uint32_t*>(&g_mb_mult);  // == a, in a vector register
     for (int i = 0; i < iters; i++) {
 #pragma unroll
         for (int k = 0; k < 8; k++) {
@@ -44,6 +52,20 @@ __global__ void __launch_bounds__(256) k_int_peak(uint32_t* out, uint32_t a, uin
                 y[k] = (uint32_t)acc;
                 if (MODE == 8) x[k] = (uint32_t)(acc >> 32);
             }
+            if (MODE >= 11 && MODE <= 13)
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(x[(k + 1) & 7]));
+            if (MODE == 11)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(mreg), "r"(y[(k + 3) & 7]));
+            if (MODE == 12)
+                asm volatile("add.u32 %0, %0, %1;" : "+r"(y[k]) : "r"(y[(k + 3) & 7]));
+            if (MODE == 13)
+                asm volatile("add.u32 %0, %0, %1;" : "+r"(y[k]) : "r"(a));
+            if (MODE == 14 || MODE == 15)
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(x[(k + 5) & 7]), "r"(x[(k + 1) & 7]));
+            if (MODE == 14)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(mreg), "r"(y[(k + 3) & 7]));
+            if (MODE == 15)
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(a), "r"(y[(k + 3) & 7]));
             if (MODE == 9)
                 asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(x[(k + 1) & 7]));
         }
@@ -96,6 +118,11 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
             case 6: k_int_peak<6><<<blocks, 256>>>(out, a, b, iters); break;
             case 7: k_int_peak<7><<<blocks, 256>>>(out, a, b, iters); break;
             case 8: k_int_peak<8><<<blocks, 256>>>(out, a, b, iters); break;
+            case 11: k_int_peak<11><<<blocks, 256>>>(out, a, b, iters); break;
+            case 12: k_int_peak<12><<<blocks, 256>>>(out, a, b, iters); break;
+            case 13: k_int_peak<13><<<blocks, 256>>>(out, a, b, iters); break;
+            case 14: k_int_peak<14><<<blocks, 256>>>(out, a, b, iters); break;
+            case 15: k_int_peak<15><<<blocks, 256>>>(out, a, b, iters); break;
             case 10: k_lds_peak<<<blocks / 2, 256, 32768>>>(out, a, iters); break;
             default: k_int_peak<9><<<blocks, 256>>>(out, a, b, iters); break;
         }
@@ -109,7 +136,7 @@ extern "C" int poslo_microbench_int_peak(int device, int mode, double* ops_per_s
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    double per_iter = (mode == 2 || mode == 4 || mode == 7 || mode == 9) ? 16.0 : 8.0;
+    double per_iter = (mode == 2 || mode == 4 || mode == 7 || mode == 9 || mode >= 11) ? 16.0 : 8.0;
     double ops = (double)(mode == 10 ? blocks / 2 : blocks) * 256 * iters * per_iter * reps;
     *ops_per_s = ops / (ms * 1e-3);
     if (ms_out) *ms_out = ms / reps;

@@ -8,6 +8,10 @@
 #pragma once
 #include "poslo_common.cuh"
 
+#ifndef POSLO_KADD
+#define POSLO_KADD 0  // + K of the FMA == 5 round: 0 VIADD, 1 onev * K IMAD, 2 K from shared memory
+#endif
+
 #define SHA_IV0 0x6a09e667u
 #define SHA_IV1 0xbb67ae85u
 #define SHA_IV2 0x3c6ef372u
@@ -55,10 +59,21 @@ PHD void sha256_init(uint32_t st[8]) {
 // constants / zero (ZM documents which constants are zero), so constant
 // terms fold and zero terms vanish.
 // Inline PTX so LLVM cannot reassociate chains of a*one+b back into IADD3s.
+#ifndef POSLO_FADD
+#define POSLO_FADD 0  // 0: mad.lo a * one + b; 1: add.u32 (ptxas picks IADD3 / IMAD.IADD); 2: mad.lo a * 1 + b
+#endif
 PHD uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
 #ifdef __CUDA_ARCH__
     uint32_t r;
+#if POSLO_FADD == 1
+    (void)one;
+    asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+#elif POSLO_FADD == 2
+    (void)one;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(r) : "r"(a), "r"(b));
+#else
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+#endif
     return r;
 #else
     return a * one + b;
@@ -82,6 +97,7 @@ struct PipeK {
     uint32_t one;       // 1
     uint32_t r22, r25;  // 2^(32-22), 2^(32-25): rotr 22 (Sigma0), rotr 25 (Sigma1)
     uint32_t s3, s10;   // 2^29, 2^22: >> 3 (sigma0), >> 10 (sigma1)
+    uint32_t onev;      // 1 in a VECTOR register (pipek_vec), for IMAD onev * K + x (FMA == 5)
 };
 
 PHD PipeK pipek_make() {
@@ -91,7 +107,36 @@ PHD PipeK pipek_make() {
     k.r25 = 1u << 7;
     k.s3 = 1u << 29;
     k.s10 = 1u << 22;
+    k.onev = 1u;
     return k;
+}
+
+// An opaque 1 that lives in a vector register: `one` is a kernel parameter
+// (uniform register), and an IMAD has room for only one uniform operand, so
+// h + W + K with K itself uniform (constant bank / loop-indexed) cannot be
+// one * K + x on `one`. onev * K + x can: IMAD Rd, R_onev, UR_K|imm, Rx.
+// Loaded once per thread through a volatile global read so ptxas cannot fold
+// it back into an IADD3 on the ALU pipe.
+#ifdef __CUDACC__
+static __device__ uint32_t g_sha_onev = 1u;
+#endif
+PHD PipeK pipek_vec(PipeK k) {
+#ifdef __CUDA_ARCH__
+    k.onev = *reinterpret_cast<volatile const uint32_t*>(&g_sha_onev);
+#endif
+    return k;
+}
+
+// x + k on the FMA pipe with k as the multiplicand of the vector 1
+PHD uint32_t kmad(uint32_t x, uint32_t k, const PipeK& pk) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(pk.onev), "r"(k), "r"(x));
+    return r;
+#else
+    (void)pk;
+    return x + k;
+#endif
 }
 
 // rotr(x, n) with p = 2^(32-n), on the FMA pipe
@@ -314,8 +359,22 @@ __constant__ uint32_t c_sha_k[64] = {
     0xc67178f2u};
 #endif
 
+#if defined(__CUDACC__) && POSLO_KADD == 2
+// K in shared memory (a vector register after the LDS), so + K can be an IMAD
+// on the uniform `one` (sha_k_smem_init() fills it at kernel start)
+static __shared__ uint32_t s_sha_k[64];
+#endif
+PHD void sha_k_smem_init() {
+#if defined(__CUDA_ARCH__) && POSLO_KADD == 2
+    if (threadIdx.x < 64) s_sha_k[threadIdx.x] = c_sha_k[threadIdx.x];
+    __syncthreads();
+#endif
+}
+
 PHD uint32_t sha_kc(int t) {
-#ifdef __CUDA_ARCH__
+#if defined(__CUDA_ARCH__) && POSLO_KADD == 2
+    return s_sha_k[t];
+#elif defined(__CUDA_ARCH__)
     return c_sha_k[t];
 #else
     return sha_k(t);
@@ -365,6 +424,26 @@ PHD uint32_t sha_kc(int t) {
         (d) = fadd((d), t1_, one);                                                    \
         (h) = fadd(sha_maj((a), (b), (c)), fadd(s0_, t1_, one), one);                 \
     } while (0)
+// + K of SHA_RND_K: 0 = a two-input add (ptxas emits VIADD R, R, UR|imm, an
+// FMA-pipe instruction on sm_100), 1 = onev * K + x (IMAD).
+#if POSLO_KADD == 2
+#define SHA_KADD(x, k) fadd((x), (k), one)
+#elif POSLO_KADD
+#define SHA_KADD(x, k) kmad((x), (k), pk)
+#else
+#define SHA_KADD(x, k) ((x) + (k))
+#endif
+// FMA == 5: every addition on the FMA pipe. As SHA_RND_F, plus h + W + K as
+// an IMAD (h + W on `one`) and a VIADD / IMAD for + K (SHA_KADD).
+// Per round 6 SHF + 4 LOP3 on the ALU pipe and 7 FMA-pipe adds, so the
+// ALU pipe carries exactly the 1024 ALU-only operations of a compression.
+#define SHA_RND_K(a, b, c, d, e, f, g, h, w, k)                                       \
+    do {                                                                              \
+        const uint32_t hwk_ = SHA_KADD(fadd((h), (w), one), (k));                     \
+        uint32_t t1_ = fadd(sha_ch((e), (f), (g)), fadd(sha_S1(e), hwk_, one), one);  \
+        (d) = fadd((d), t1_, one);                                                    \
+        (h) = fadd(sha_maj((a), (b), (c)), fadd(sha_S0(a), t1_, one), one);           \
+    } while (0)
 #define SHA_SCHED_B(i)                                                                 \
     do {                                                                              \
         const uint32_t x15_ = W[((i) + 1) & 15], x2_ = W[((i) + 14) & 15];            \
@@ -413,6 +492,7 @@ PHD uint32_t sha_sched_p(uint32_t w16, uint32_t w15, uint32_t w7, uint32_t w2, c
 #define SHA_RND_SEL(...)                                        \
     do {                                                        \
         if (FMA >= 16) sha_rnd_p<FMA - 16>(__VA_ARGS__, pk);    \
+        else if (FMA == 5) SHA_RND_K(__VA_ARGS__);              \
         else if (FMA >= 4) SHA_RND_B(__VA_ARGS__);              \
         else if (FMA >= 3) SHA_RND_F3(__VA_ARGS__);             \
         else if (FMA) SHA_RND_F(__VA_ARGS__);                   \
@@ -487,6 +567,7 @@ PHD void sha256_rounds_loop(uint32_t st[8], uint32_t W[16], int blk0, const Pipe
 #pragma unroll
         for (int i = 0; i < 16; i++) {
             if (FMA >= 16) W[i] = sha_sched_p<FMA - 16>(W[i], W[(i + 1) & 15], W[(i + 9) & 15], W[(i + 14) & 15], pk);
+            else if (FMA == 5) SHA_SCHED_F(i);
             else if (FMA >= 4) SHA_SCHED_B(i);
             else if (FMA >= 2) SHA_SCHED_F(i);
             else SHA_SCHED(i);

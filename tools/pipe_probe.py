@@ -12,7 +12,8 @@ lib.poslo_microbench_int_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POI
                                           ctypes.POINTER(ctypes.c_double)]
 names = {0: "LOP3", 1: "IMAD reg", 2: "LOP3+IMAD reg", 3: "IMAD imm", 4: "LOP3+IMAD imm",
          5: "SHF.R.W", 6: "IMAD.HI imm", 7: "LOP3+IMAD.HI imm", 8: "IMAD.WIDE acc64", 9: "LOP3+IMAD.WIDE",
-         10: "LDS table lookup"}
+         10: "LDS table lookup", 11: "LOP3+IMAD R-R-R", 12: "LOP3+add reg", 13: "LOP3+add UR",
+         14: "LOP3(3R)+IMAD R-R-R", 15: "LOP3(3R)+IMAD R-UR-R"}
 out = {}
 for rep in range(2):
     for m, n in names.items():
