@@ -15,6 +15,10 @@
 //                                      scheme-F verifier output: aver_f_single per
 //                                      entry, aver_f_batch (all / a subset), fine
 //                                      distillation CCD + SeBVer V/U/I, JSON
+//   ref_tool paver FILE                the reference paver (and agg_ekeys' e-hat)
+//                                      on a fixture written by the GPU tests
+//                                      (tests/test_gpu_fullsize.py, "PVIO"
+//                                      layout below), JSON
 //   ref_tool bench S LOG2N N2 LEN WORKERS SEED REPS [MODE]
 //                                      times reference paver (MODE=coarse) or
 //                                      the per-epoch aver loop sharded over
@@ -415,6 +419,71 @@ int cmd_golden_f(int argc, char** argv) {
     return 0;
 }
 
+// ---- paver on a fixture file -----------------------------------------------
+// "PVIO" u32 suite, n1, n2, n_u, entry_len, n_epochs, workers, ds_capacity (LE)
+// u32 pk_len, pk (PoslocPublicKey wire), u32 ds_len, ds (SeedStack wire),
+// s_hat (32 B LE), u8 has_agg, r_hat_agg (32 B), epochs (u32 LE x n_epochs),
+// payload (n_epochs x n2 x entry_len bytes, epoch-major).
+int cmd_paver(int argc, char** argv) {
+    if (argc < 3) return 2;
+    FILE* f = std::fopen(argv[2], "rb");
+    if (!f) return 3;
+    Bytes buf;
+    uint8_t tmp[1 << 16];
+    size_t got;
+    while ((got = std::fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + got);
+    std::fclose(f);
+    size_t pos = 0;
+    auto u32 = [&]() {
+        uint32_t v;
+        std::memcpy(&v, buf.data() + pos, 4);
+        pos += 4;
+        return v;
+    };
+    if (buf.size() < 4 || std::memcmp(buf.data(), "PVIO", 4) != 0) return 4;
+    pos = 4;
+    SuiteConfig suite{static_cast<SuiteId>(u32()), 0, 0, 0};
+    suite.n1 = u32();
+    suite.n2 = u32();
+    suite.n_u = u32();
+    const uint32_t len = u32(), n_ep = u32(), workers = u32(), cap = u32();
+    const uint32_t pk_len = u32();
+    PoslocPublicKey pk = PoslocPublicKey::deserialize(Bytes(buf.begin() + pos, buf.begin() + pos + pk_len));
+    pos += pk_len;
+    const uint32_t ds_len = u32();
+    Reader rd(buf.data() + pos, ds_len);
+    SeedStack ds = SeedStack::deserialize(rd, cap);
+    pos += ds_len;
+    Scalar s_hat = Scalar::from_canonical_le(buf.data() + pos);
+    pos += 32;
+    const bool has_agg = buf[pos++] != 0;
+    std::optional<GroupElement> agg;
+    if (has_agg) agg = GroupElement::from_bytes(buf.data() + pos);
+    pos += 32;
+    std::vector<uint32_t> eps(n_ep);
+    for (auto& e : eps) e = u32();
+    std::map<uint32_t, std::vector<Bytes>> batches;
+    for (uint32_t k = 0; k < n_ep; k++) {
+        std::vector<Bytes> ep;
+        ep.reserve(suite.n2);
+        for (uint32_t j = 0; j < suite.n2; j++, pos += len) ep.emplace_back(buf.begin() + pos, buf.begin() + pos + len);
+        batches.emplace(eps[k], std::move(ep));
+    }
+    std::string error;
+    int verdict = -1;
+    Scalar e_hat;
+    try {
+        for (auto& p : agg_ekeys(suite, batches, ds, workers)) e_hat = e_hat.add(p.e);
+        verdict = paver(pk, batches, s_hat, agg, ds, workers) ? 1 : 0;
+    } catch (const std::exception& ex) {
+        error = ex.what();
+    }
+    std::printf("{\"paver\": %d, \"error\": \"%s\", \"e_hat\": \"", verdict, error.c_str());
+    for (uint8_t c : e_hat.le_bytes()) std::printf("%02x", c);
+    std::printf("\"}\n");
+    return 0;
+}
+
 // ---- bench ---------------------------------------------------------------
 int cmd_bench(int argc, char** argv) {
     if (argc < 9) return 2;
@@ -535,7 +604,7 @@ int main(int argc, char** argv) {
     randombytes_set_implementation(&g_rb_impl);
     if (sodium_init() < 0) return 3;
     if (argc < 2) {
-        std::fprintf(stderr, "usage: ref_tool kat|golden|bench ...\n");
+        std::fprintf(stderr, "usage: ref_tool kat|golden|golden_f|paver|bench ...\n");
         return 2;
     }
     std::string cmd = argv[1];
@@ -544,6 +613,7 @@ int main(int argc, char** argv) {
         if (cmd == "golden") return cmd_golden(argc, argv);
         if (cmd == "golden_f") return cmd_golden_f(argc, argv);
         if (cmd == "bench") return cmd_bench(argc, argv);
+        if (cmd == "paver") return cmd_paver(argc, argv);
     } catch (std::exception& e) {
         std::fprintf(stderr, "ref_tool: %s\n", e.what());
         return 1;
