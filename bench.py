@@ -332,6 +332,13 @@ def dropin_line(a):
                          "first_call_ms": j["first_call_ms"], "fresh_y_ms": j["fresh_y_ms"],
                          "fold_rhat_ms": j["fold_rhat_ms"], "agg_ekeys_ms": j["agg_ekeys_ms"],
                          "ok": j["ok"] and j["tamper_rejected"], "entries": j["entries"]}
+            if "host_gather_ms" in j:
+                # host roofline of the drop-in: the map walk alone (no device) and a
+                # plain memcpy of the same bytes, on all host threads
+                out[name]["host"] = {"threads": j["host_threads"], "gather_only_ms": j["host_gather_ms"],
+                                     "memcpy_ms": j["host_copy_ms"], "memcpy_gbs": j["host_copy_gbs"],
+                                     "last_call": j["last_call"],
+                                     "frac_of_gather_bound": round(j["host_gather_ms"] / j["warm_mean_ms"], 4)}
         except Exception as e:  # reported, never silently replaced
             out[name] = {"error": str(e)}
     out["path"] = ("poslo::paver(pk, std::map<u32, vector<Bytes>>, s_hat, R-hat aggregate, ds, workers=1) from "

@@ -272,6 +272,21 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* batch, co
                                 uint32_t n_seg, uint8_t* verdicts, uint8_t* seg_s, uint8_t* seg_r,
                                 uint8_t* seg_e, poslo_error* err);
 
+/* One distill_epoch (distiller.cpp:60-89) in a single device round trip, for
+ * callers that distil a stream epoch by epoch (the C++ ColdCryptoData
+ * drop-in): the host-resident batch holds ONE epoch (n2 entries, verified
+ * with the batch's ds = the epoch signature's stack); s_hat / r_hat its
+ * signature scalar and commitment; acc_s / acc_r the running valid and
+ * umbrella aggregates (2 x 32 B each: [valid, umbrella]). *verdict = aver's
+ * result; out_s / out_r = the aggregates with (s_hat, r_hat) folded into
+ * both when valid (Scalar::add, group_combine), unchanged otherwise. Errors
+ * as agg_ekeys (SeedNotDisclosed, FormatError), StateError for a batch size
+ * other than n2. */
+int poslo_gpu_distill_step(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t y[32],
+                           const uint8_t s_hat[32], const uint8_t r_hat[32], const uint8_t acc_s[64],
+                           const uint8_t acc_r[64], uint8_t* verdict, uint8_t out_s[64], uint8_t out_r[64],
+                           poslo_error* err);
+
 /* Masked segmented folds on the device: for g < n_seg, over items k in
  * [seg[g], seg[g+1]) with mask[k] != 0 (mask NULL = all): out_s[g] = sum of
  * scalars mod l and out_r[g] = group_combine fold of points. Either of

@@ -1677,6 +1677,87 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
     return ok(err);
 }
 
+// One distill_epoch (distiller.cpp:60-89) in ONE device round trip: hash,
+// check, and on a valid verdict the fold of (s-hat, R-hat) into both running
+// aggregates (fold_valid, :45-53), all queued on the stream; the hash error
+// word, the verdict and the two updated pairs come back in one pinned copy.
+int poslo_gpu_distill_step(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32], const uint8_t s_hat[32],
+                           const uint8_t r_hat[32], const uint8_t acc_s[64], const uint8_t acc_r[64],
+                           uint8_t* verdict, uint8_t out_s[64], uint8_t out_r[64], poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!b || !y || !s_hat || !r_hat || !acc_s || !acc_r || !verdict || !out_s || !out_r)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (b->n_epochs != 1 || b->device_resident)
+        return set_err(err, POSLO_INVALID_ARGUMENT, 0, "distill_step takes one host-resident epoch");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
+    Guard g(ctx);
+    if (b->epoch_starts && b->epoch_starts[1] - b->epoch_starts[0] != b->n2)
+        return set_err(err, POSLO_STATE_ERROR, b->epochs[0], "every batch must hold exactly n2 entries");
+    if (!scalar_canonical(s_hat) || !scalar_canonical(acc_s) || !scalar_canonical(acc_s + 32))
+        return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    cudaStream_t s = ctx->stream;
+    int* d_flags;
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, s));
+    int rc = ensure_tables(ctx, y, d_flags, err);
+    if (rc) return rc;
+    // items [valid acc, item, umbrella acc, item], mask [1, v, 1, v]
+    uint8_t items[256];
+    std::memcpy(items, acc_s, 32);
+    std::memcpy(items + 32, s_hat, 32);
+    std::memcpy(items + 64, acc_s + 32, 32);
+    std::memcpy(items + 96, s_hat, 32);
+    std::memcpy(items + 128, acc_r, 32);
+    std::memcpy(items + 160, r_hat, 32);
+    std::memcpy(items + 192, acc_r + 32, 32);
+    std::memcpy(items + 224, r_hat, 32);
+    uint8_t* d_items;
+    UPLOAD(b_s, items, sizeof items, d_items);
+    const uint32_t* d_sc = reinterpret_cast<const uint32_t*>(d_items);
+    const uint8_t* d_pt = d_items + 128;
+    Prepared P;
+    rc = run_hash(ctx, b, P, err);
+    if (rc) return rc;
+    uint8_t *d_verdict, *d_mask;
+    ENSURE(b_verdict, 1, d_verdict);
+    ENSURE(b_mask, 4, d_mask);
+    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, 1, P.d_etilde, d_sc + 8,
+                            d_pt + 32, nullptr, d_verdict, s);
+    CU(cudaMemsetAsync(d_mask, 1, 4, s));
+    CU(cudaMemcpyAsync(d_mask + 1, d_verdict, 1, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(d_mask + 3, d_verdict, 1, cudaMemcpyDeviceToDevice, s));
+    static const uint64_t seg64[3] = {0, 2, 4};
+    static const uint32_t seg32[3] = {0, 2, 4};
+    uint64_t* d_seg;
+    uint32_t *d_seg32, *d_out_s;
+    uint8_t* d_out_r;
+    UPLOAD(b_seg, seg64, sizeof seg64, d_seg);
+    UPLOAD(b_seg32, seg32, sizeof seg32, d_seg32);
+    ENSURE(b_out_s, 16, d_out_s);
+    ENSURE(b_out_r, 64, d_out_r);
+    launch_segsum_mod_l(d_sc, d_seg, 2, d_mask, d_out_s, s, /*skip_val=*/0);
+    launch_segfold_points(d_pt, d_seg32, 2, d_mask, d_out_r, d_flags + 1, s);
+    ctx->launches += 3;
+    PinnedStage* st = ctx->stage;
+    CU(cudaMemcpyAsync(&st->err_key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(&st->verdict, d_verdict, 1, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(st->flags, d_flags, 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(st->step_out, d_out_s, 64, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(st->step_out + 64, d_out_r, 64, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    rc = map_hash_error(st->err_key, b, err);
+    if (rc) return rc;
+    if (st->flags[0]) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding (Y)");
+    if (st->flags[1]) return set_err(err, POSLO_FORMAT_ERROR, 0, "invalid group element encoding");
+    *verdict = st->verdict;
+    std::memcpy(out_s, st->step_out, 64);
+    std::memcpy(out_r, st->step_out + 64, 64);
+    count_op(ctx, kOpDoubleExp, 1);
+    count_op(ctx, kOpCombine, 1 + (st->verdict ? 2 : 0));
+    finish_timing(ctx);
+    return ok(err);
+}
+
 // ---- scheme F ----------------------------------------------------------------
 // Per-entry scalars of a fine batch into device memory (d_e: n x 8 limbs).
 static int fine_scalars_dev(poslo_gpu_ctx* ctx, const poslo_fine_batch* fb, uint32_t** d_e_out, poslo_error* err) {

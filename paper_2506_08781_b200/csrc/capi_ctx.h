@@ -26,6 +26,7 @@ struct PinnedStage {  // pinned host landing zone for the per-call small D2H cop
     int flags[4];
     uint8_t verdict;
     unsigned long long scan[3];  // raw-image scan state {next record, records so far} + sentinel
+    uint8_t step_out[128];       // poslo_gpu_distill_step: the two updated (s, R) pairs
 };
 
 struct poslo_gpu_ctx {

@@ -196,7 +196,26 @@ struct Packed {
     std::atomic<bool> mismatch{false};  // gather met an entry of another length (fixed layout assumed)
     Bytes ds;
     poslo_batch b{};
+    double fill_ms = 0;  // time inside gather() (the host side of the pipelined copy)
 };
+
+// Host-side breakdown of the last paver / agg_ekeys call of this process
+// (poslo_dropin_last_stats): pack = sizing the map, fill = gathering it into
+// the pinned staging ring (overlapped with the copies and hashing), call =
+// the whole drop-in call.
+std::mutex g_stats_m;
+double g_stats[4] = {0, 0, 0, 0};  // pack_ms, fill_ms, call_ms, entries
+using sclock = std::chrono::steady_clock;
+double ms_between(sclock::time_point a, sclock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+}
+void record_stats(double pack_ms, double fill_ms, double call_ms, double entries) {
+    std::lock_guard<std::mutex> lk(g_stats_m);
+    g_stats[0] = pack_ms;
+    g_stats[1] = fill_ms;
+    g_stats[2] = call_ms;
+    g_stats[3] = entries;
+}
 
 uint64_t byte_at(const Packed& p, uint64_t t) { return p.fixed ? t * p.len0 : p.offsets[t]; }
 
@@ -232,6 +251,7 @@ bool copy_fixed(const std::vector<Bytes>& ms, uint64_t s0, uint64_t t0, uint64_t
 // epochs spread over the host cores.
 int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
     Packed& p = *static_cast<Packed*>(user);
+    const auto t_fill = sclock::now();
     const uint64_t last = first + count;
     const int64_t k0 = std::upper_bound(p.starts.begin(), p.starts.end(), first) - p.starts.begin() - 1;
     const int64_t k1 = std::lower_bound(p.starts.begin(), p.starts.end(), last) - p.starts.begin();
@@ -259,7 +279,43 @@ int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
             }
         }
     });
+    p.fill_ms += ms_between(t_fill, sclock::now());
     return p.mismatch.load() ? 1 : 0;  // a mismatch aborts the call; the caller re-packs with offsets
+}
+
+// One in-order walk of the map into p.epochs / p.msgs / p.starts (the batch
+// sizes, turned into entry offsets by the caller). The map's nodes are
+// scattered between the entries' heap blocks, so a serial walk is one cache
+// and TLB miss per epoch (~25 ms at 2^18 epochs); the key range is cut into
+// pieces at lower_bound() of evenly spaced keys and the pieces are walked on
+// every host core, each writing its own slice (its offset in the map is its
+// count of earlier nodes, from a first parallel counting pass over the same
+// pieces, which also warms the nodes for the second).
+void walk_map(const std::map<uint32_t, std::vector<Bytes>>& batches, Packed& p) {
+    const size_t ne = batches.size();
+    if (ne == 0) return;
+    const int64_t pieces = ne >= 4096 ? 256 : 1;
+    const uint64_t k_lo = batches.begin()->first, k_hi = batches.rbegin()->first;
+    std::vector<std::map<uint32_t, std::vector<Bytes>>::const_iterator> cut(pieces + 1);
+    cut[0] = batches.begin();
+    cut[pieces] = batches.end();
+    for (int64_t q = 1; q < pieces; q++)
+        cut[q] = batches.lower_bound((uint32_t)(k_lo + (k_hi - k_lo + 1) * (uint64_t)q / (uint64_t)pieces));
+    std::vector<size_t> first(pieces + 1, 0);
+    pool().parallel_for(pieces, [&](int64_t q) {
+        size_t c = 0;
+        for (auto it = cut[q]; it != cut[q + 1]; ++it) c++;
+        first[q + 1] = c;
+    });
+    for (int64_t q = 0; q < pieces; q++) first[q + 1] += first[q];
+    pool().parallel_for(pieces, [&](int64_t q) {
+        size_t k = first[q];
+        for (auto it = cut[q]; it != cut[q + 1]; ++it, ++k) {
+            p.epochs[k] = it->first;
+            p.msgs[k] = &it->second;
+            p.starts[k] = it->second.size();
+        }
+    });
 }
 
 // fixed_guess: assume one entry length (checked entry by entry while the
@@ -268,18 +324,18 @@ int gather(void* user, uint64_t first, uint64_t count, uint8_t* dst) {
 void pack(const SuiteConfig& suite, const std::map<uint32_t, std::vector<Bytes>>& batches,
           const SeedStack& ds, Packed& p, bool fixed_guess) {
     const size_t ne = batches.size();
-    p.msgs.reserve(ne);
-    p.epochs.reserve(ne);
-    p.starts.reserve(ne + 1);
+    p.msgs.resize(ne);
+    p.epochs.resize(ne);
+    p.starts.resize(ne + 1);
+    walk_map(batches, p);
     uint64_t t = 0;
-    for (const auto& [i, msgs] : batches) {
-        p.epochs.push_back(i);
-        p.msgs.push_back(&msgs);
-        p.starts.push_back(t);
-        t += msgs.size();
-        if (msgs.size() != suite.n2) p.uniform = false;
+    for (size_t k = 0; k < ne; k++) {  // entry index of each epoch (the walk stored sizes in starts)
+        const uint64_t sz = p.starts[k];
+        p.starts[k] = t;
+        t += sz;
+        if (sz != suite.n2) p.uniform = false;
     }
-    p.starts.push_back(t);
+    p.starts[ne] = t;
     const uint64_t n = t;
     // sizing pass over the entry headers, in parallel: one length, or offsets
     for (size_t k = 0; k < ne && p.len0 == 0 && n; k++)
@@ -355,15 +411,21 @@ std::vector<EpochKeyAggregate> agg_ekeys(const SuiteConfig& suite,
 bool paver(const PoslocPublicKey& pk, const std::map<uint32_t, std::vector<Bytes>>& batches,
            const Scalar& s_hat, const std::optional<GroupElement>& r_hat_agg, const SeedStack& ds,
            unsigned workers) {
-    // same validation order as batch_verify.cpp:68-83
-    for (const auto& [i, msgs] : batches)
-        if (msgs.size() != pk.suite.n2) throw StateError("every batch must hold exactly n2 entries");
+    // same validation order as batch_verify.cpp:68-83: batch sizes (the
+    // pack's map walk), the commitments, then workers (agg_ekeys, :15)
+    const auto t_call = sclock::now();
+    double pack_ms = 0;
+    Packed p;
+    pack(pk.suite, batches, ds, p, true);
+    pack_ms += ms_between(t_call, sclock::now());
+    for (const std::vector<Bytes>* m : p.msgs)
+        if (m->size() != pk.suite.n2) throw StateError("every batch must hold exactly n2 entries");
     std::vector<uint8_t> r_hats;
-    if (!r_hat_agg) {  // both maps are ordered: one merge walk finds every commitment
-        r_hats.resize(32 * batches.size());
+    if (!r_hat_agg) {  // both key lists are ordered: one merge walk finds every commitment
+        r_hats.resize(32 * p.epochs.size());
         auto it = pk.r_hats.begin();
         size_t k = 0;
-        for (const auto& [i, msgs] : batches) {
+        for (const uint32_t i : p.epochs) {
             while (it != pk.r_hats.end() && it->first < i) ++it;
             if (it == pk.r_hats.end() || it->first != i)
                 throw StateError("commitment for epoch " + std::to_string(i) + " no longer in public key");
@@ -373,20 +435,33 @@ bool paver(const PoslocPublicKey& pk, const std::map<uint32_t, std::vector<Bytes
     if (workers == 0) throw StateError("worker count must be at least 1");
     uint8_t verdict = 0;
     poslo_error err{};
-    auto run = [&](bool fixed_guess, Packed& p) {
-        pack(pk.suite, batches, ds, p, fixed_guess);
-        return poslo_gpu_paver(device(workers), &p.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
+    auto run = [&](bool fixed_guess, Packed& q) {
+        if (&q != &p) {
+            const auto t_pack = sclock::now();
+            pack(pk.suite, batches, ds, q, fixed_guess);
+            pack_ms += ms_between(t_pack, sclock::now());
+        }
+        return poslo_gpu_paver(device(workers), &q.b, pk.y.bytes().data(), s_hat.le_bytes().data(),
                                r_hat_agg ? r_hat_agg->bytes().data() : nullptr, r_hat_agg ? nullptr : r_hats.data(),
                                &verdict, &err);
     };
-    Packed p;
     int rc = run(true, p);
+    double fill_ms = p.fill_ms, entries = (double)p.b.n_entries;
     if (rc != POSLO_OK && p.mismatch.load()) {  // mixed entry lengths: again with byte offsets
         Packed q;
         rc = run(false, q);
+        fill_ms += q.fill_ms;
     }
+    record_stats(pack_ms, fill_ms, ms_between(t_call, sclock::now()), entries);
     if (rc != POSLO_OK) rethrow(err);
     return verdict != 0;
 }
 
 }  // namespace poslo
+
+// Host-side breakdown of the last drop-in paver call: {pack_ms, fill_ms,
+// call_ms, entries} (bench.py's e2e_dropin line reports it).
+extern "C" void poslo_dropin_last_stats(double out[4]) {
+    std::lock_guard<std::mutex> lk(poslo::g_stats_m);
+    for (int k = 0; k < 4; k++) out[k] = poslo::g_stats[k];
+}

@@ -3,8 +3,9 @@
 // distiller.hpp:31-98 (implementation it replaces: proj/src/distiller.cpp)
 // on top of the C-ABI in include/poslo_gpu.h. Every verdict, hash, modular
 // sum and group fold runs on the device:
-//   distill_epoch       -> poslo_gpu_distill_coarse (the epoch verified with
-//                          its own signature's ds) + poslo_gpu_segfold
+//   distill_epoch       -> poslo_gpu_distill_step (the epoch verified with
+//                          its own signature's ds and folded into the valid
+//                          and umbrella aggregates: one device round trip)
 //   distill_epoch_fine  -> poslo_gpu_fine_verify (seed tails, or the epoch's
 //                          new stack for the ds-carrying entry) + segfold
 //   sebver (coarse)     -> poslo_gpu_sebver
@@ -166,17 +167,20 @@ void ColdCryptoData::distill_epoch(PoslocPublicKey& pk, const std::vector<Bytes>
     b.ds = dsw.data();
     b.ds_len = static_cast<uint32_t>(dsw.size());
     b.ds_capacity = suite_.depth();
-    const uint32_t seg[2] = {0, 1};
-    uint8_t verdict = 0, seg_s[kScalarBytes], seg_r[kPointBytes];
+    // verdict and the fold into both running aggregates in one device round trip
+    uint8_t verdict = 0, acc_s[2 * kScalarBytes], acc_r[2 * kPointBytes], out_s[2 * kScalarBytes],
+        out_r[2 * kPointBytes];
+    std::memcpy(acc_s, valid_.s.le_bytes().data(), kScalarBytes);
+    std::memcpy(acc_s + kScalarBytes, umb_acc_.s.le_bytes().data(), kScalarBytes);
+    std::memcpy(acc_r, valid_.r.bytes().data(), kPointBytes);
+    std::memcpy(acc_r + kPointBytes, umb_acc_.r.bytes().data(), kPointBytes);
     poslo_error err{};
-    check(poslo_gpu_distill_coarse(dev(), &b, pk.y.bytes().data(), sig.s_hat.le_bytes().data(),
-                                   it->second.bytes().data(), seg, 1, &verdict, seg_s, seg_r, &err),
+    check(poslo_gpu_distill_step(dev(), &b, pk.y.bytes().data(), sig.s_hat.le_bytes().data(),
+                                 it->second.bytes().data(), acc_s, acc_r, &verdict, out_s, out_r, &err),
           err);
     if (verdict) {
-        const AggregatePair item{sig.s_hat, it->second};
-        auto out = fold({valid_, umb_acc_}, {{item}, {item}});
-        valid_ = out[0];
-        umb_acc_ = out[1];
+        valid_ = AggregatePair{scalar_of(out_s), point_of(out_r)};
+        umb_acc_ = AggregatePair{scalar_of(out_s + kScalarBytes), point_of(out_r + kPointBytes)};
         has_valid_ = true;
         umb_acc_nonempty_ = true;
     } else {

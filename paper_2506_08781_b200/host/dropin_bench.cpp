@@ -18,6 +18,7 @@
 #include <cstring>
 #include <map>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "../../include/poslo_synth.h"
@@ -27,6 +28,16 @@
 
 using namespace poslo;
 using clk = std::chrono::steady_clock;
+
+extern "C" void poslo_dropin_last_stats(double out[4]);
+
+// f(t, T) on T host threads
+template <class F>
+static void on_threads(unsigned T, F f) {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; t++) th.emplace_back([&, t] { f(t, T); });
+    for (auto& x : th) x.join();
+}
 
 static double ms_since(clk::time_point t0) { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); }
 
@@ -162,6 +173,42 @@ int main(int argc, char** argv) {
     const bool ok_tamper = paver(pk, batches, s_hat, r_agg, ds, workers);
     batches[n1 / 2][n2 / 3][0] ^= 1;
 
+    double st[4];
+    poslo_dropin_last_stats(st);  // the tamper call: same shape as a warm call
+
+    // Host roofline of the drop-in: (a) a plain parallel memcpy of the same
+    // bytes between two contiguous buffers, (b) a parallel gather of the
+    // std::map into one contiguous buffer with no device work; best of 3,
+    // every host thread.
+    const unsigned T = std::max(1u, std::thread::hardware_concurrency());
+    const size_t bytes = (size_t)n * L;
+    std::vector<uint8_t> src(bytes, 1), dst(bytes, 0);
+    double copy_ms = 1e30, gather_ms = 1e30;
+    for (int r = 0; r < 3; r++) {
+        auto t1 = clk::now();
+        on_threads(T, [&](unsigned t, unsigned TT) {
+            const size_t a = bytes * t / TT, z = bytes * (t + 1) / TT;
+            std::memcpy(dst.data() + a, src.data() + a, z - a);
+        });
+        copy_ms = std::min(copy_ms, ms_since(t1));
+    }
+    std::vector<const std::vector<Bytes>*> eps;
+    for (const auto& [i, v] : batches) eps.push_back(&v);
+    for (int r = 0; r < 3; r++) {
+        auto t1 = clk::now();
+        on_threads(T, [&](unsigned t, unsigned TT) {
+            const size_t a = eps.size() * t / TT, z = eps.size() * (t + 1) / TT;
+            for (size_t k = a; k < z; k++) {
+                uint8_t* d = dst.data() + k * (size_t)n2 * L;
+                for (const Bytes& m : *eps[k]) {
+                    std::memcpy(d, m.data(), L);
+                    d += L;
+                }
+            }
+        });
+        gather_ms = std::min(gather_ms, ms_since(t1));
+    }
+
     double best = 1e30, sum = 0;
     for (double w : warm) {
         best = std::min(best, w);
@@ -173,7 +220,8 @@ int main(int argc, char** argv) {
         "\"build_map_ms\": %.1f, \"first_call_ms\": %.3f, \"warm_ms\": [%s], \"warm_best_ms\": %.3f, "
         "\"warm_mean_ms\": %.3f, \"fresh_y_ms\": %.3f, \"fold_rhat_ms\": %.3f, \"agg_ekeys_ms\": %.3f, "
         "\"eps_warm_best\": %.1f, \"eps_warm_mean\": %.1f, \"ok\": %s, \"tamper_rejected\": %s, "
-        "\"n_parts\": %zu}\n",
+        "\"n_parts\": %zu, \"host_threads\": %u, \"host_copy_ms\": %.3f, \"host_copy_gbs\": %.2f, "
+        "\"host_gather_ms\": %.3f, \"last_call\": {\"pack_ms\": %.3f, \"fill_ms\": %.3f, \"call_ms\": %.3f}}\n",
         (unsigned long long)n, n2, L, suite_no, workers, poslo_gpu_device_count(), build_ms, first_ms,
         [&] {
             static char buf[4096];
@@ -183,6 +231,7 @@ int main(int argc, char** argv) {
             return buf;
         }(),
         best, mean, fresh_ms, fold_ms, agg_ms, n / (best * 1e-3), n / (mean * 1e-3),
-        (ok_first && ok_warm && ok_fresh && ok_fold) ? "true" : "false", ok_tamper ? "false" : "true", parts.size());
+        (ok_first && ok_warm && ok_fresh && ok_fold) ? "true" : "false", ok_tamper ? "false" : "true", parts.size(),
+        T, copy_ms, bytes / (copy_ms * 1e6), gather_ms, st[0], st[1], st[2]);
     return 0;
 }
