@@ -205,6 +205,13 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* batch, const uint8_t 
  * fold and final check of paver (batch_verify.cpp:83-86). parts_on_device:
  * e_parts is a device pointer (e.g. the output of an all-gather). */
 int poslo_gpu_agg_ekeys_partial(poslo_gpu_ctx* ctx, const poslo_batch* batch, uint8_t* d_e_part, poslo_error* err);
+/* The e-hat-independent half of a later combine_check with the same (y, s_hat,
+ * r_hat) -- alpha^s-hat and the R-hat operand -- queued now on an internal
+ * stream, so it overlaps the caller's agg_ekeys_partial and the all-gather
+ * and combine_check is left with the fold and the Y^e-hat half. Optional: a
+ * combine_check with other inputs (or without a prepare) computes it inline. */
+int poslo_gpu_combine_check_prepare(poslo_gpu_ctx* ctx, const uint8_t y[32], const uint8_t s_hat[32],
+                                    const uint8_t r_hat[32], poslo_error* err);
 int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t* e_parts, int32_t parts_on_device,
                             const uint8_t y[32], const uint8_t s_hat[32], const uint8_t r_hat[32], uint8_t* verdict,
                             poslo_error* err);

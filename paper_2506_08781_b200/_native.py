@@ -78,7 +78,7 @@ EXPORTS = [
     "poslo_gpu_sig_epochs", "poslo_gpu_log_scan", "poslo_gpu_create_multi", "poslo_gpu_member_count",
     "poslo_gpu_device_count", "poslo_gpu_agg_ekeys_partial", "poslo_gpu_combine_check",
     "poslo_gpu_group_op_counts", "poslo_gpu_reset_group_op_counts", "poslo_gpu_distill_coarse_ex",
-    "poslo_gpu_distill_step",
+    "poslo_gpu_distill_step", "poslo_gpu_combine_check_prepare",
 ]
 
 _lib = None
@@ -140,6 +140,7 @@ def load():
         "poslo_gpu_reset_group_op_counts": ([], None),
         "poslo_gpu_distill_coarse_ex": ([P, B, P, P, P, P, c.c_uint32, P, P, P, P, E], c.c_int),
         "poslo_gpu_distill_step": ([P, B, P, P, P, P, P, P, P, P, E], c.c_int),
+        "poslo_gpu_combine_check_prepare": ([P, P, P, P, E], c.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -357,6 +357,11 @@ class Verifier:
         """e-hat of this shard's batch (a filled N.PosloBatch) into 32 bytes of device memory."""
         self._call(self._lib.poslo_gpu_agg_ekeys_partial, ctypes.byref(cb), ctypes.c_void_p(d_out))
 
+    def combine_check_prepare(self, y: bytes, s_hat: bytes, r_hat: bytes):
+        """Queues the e-hat-independent half of the next combine_check with these
+        inputs (overlaps the caller's hashing and all-gather)."""
+        self._call(self._lib.poslo_gpu_combine_check_prepare, _buf(y), _buf(s_hat), _buf(r_hat))
+
     def combine_check(self, parts, y: bytes, s_hat: bytes, r_hat: bytes, n_parts: Optional[int] = None) -> bool:
         """parts: bytes (host, n x 32) or an int device pointer (then n_parts is required)."""
         v = ctypes.c_uint8(0)

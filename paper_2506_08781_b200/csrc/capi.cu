@@ -14,8 +14,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
 #include <functional>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/poslo_gpu.h"
@@ -223,6 +226,87 @@ bool device_readable(const void* p) {
            (a.type == cudaMemoryTypeHost && a.devicePointer != nullptr);
 }
 
+// Plain pageable host memory (not registered with CUDA): a DMA from it is
+// staged by the driver synchronously, chunk by chunk, at a fraction of the
+// link rate, so run_hash stages such logs itself (parallel host copies into
+// the pinned ring, the DMA of chunk c overlapping the copy of chunk c + 1).
+bool host_pageable(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Persistent host workers for copy_parallel (one copy at a time per process;
+// concurrent callers serialise on the pool, each copy still runs on every core).
+class HostCopyPool {
+public:
+    static HostCopyPool& get() {
+        static HostCopyPool p;
+        return p;
+    }
+    void copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
+        const size_t T = th_.size() + 1;
+        if (bytes < (4u << 20) || T == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one(call_);
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            dst_ = dst;
+            src_ = src;
+            bytes_ = bytes;
+            parts_ = T;
+            next_.store(0);
+            busy_ = (int)th_.size();
+            gen_++;
+        }
+        cv_.notify_all();
+        run();
+        std::unique_lock<std::mutex> lk(m_);
+        done_.wait(lk, [this] { return busy_ == 0; });
+    }
+
+private:
+    HostCopyPool() {
+        const unsigned n = std::min(std::max(1u, std::thread::hardware_concurrency()), 64u) - 1;
+        for (unsigned i = 0; i < n; i++) th_.emplace_back([this] { work(); });
+        for (auto& t : th_) t.detach();  // process lifetime: never joined at exit
+    }
+    void run() {
+        for (size_t k = next_.fetch_add(1); k < parts_; k = next_.fetch_add(1)) {
+            const size_t a = bytes_ * k / parts_, z = bytes_ * (k + 1) / parts_;
+            std::memcpy(dst_ + a, src_ + a, z - a);
+        }
+    }
+    void work() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            run();
+            std::lock_guard<std::mutex> lk(m_);
+            if (--busy_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_, call_;
+    std::condition_variable cv_, done_;
+    uint8_t* dst_ = nullptr;
+    const uint8_t* src_ = nullptr;
+    size_t bytes_ = 0, parts_ = 0;
+    std::atomic<size_t> next_{0};
+    int busy_ = 0;
+    uint64_t gen_ = 0;
+};
+
 // After the whole raw image is scanned: read_log's FormatError on a
 // truncated record, epochs_of's on a count that is not a nonzero multiple of
 // n2 (tools/poslo.cpp:32-40), and the batch must name exactly that many
@@ -318,6 +402,9 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
     const bool chunked = !raw_image && !b->device_resident && P.uniform && (b->offsets || epoch_bytes > 0) &&
                          ((b->payload_bytes >= 2 * kChunkBytes && n_ep > 1) || (has_fill && n_ep > 0));
     const bool raw_chunked = raw_image && !b->device_resident && b->payload_bytes >= 2 * kChunkBytes && n_ep > 1;
+    // a pageable host log goes through the pinned ring like a producer's chunks
+    const bool stage_pageable = chunked && !has_fill && host_pageable(b->payload);
+    const bool use_ring = has_fill || stage_pageable;
     auto epoch_byte = [&](uint32_t e) -> uint64_t {  // first payload byte of the e-th queried epoch
         return b->offsets ? b->offsets[(uint64_t)e * b->n2] : (uint64_t)e * epoch_bytes;
     };
@@ -581,7 +668,7 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
             CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             ctx->chunk_ev.push_back(ev);
         }
-        if (has_fill) {  // pinned ring for the producer: kFillSlots chunks in flight
+        if (use_ring) {  // pinned ring for the producer / pageable source: kFillSlots chunks in flight
             size_t need = 0;
             for (uint32_t c = 0; c < n_chunks; c++)
                 need = std::max<size_t>(need, epoch_byte(cut[c + 1]) - epoch_byte(cut[c]));
@@ -605,11 +692,13 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
         for (uint32_t c = 0; c < n_chunks; c++) {
             const uint32_t e0 = cut[c], e1 = cut[c + 1];
             const uint64_t off = epoch_byte(e0), bytes = epoch_byte(e1) - off;
-            if (has_fill) {
+            if (use_ring) {
                 // produce chunk c into a free slot while chunks c-1, c-2 copy and hash
                 const int sl = (int)(c % poslo_gpu_ctx::kFillSlots);
                 CU(cudaEventSynchronize(ctx->fill_ev[sl]));
-                if (b->fill(b->fill_user, (uint64_t)e0 * b->n2, (uint64_t)(e1 - e0) * b->n2, ctx->fill_slot[sl]) != 0) {
+                if (stage_pageable)
+                    HostCopyPool::get().copy(ctx->fill_slot[sl], b->payload + off, bytes);
+                else if (b->fill(b->fill_user, (uint64_t)e0 * b->n2, (uint64_t)(e1 - e0) * b->n2, ctx->fill_slot[sl]) != 0) {
                     cudaStreamSynchronize(ctx->copy);
                     cudaStreamSynchronize(s);
                     return set_err(err, POSLO_INVALID_ARGUMENT, 0, "fill producer failed");
@@ -952,6 +1041,7 @@ int poslo_gpu_create(int device, poslo_gpu_ctx** out, poslo_error* err) {
         e = cudaEventCreateWithFlags(&ctx->ev_side[i], cudaEventDisableTiming);
     for (int i = 0; i < 2 && e == cudaSuccess; i++)
         e = cudaEventCreateWithFlags(&ctx->ev_hash[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_pre, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         poslo_gpu_destroy(ctx);
         return set_err(err, POSLO_CUDA_ERROR, 0, "stream: %s", cudaGetErrorString(e));
@@ -1025,7 +1115,8 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_pts, &ctx->b_foldscratch, &ctx->b_rhat, &ctx->b_pre, &ctx->b_starts_ds,
                       &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok,
                       &ctx->b_scan_exit, &ctx->b_scan_cnt, &ctx->b_scan_start, &ctx->b_scan_base,
-                      &ctx->b_scan_off, &ctx->b_scan_state, &ctx->b_seg_e, &ctx->b_out_e};
+                      &ctx->b_scan_off, &ctx->b_scan_state, &ctx->b_seg_e, &ctx->b_out_e, &ctx->b_ppre_s, &ctx->b_ppre_r,
+                      &ctx->b_ppre};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
@@ -1047,6 +1138,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
         if (ev) cudaEventDestroy(ev);
     for (auto& ev : ctx->ev_hash)
         if (ev) cudaEventDestroy(ev);
+    if (ctx->ev_pre) cudaEventDestroy(ctx->ev_pre);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
     if (prev >= 0) cudaSetDevice(prev);
@@ -1221,6 +1313,40 @@ int poslo_gpu_agg_ekeys_partial(poslo_gpu_ctx* ctx, const poslo_batch* b, uint8_
     return ok(err);
 }
 
+// The e-hat-independent half of the next combine_check with these inputs,
+// queued on the side stream now (before the caller's hashing), so that only
+// the fold and the Y^e-hat half remain after the all-gather.
+int poslo_gpu_combine_check_prepare(poslo_gpu_ctx* ctx, const uint8_t y[32], const uint8_t s_hat[32],
+                                    const uint8_t r_hat[32], poslo_error* err) {
+    if (!ctx) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null context");
+    if (!y || !s_hat || !r_hat) return set_err(err, POSLO_INVALID_ARGUMENT, 0, "null argument");
+    if (!ctx->members.empty()) ctx = ctx->members[0];
+    if (!scalar_canonical(s_hat)) return set_err(err, POSLO_FORMAT_ERROR, 0, "non-canonical scalar");
+    Guard g(ctx);
+    int* d_flags;
+    ENSURE(b_flags, 4, d_flags);
+    CU(cudaMemsetAsync(d_flags, 0, 16, ctx->stream));
+    int rc = ensure_tables(ctx, y, d_flags, err);
+    if (rc) return rc;
+    // own buffers: the side-stream kernel may run after later calls reuse the shared ones
+    uint32_t* d_s;
+    uint8_t* d_rhat;
+    void* d_pre;
+    UPLOAD(b_ppre_s, s_hat, 32, d_s);
+    UPLOAD(b_ppre_r, r_hat, 32, d_rhat);
+    ENSURE(b_ppre, 256, d_pre);
+    CU(cudaEventRecord(ctx->ev_side[0], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
+    launch_check_pre(ctx->d_tabB, d_s, d_rhat, d_pre, ctx->side);
+    ctx->launches += 1;
+    CU(cudaEventRecord(ctx->ev_pre, ctx->side));
+    std::memcpy(ctx->pre_key, y, 32);
+    std::memcpy(ctx->pre_key + 32, s_hat, 32);
+    std::memcpy(ctx->pre_key + 64, r_hat, 32);
+    ctx->pre_valid = true;
+    return ok(err);
+}
+
 int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t* e_parts, int32_t parts_on_device,
                             const uint8_t y[32], const uint8_t s_hat[32], const uint8_t r_hat[32], uint8_t* verdict,
                             poslo_error* err) {
@@ -1251,20 +1377,32 @@ int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t*
         UPLOAD(b_e, e_parts, (size_t)n_parts * 32, d_up);
         d_parts = d_up;
     }
-    uint32_t *d_sum, *d_scr, *d_s;
-    uint8_t *d_rhat, *d_verdict;
+    uint32_t *d_sum, *d_scr;
+    uint8_t* d_verdict;
     void* d_pre;
     ENSURE(b_sum, 8, d_sum);
     ENSURE(b_scratch, 17 * 1024, d_scr);
-    UPLOAD(b_s, s_hat, 32, d_s);
-    UPLOAD(b_rhat, r_hat, 32, d_rhat);
     ENSURE(b_pre, 256, d_pre);
     ENSURE(b_verdict, 1, d_verdict);
     // the rank-ordered fold mod l (batch_verify.cpp:83-85), then the one check (:86)
     launch_sum_mod_l(d_parts, 8, n_parts, nullptr, d_sum, d_scr, ctx->stream);
-    launch_check_pre(ctx->d_tabB, d_s, d_rhat, d_pre, ctx->stream);
+    const bool prepared = ctx->pre_valid && std::memcmp(ctx->pre_key, y, 32) == 0 &&
+                          std::memcmp(ctx->pre_key + 32, s_hat, 32) == 0 &&
+                          std::memcmp(ctx->pre_key + 64, r_hat, 32) == 0;
+    ctx->pre_valid = false;
+    if (prepared) {  // queued by combine_check_prepare on the side stream
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_pre, 0));
+        d_pre = ctx->b_ppre.p;
+    } else {
+        uint32_t* d_s;
+        uint8_t* d_rhat;
+        UPLOAD(b_s, s_hat, 32, d_s);
+        UPLOAD(b_rhat, r_hat, 32, d_rhat);
+        launch_check_pre(ctx->d_tabB, d_s, d_rhat, d_pre, ctx->stream);
+        ctx->launches += 1;
+    }
     launch_check_post(ctx->d_tabY, d_sum, d_pre, d_verdict, ctx->stream);
-    ctx->launches += 4;
+    ctx->launches += 3;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&ctx->stage->verdict, d_verdict, 1, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

@@ -36,6 +36,11 @@ struct poslo_gpu_ctx {
     cudaStream_t copy = nullptr;  // H2D of host-resident logs, overlapped with hashing
     cudaStream_t side = nullptr;  // e-hat-independent part of the group check, overlapped with hashing
     cudaEvent_t ev_side[2] = {};
+    // combine_check_prepare: the e-hat-independent half of the next
+    // combine_check (alpha^s-hat, R-hat decode) queued on `side`, keyed by its inputs
+    bool pre_valid = false;
+    uint8_t pre_key[96] = {};
+    cudaEvent_t ev_pre = nullptr;
     cudaStream_t hash2 = nullptr;  // second hash stream: epoch pieces alternate so one piece's tail
     cudaEvent_t ev_hash[2] = {};   // overlaps the next piece instead of idling at a kernel boundary
     std::vector<cudaEvent_t> chunk_ev;
@@ -43,7 +48,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state, b_seg_e, b_out_e;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state, b_seg_e, b_out_e, b_ppre_s, b_ppre_r, b_ppre;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;

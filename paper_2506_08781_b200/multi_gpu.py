@@ -130,10 +130,15 @@ def _root(group) -> int:
 
 # ---------------------------------------------------------------- coarse PAVer
 class ShardedPaver:
-    """Coarse PAVer over a sharded log: partial e-hat into device memory, an
-    all-gather of the partials (NCCL: device to device, no host hop), the
-    rank-ordered fold mod l and ONE check on rank 0, whose verdict every rank
-    receives. Buffers are allocated once and reused across steps."""
+    """Coarse PAVer over a sharded log: partial e-hat into device memory, ONE
+    all-gather of (partial, status) per rank (NCCL: device to device, no host
+    hop), the rank-ordered fold mod l and ONE check on rank 0, whose verdict
+    every rank receives. Rank 0 queues the e-hat-independent half of the check
+    (alpha^s-hat, the R-hat operand) on a side stream before hashing, so after
+    the all-gather only the fold and the Y^e-hat half remain. Buffers are
+    allocated once and reused across steps."""
+
+    REC = 64  # bytes per rank in the gather: partial e-hat (32) | status (1) | pad
 
     def __init__(self, v: api.Verifier, group=None):
         self.v, self.group = v, group
@@ -141,34 +146,39 @@ class ShardedPaver:
         self.rank = dist.get_rank(group)
         self.nccl = dist.get_backend(group) == "nccl"
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.part = torch.zeros(32, dtype=torch.uint8, device=dev)
-        self.parts = torch.zeros(32 * self.world, dtype=torch.uint8, device=dev if self.nccl else "cpu")
+        self.rec = torch.zeros(self.REC, dtype=torch.uint8, device=dev)
+        self.recs = torch.zeros(self.REC * self.world, dtype=torch.uint8, device=dev if self.nccl else "cpu")
         self.flag = torch.zeros(1, dtype=torch.uint8, device=dev if self.nccl else "cpu")
-        self.status = torch.zeros(self.world, dtype=torch.uint8, device=dev if self.nccl else "cpu")
 
     def __call__(self, cb, y: bytes, s_hat: bytes, r_hat: bytes) -> bool:
-        _, exc = _guard(lambda: self.v.agg_ekeys_partial(cb, self.part.data_ptr()))
-        # one status byte per rank; the full error record only when someone failed
-        self.flag[0] = 0 if exc is None else 1
-        dist.all_gather_into_tensor(self.status, self.flag, group=self.group)
-        if int(self.status.max().item()):
-            agree(exc, self.group)
-        if self.nccl:
-            dist.all_gather_into_tensor(self.parts, self.part, group=self.group)
+        prep_exc = None
+        if self.rank == 0:  # overlaps this rank's hashing
+            _, prep_exc = _guard(lambda: self.v.combine_check_prepare(y, s_hat, r_hat))
+        _, exc = _guard(lambda: self.v.agg_ekeys_partial(cb, self.rec.data_ptr()))
+        if exc is not None:
+            self.rec[32] = 1
         else:
-            dist.all_gather_into_tensor(self.parts, self.part.cpu(), group=self.group)
-        ok, exc = None, None
+            self.rec[32] = 0
+        if self.nccl:
+            dist.all_gather_into_tensor(self.recs, self.rec, group=self.group)
+        else:
+            dist.all_gather_into_tensor(self.recs, self.rec.cpu(), group=self.group)
+        ok, exc0 = None, None
         if self.rank == 0:
-            if self.nccl:
-                ok, exc = _guard(lambda: self.v.combine_check(self.parts.data_ptr(), y, s_hat, r_hat,
-                                                              n_parts=self.world))
+            host = self.recs.cpu().numpy().reshape(self.world, self.REC)  # one small D2H: statuses + partials
+            if host[:, 32].any():
+                res = 2
             else:
-                ok, exc = _guard(lambda: self.v.combine_check(self.parts.numpy().tobytes(), y, s_hat, r_hat))
-        self.flag[0] = (2 if exc is not None else (1 if ok else 0)) if self.rank == 0 else 0
+                parts = host[:, :32].tobytes()
+                ok, exc0 = _guard(lambda: self.v.combine_check(parts, y, s_hat, r_hat))
+                if exc0 is None and prep_exc is not None:
+                    exc0 = prep_exc
+                res = 2 if exc0 is not None else (1 if ok else 0)
+            self.flag[0] = res
         dist.broadcast(self.flag, src=_root(self.group), group=self.group)
         res = int(self.flag.item())
-        if res == 2:
-            agree(exc if self.rank == 0 else None, self.group)
+        if res == 2:  # a rank failed while hashing, or rank 0's check raised: every rank raises the same
+            agree(exc if exc is not None else (exc0 if self.rank == 0 else None), self.group)
         return res == 1
 
 

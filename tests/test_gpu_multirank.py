@@ -57,8 +57,8 @@ def _worker(rank, world, port, q):
         sp = M.ShardedPaver(v)
         out["c2_verdict"] = sp(sl.batch(), sl.Y, S, R)
         if rank == 0:
-            p = sp.parts.cpu().numpy().tobytes() if sp.parts.is_cuda else sp.parts.numpy().tobytes()
-            out["c2_e_hat"] = v.scalar_sum([p[32 * r:32 * r + 32] for r in range(world)])
+            p = sp.recs.cpu().numpy().tobytes()  # per rank: partial e-hat (32 B) | status | pad
+            out["c2_e_hat"] = v.scalar_sum([p[sp.REC * r:sp.REC * r + 32] for r in range(world)])
         out["c2_e_tilde"] = b"".join(M.sharded_e_tilde(v, sl.batch()))
         if world == 1:  # the direct single-context calls agree
             et, eh = ctypes.create_string_buffer(32 * sl.n1), ctypes.create_string_buffer(32)

@@ -317,7 +317,9 @@ def test_seed_derivation_dense_and_sparse_stacks(verifier, suite):
 
 def test_chunked_host_path_matches_device_resident(verifier):
     """A host-resident log > 128 MiB streams in 64 MiB chunks on a copy
-    stream; results must equal the device-resident call bit for bit."""
+    stream (from pinned memory directly, from pageable memory through the
+    pinned staging ring); results must equal the device-resident call bit for
+    bit."""
     import ctypes
 
     import torch
@@ -349,6 +351,10 @@ def test_chunked_host_path_matches_device_resident(verifier):
     et_h, eh_h = run(host.data_ptr(), 0)
     et_d, eh_d = run(dev.data_ptr(), 1)
     assert et_h == et_d and eh_h == eh_d
+    # the same log in PAGEABLE host memory: staged through the pinned ring by host copies
+    pageable = host.numpy().copy()
+    et_p, eh_p = run(pageable.ctypes.data, 0)
+    assert et_p == et_d and eh_p == eh_d
     # sampled epochs against the oracle
     for k in (0, 1, 4097, n1 - 1):
         ents = [bytes(host[(k * n2 + j) * L:(k * n2 + j + 1) * L].numpy()) for j in range(n2)]
