@@ -245,8 +245,9 @@ bool host_pageable(const void* p) {
 class HostCopyPool {
 public:
     static HostCopyPool& get() {
-        static HostCopyPool p;
-        return p;
+        // never destroyed: the detached workers may still wait on cv_ at exit
+        static HostCopyPool* p = new HostCopyPool();
+        return *p;
     }
     void copy(uint8_t* dst, const uint8_t* src, size_t bytes) {
         const size_t T = th_.size() + 1;
