@@ -473,7 +473,8 @@ def main():
                 call(lib.poslo_gpu_distill_coarse_ex, ctypes.byref(b), Yb,
                      *[ctypes.c_void_p(x) if isinstance(x, int) else x for x in (s_, r_)],
                      ctypes.c_void_p(seg.ctypes.data), ng, verd, *o)
-                res = {"invalid": [sl.first_epoch + k for k in range(n1_local) if not verd.raw[k]]}
+                vr = verd.raw  # one copy (ctypes .raw builds a new bytes object per access)
+                res = {"invalid": [sl.first_epoch + k for k in range(n1_local) if not vr[k]]}
             last["res"] = res
             return 1
 

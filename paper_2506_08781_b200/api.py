@@ -517,7 +517,8 @@ class Verifier:
                    _buf(b"".join(points)) if points else None, _buf(m) if m else None,
                    segs.ctypes.data if ng else None, ng, out_s if scalars else None,
                    out_r if points else None)
-        return [(out_s.raw[32 * g:32 * g + 32], out_r.raw[32 * g:32 * g + 32]) for g in range(ng)]
+        rs, rr = out_s.raw, out_r.raw  # ctypes .raw copies the whole buffer per access
+        return [(rs[32 * g:32 * g + 32], rr[32 * g:32 * g + 32]) for g in range(ng)]
 
     # -- SeBVer over a coarse CCD (distiller.cpp:181-233)
     def sebver(self, y: bytes, suite: SuiteConfig, all_msgs, ds: SeedStack, epochs_distilled: int,

@@ -61,11 +61,18 @@ PHD void sha256_init(uint32_t st[8]) {
 // Inline PTX so LLVM cannot reassociate chains of a*one+b back into IADD3s.
 #ifndef POSLO_FADD
 #define POSLO_FADD 0  // 0: mad.lo a * one + b; 1: add.u32 (ptxas picks IADD3 / IMAD.IADD); 2: mad.lo a * 1 + b
+                      // 3: a * c_fadd_one + b with the multiplier read from the constant bank
+#endif
+#if defined(__CUDACC__) && POSLO_FADD == 3
+__constant__ uint32_t c_fadd_one = 1u;
 #endif
 PHD uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
 #ifdef __CUDA_ARCH__
     uint32_t r;
-#if POSLO_FADD == 1
+#if POSLO_FADD == 3
+    (void)one;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(c_fadd_one), "r"(b));
+#elif POSLO_FADD == 1
     (void)one;
     asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
 #elif POSLO_FADD == 2

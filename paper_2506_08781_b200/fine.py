@@ -154,7 +154,8 @@ def fine_scalars(v: api.Verifier, fb: FineBatch, want_each=True, want_sum=False)
     tot = ctypes.create_string_buffer(32) if want_sum else None
     cs = fb.cstruct()
     v._call(v._lib.poslo_gpu_fine_scalars, ctypes.byref(cs), out, tot)
-    each = [out.raw[32 * k:32 * k + 32] for k in range(fb.n)] if want_each else None
+    raw = out.raw  # ctypes .raw copies the whole buffer per access
+    each = [raw[32 * k:32 * k + 32] for k in range(fb.n)] if want_each else None
     return each, (tot.raw if want_sum else None)
 
 
@@ -163,7 +164,8 @@ def fine_verify(v: api.Verifier, fb: FineBatch, y: bytes, s: Sequence[bytes], r:
     cs = fb.cstruct()
     v._call(v._lib.poslo_gpu_fine_verify, ctypes.byref(cs), _buf(y), _buf(b"".join(s)) if s else None,
             _buf(b"".join(r)) if r else None, verd)
-    return [bool(verd.raw[k]) for k in range(fb.n)]
+    vr = verd.raw
+    return [bool(vr[k]) for k in range(fb.n)]
 
 
 def aver_f_single_batch(pk: PoslofPublicKey, msgs: Sequence[bytes], sigs: Sequence[FineSignature],

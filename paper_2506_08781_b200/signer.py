@@ -75,4 +75,5 @@ def sign_epochs(sk: PoslocSecretKey, batches: Dict[int, Sequence[bytes]],
     out = ctypes.create_string_buffer(max(n, 1) * 32)
     cb = pb.cstruct()
     v._call(v._lib.poslo_gpu_sig_epochs, ctypes.byref(cb), _buf(sk.r), _buf(sk.y), out)
-    return {int(e): out.raw[32 * k:32 * k + 32] for k, e in enumerate(pb.epochs)}
+    raw = out.raw  # ctypes .raw copies the whole buffer per access
+    return {int(e): raw[32 * k:32 * k + 32] for k, e in enumerate(pb.epochs)}
