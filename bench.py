@@ -473,8 +473,8 @@ def main():
                 call(lib.poslo_gpu_distill_coarse_ex, ctypes.byref(b), Yb,
                      *[ctypes.c_void_p(x) if isinstance(x, int) else x for x in (s_, r_)],
                      ctypes.c_void_p(seg.ctypes.data), ng, verd, *o)
-                vr = verd.raw  # one copy (ctypes .raw builds a new bytes object per access)
-                res = {"invalid": [sl.first_epoch + k for k in range(n1_local) if not vr[k]]}
+                vr = np.frombuffer(verd.raw, dtype=np.uint8, count=n1_local)  # one copy of the verdicts
+                res = {"invalid": (np.flatnonzero(vr == 0) + sl.first_epoch).tolist()}
             last["res"] = res
             return 1
 

@@ -243,7 +243,8 @@ def sharded_distill(v: api.Verifier, cb, first_epoch: int, y: bytes, s_hats, r_h
     if dist.get_rank(group) != 0:
         return None
     verdicts = b"".join(verd_all)
-    invalid = [first_epoch + i for i, x in enumerate(verdicts) if not x]  # rank 0 holds the first shard
+    # rank 0 holds the first shard
+    invalid = (np.flatnonzero(np.frombuffer(verdicts, dtype=np.uint8) == 0) + first_epoch).tolist()
     # fold the pieces of each umbrella in rank order (one segmented fold on the device)
     recs = [(struct.unpack("<I", p[k:k + 4])[0], p[k + 4:k + 36], p[k + 36:k + 68], p[k + 68:k + 100])
             for p in piece_all for k in range(0, len(p), 100)]
