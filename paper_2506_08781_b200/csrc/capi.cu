@@ -857,13 +857,13 @@ int gen_table(poslo_gpu_ctx* ctx, int kind, int* d_flags, void** out, poslo_erro
         const size_t bytes = kind == 0 ? kCombTableBytes : kind == 1 ? kComb256TableBytes : kComb16TableBytes;
         void* p = nullptr;
         CU(cudaMalloc(&p, bytes));
-        if (kind == 0)
-            launch_build_table(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
-        else if (kind == 1)
-            launch_build_table256(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
-        else
-            launch_build_table65536(nullptr, ctx->d_pk, p, d_flags, ctx->stream);
-        ctx->launches += 2;
+        if (ctx->pk_owner != 1) {  // the generator's powers, once per context for all radices
+            launch_table_powers(nullptr, ctx->d_pk, d_flags, ctx->stream);
+            ctx->pk_owner = 1;
+            ctx->launches += 1;
+        }
+        launch_table_fill(kind, ctx->d_pk, p, ctx->stream);
+        ctx->launches += 1;
         cudaError_t e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) {
             cudaFree(p);
@@ -875,18 +875,43 @@ int gen_table(poslo_gpu_ctx* ctx, int kind, int* d_flags, void** out, poslo_erro
     return POSLO_OK;
 }
 
+// d_pk <- the powers 16^i Y, unless it already holds them (one chain per Y
+// serves the radix-16, 256 and 2^16 tables).
+int y_powers(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err) {
+    if (ctx->pk_owner == 2 && std::memcmp(ctx->pk_key, y, 32) == 0) return POSLO_OK;
+    uint8_t* d_y;
+    UPLOAD(b_y, y, 32, d_y);
+    launch_table_powers(d_y, ctx->d_pk, d_flags, ctx->stream);
+    ctx->pk_owner = 2;
+    std::memcpy(ctx->pk_key, y, 32);
+    ctx->launches += 1;
+    return POSLO_OK;
+}
+
 int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_error* err, bool wide = false,
                   bool xwide = false) {
     if (!ctx->d_pk) CU(cudaMalloc(&ctx->d_pk, 64 * kGptBytes));
+    // the generator's tables first (one power chain for all of them), then Y's
     if (!ctx->d_tabB) {
         int rc = gen_table(ctx, 0, d_flags, &ctx->d_tabB, err);
+        if (rc) return rc;
+    }
+    if (wide && !ctx->d_tabB256) {
+        int rc = gen_table(ctx, 1, d_flags, &ctx->d_tabB256, err);
+        if (rc) return rc;
+    }
+    if (xwide && !ctx->d_tabB16) {
+        int rc = gen_table(ctx, 2, d_flags, &ctx->d_tabB16, err);
         if (rc) return rc;
     }
     if (!ctx->d_tabY) CU(cudaMalloc(&ctx->d_tabY, kCombTableBytes));
     if (!ctx->tabY_valid || std::memcmp(ctx->tabY_key, y, 32) != 0) {
         uint8_t* d_y;
         UPLOAD(b_y, y, 32, d_y);
-        launch_build_table(d_y, ctx->d_pk, ctx->d_tabY, d_flags, ctx->stream);
+        launch_table_powers(d_y, ctx->d_pk, d_flags, ctx->stream);
+        ctx->pk_owner = 2;
+        std::memcpy(ctx->pk_key, y, 32);
+        launch_table_fill(0, ctx->d_pk, ctx->d_tabY, ctx->stream);
         ctx->launches += 2;
         int bad = 0;
         CU(cudaMemcpyAsync(&bad, d_flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -905,10 +930,10 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
         }
         if (!ctx->d_tabY256) CU(cudaMalloc(&ctx->d_tabY256, kComb256TableBytes));
         if (!ctx->tabY256_valid || std::memcmp(ctx->tabY256_key, y, 32) != 0) {
-            uint8_t* d_y;
-            UPLOAD(b_y, y, 32, d_y);  // Y already validated by the radix-16 build above
-            launch_build_table256(d_y, ctx->d_pk, ctx->d_tabY256, d_flags, ctx->stream);
-            ctx->launches += 2;
+            const int rc = y_powers(ctx, y, d_flags, err);  // Y already validated by the radix-16 build above
+            if (rc) return rc;
+            launch_table_fill(1, ctx->d_pk, ctx->d_tabY256, ctx->stream);
+            ctx->launches += 1;
             std::memcpy(ctx->tabY256_key, y, 32);
             ctx->tabY256_valid = true;
         }
@@ -920,10 +945,10 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
         }
         if (!ctx->d_tabY16) CU(cudaMalloc(&ctx->d_tabY16, kComb16TableBytes));
         if (!ctx->tabY16_valid || std::memcmp(ctx->tabY16_key, y, 32) != 0) {
-            uint8_t* d_y;
-            UPLOAD(b_y, y, 32, d_y);  // Y already validated by the radix-16 build above
-            launch_build_table65536(d_y, ctx->d_pk, ctx->d_tabY16, d_flags, ctx->stream);
-            ctx->launches += 2;
+            const int rc = y_powers(ctx, y, d_flags, err);  // Y already validated by the radix-16 build above
+            if (rc) return rc;
+            launch_table_fill(2, ctx->d_pk, ctx->d_tabY16, ctx->stream);
+            ctx->launches += 1;
             std::memcpy(ctx->tabY16_key, y, 32);
             ctx->tabY16_valid = true;
         }

@@ -54,7 +54,9 @@ struct poslo_gpu_ctx {
     void* d_tabY = nullptr;
     void* d_tabB256 = nullptr;  // radix-256 combs for batched checks (built on first use)
     void* d_tabY256 = nullptr;
-    void* d_pk = nullptr;
+    void* d_pk = nullptr;          // 64 powers 16^i P of the last point P tables were built for
+    int pk_owner = 0;              // whose powers d_pk holds: 0 none, 1 the generator, 2 Y = pk_key
+    uint8_t pk_key[32] = {};
     uint8_t tabY_key[32] = {};
     bool tabY_valid = false;
     uint8_t tabY256_key[32] = {};

@@ -137,7 +137,7 @@ __global__ void k_table_fill256(const gpt* __restrict__ pk, gcached* __restrict_
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 32 * 128) return;
     const int k = t >> 7, m = (t & 127) + 1;
-    const gpt base = pk[k];
+    const gpt base = pk[2 * k];  // pk[i] = 16^i P: 256^k P = pk[2k]
     gpt q = pt_identity();
     for (int b = 7; b >= 0; b--) {
         q = pt_dbl(q);
@@ -146,21 +146,50 @@ __global__ void k_table_fill256(const gpt* __restrict__ pk, gcached* __restrict_
     tab[t] = pt_to_cached(q);
 }
 
-// Radix-2^16 fill: thread t = 32768 k + (m - 1) writes m 2^(16k) P for
-// m = 1 .. 32768 (signed digits |d| <= 2^15), by double-and-add on the bits
-// of m (<= 16 doublings + 16 additions) and one inversion to affine Niels.
-__global__ void k_table_fill65536(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
+// Radix-2^16 fill: m 2^(16k) P for m = 1 .. 32768 (signed digits |d| <=
+// 2^15), 16 bases 2^(16k) P = pk[4k]. Thread t owns a run of kRun consecutive
+// multiples m0 .. m0 + kRun - 1 of one base: m0 B by double-and-add, then one
+// mixed addition of B per multiple, the run's Z coordinates inverted together
+// (Montgomery's trick: one inversion and 3 multiplications per point instead
+// of an inversion per point). The table slots hold (X, Y, Z) until the
+// backward pass overwrites them with the affine Niels form.
+constexpr uint32_t kRun = 32;
+__global__ void __launch_bounds__(128) k_table_fill65536(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= 16u * 32768u) return;
-    const uint32_t k = t >> 15, m = (t & 32767u) + 1;
-    const gpt base = pk[k];
+    if (t >= 16u * (32768u / kRun)) return;
+    const uint32_t k = t / (32768u / kRun), m0 = (t % (32768u / kRun)) * kRun + 1;
+    const gpt base = pk[4 * k];  // pk[i] = 16^i P: 2^(16k) P = pk[4k]
+    const gcached bc = pt_to_cached(base);
     gpt q = pt_identity();
 #pragma unroll 1
     for (int b = 15; b >= 0; b--) {
         q = pt_dbl(q);
-        if ((m >> b) & 1) q = pt_add(q, base);
+        if ((m0 >> b) & 1) q = pt_add(q, base);
     }
-    tab[t] = pt_to_cached(q);
+    gcached* out = tab + (size_t)k * 32768u + (m0 - 1);
+    fe pre[kRun];  // prefix products of Z (local memory)
+#pragma unroll 1
+    for (uint32_t r = 0; r < kRun; r++) {
+        out[r].YpX = q.X;
+        out[r].YmX = q.Y;
+        out[r].T2d = q.Z;
+        pre[r] = r ? fe_mul(pre[r - 1], q.Z) : q.Z;
+        if (r + 1 < kRun) q = pt_add_cached(q, bc);
+    }
+    const fe d2 = FE_CONST(FE_D2_LIMBS);
+    fe inv = fe_invert(pre[kRun - 1]);
+#pragma unroll 1
+    for (int r = (int)kRun - 1; r >= 0; r--) {
+        const fe X = out[r].YpX, Y = out[r].YmX, Z = out[r].T2d;
+        const fe zi = r ? fe_mul(inv, pre[r - 1]) : inv;
+        if (r) inv = fe_mul(inv, Z);
+        const fe x = fe_mul(X, zi), y = fe_mul(Y, zi);
+        gcached c;
+        c.YpX = fe_add(y, x);
+        c.YmX = fe_sub(y, x);
+        c.T2d = fe_mul(fe_mul(x, y), d2);
+        out[r] = c;
+    }
 }
 
 __global__ void k_table_fill(const gpt* __restrict__ pk, gcached* __restrict__ tab) {
@@ -619,21 +648,37 @@ void launch_point_validate(const uint8_t* d_pts, uint32_t n, uint8_t* d_ok, cuda
     k_validate<<<(n + 127) / 128, 128, 0, s>>>(d_pts, n, d_ok);
 }
 
+// One chain of powers pk[i] = 16^i P (i < 64) serves every comb radix
+// (256^k P = pk[2k], 2^(16k) P = pk[4k]): computed once per point.
+void launch_table_powers(const uint8_t* d_enc, void* d_pk, int* d_bad, cudaStream_t s) {
+    k_table_pow<4><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk), d_bad);
+}
+
+void launch_table_fill(int kind, const void* d_pk, void* d_table, cudaStream_t s) {
+    const gpt* pk = static_cast<const gpt*>(d_pk);
+    gcached* tab = static_cast<gcached*>(d_table);
+    if (kind == 0)
+        k_table_fill<<<4, 128, 0, s>>>(pk, tab);
+    else if (kind == 1)
+        k_table_fill256<<<32, 128, 0, s>>>(pk, tab);
+    else
+        k_table_fill65536<<<16 * (32768 / kRun) / 128, 128, 0, s>>>(pk, tab);
+}
+
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s) {
-    k_table_pow<4><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
-    k_table_fill<<<4, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
+    launch_table_powers(d_enc, d_pk_scratch, d_bad, s);
+    launch_table_fill(0, d_pk_scratch, d_table, s);
 }
 
 void launch_build_table65536(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s) {
-    k_table_pow<16><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
-    k_table_fill65536<<<16 * 32768 / 128, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch),
-                                                       static_cast<gcached*>(d_table));
+    launch_table_powers(d_enc, d_pk_scratch, d_bad, s);
+    launch_table_fill(2, d_pk_scratch, d_table, s);
 }
 
 void launch_build_table256(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad, cudaStream_t s) {
-    k_table_pow<8><<<1, 32, 0, s>>>(d_enc, static_cast<gpt*>(d_pk_scratch), d_bad);
-    k_table_fill256<<<32, 128, 0, s>>>(static_cast<const gpt*>(d_pk_scratch), static_cast<gcached*>(d_table));
+    launch_table_powers(d_enc, d_pk_scratch, d_bad, s);
+    launch_table_fill(1, d_pk_scratch, d_table, s);
 }
 
 void launch_group_check_comb(const void* d_tabY, const void* d_tabB, const void* d_tabY256,

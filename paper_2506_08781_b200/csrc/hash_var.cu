@@ -229,8 +229,16 @@ __global__ void __launch_bounds__(kVarT, POSLO_VAR_MINB) k_hash_s1_var(EntryLayo
     v.slot[24] = 0;
     v.slot[29] = 0x80u;
     v.slot[30] = 0;
+    // Sorted position of this thread's entry in iteration it: the tile's 128
+    // positions of an iteration go to the 4 warps in a rotating order, so every
+    // warp takes each rank (longest .. shortest quarter) equally often and the
+    // warps of a CTA finish together at the reduction barrier (a fixed order
+    // gave warp 0 the longest quarter every time).
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll 1
-    for (uint32_t i = threadIdx.x; i < count; i += kVarT) {
+    for (uint32_t base = 0, it = 0; base < count; base += kVarT, it++) {
+        const uint32_t i = base + (((warp + it) & (kVarT / 32 - 1)) << 5) + lane;
+        if (i >= count) continue;
         const uint32_t j = j0 + order[i];
         const uint64_t ent = ebase + j;
         uint64_t L;

@@ -131,6 +131,10 @@ constexpr size_t kCombTableBytes = 512 * kCachedBytes;      // radix 16: 64 x 8 
 constexpr size_t kComb256TableBytes = 4096 * kCachedBytes;  // radix 256: 32 x 128 points
 constexpr size_t kComb16TableBytes = (size_t)16 * 32768 * kCachedBytes;  // radix 2^16: 16 x 32768 points (60 MiB)
 constexpr uint32_t kCtaCheckMax = 1024;          // larger batches use one thread per check (radix-256 combs)
+// pk[i] = 16^i P, i < 64 (P decoded from d_enc, or the generator); then the
+// comb table of radix kind 0 = 16, 1 = 256, 2 = 2^16 from those powers.
+void launch_table_powers(const uint8_t* d_enc, void* d_pk, int* d_bad, cudaStream_t s);
+void launch_table_fill(int kind, const void* d_pk, void* d_table, cudaStream_t s);
 void launch_build_table(const uint8_t* d_enc, void* d_pk_scratch, void* d_table, int* d_bad,
                         cudaStream_t s);
 // commit_check via comb tables of Y and alpha (CTA-per-check for n <= 1024,

@@ -95,7 +95,7 @@ class ColdCryptoData:
         batches = {i0 + k: list(m) for k, m in enumerate(msgs_list)}
         sig_of = {i0 + k: s for k, s in enumerate(sigs)}
         # umbrella pieces: cut where an epoch index is a multiple of w
-        cuts = [0] + [k for k in range(1, n) if (i0 + k) % w == 0] + [n]
+        cuts = [0] + list(range((-i0) % w or w, n, w)) + [n]  # k >= 1 with (i0 + k) % w == 0
         verdicts, parts = self.v.distill_coarse(pk, batches, sig_of, cuts)
         has = [any(verdicts[cuts[g]:cuts[g + 1]]) for g in range(len(cuts) - 1)]
         for k in range(n):
@@ -186,7 +186,7 @@ class ColdCryptoData:
         fb = F.FineBatch(self.suite.suite, msgs, [None if sg.carries_ds() else sg.tail for sg in sigs], derive,
                          [i0 + k for k in range(n)], [ss[-1].tail for ss in sigs_list], None, self.suite.depth())
         verdicts = F.fine_verify(self.v, fb, pk.y, [sg.s for sg in sigs], [sg.r for sg in sigs])
-        cuts = [0] + [k * n2 for k in range(1, n) if (i0 + k) % w == 0] + [n * n2]
+        cuts = [0] + [k * n2 for k in range((-i0) % w or w, n, w)] + [n * n2]
         parts = self.v.segfold([sg.s for sg in sigs], [sg.r for sg in sigs], verdicts, cuts)
         has = [any(verdicts[cuts[g]:cuts[g + 1]]) for g in range(len(cuts) - 1)]
         for t, ok in enumerate(verdicts):

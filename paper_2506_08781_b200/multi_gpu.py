@@ -214,7 +214,8 @@ def sharded_epoch_verdicts(v: api.Verifier, cb, y: bytes, s_hats, r_hats, group=
 # ---------------------------------------------------------------- distillation
 def umbrella_cuts(first_epoch: int, n_epochs: int, w: int) -> List[int]:
     """Batch positions where this shard's epochs cross an umbrella boundary."""
-    return [0] + [k for k in range(1, n_epochs) if (first_epoch + k) % w == 0] + [n_epochs]
+    first = (-first_epoch) % w or w  # smallest k >= 1 with (first_epoch + k) % w == 0
+    return [0] + list(range(first, n_epochs, w)) + [n_epochs]
 
 
 def sharded_distill(v: api.Verifier, cb, first_epoch: int, y: bytes, s_hats, r_hats, w: int, group=None,
