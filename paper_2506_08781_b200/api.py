@@ -15,7 +15,7 @@ import ctypes
 import struct
 import threading
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -503,6 +503,23 @@ class Verifier:
                     [(sr_[32 * g:32 * g + 32], rr[32 * g:32 * g + 32], er[32 * g:32 * g + 32]) for g in range(ng)])
         return ([bool(vr[k]) for k in range(len(eps))],
                 [(sr_[32 * g:32 * g + 32], rr[32 * g:32 * g + 32]) for g in range(ng)])
+
+    def distill_step(self, pk: PoslocPublicKey, epoch: int, msgs: Sequence[bytes], sig: "EpochSignature",
+                     acc: Sequence[Tuple[bytes, bytes]]):
+        """ONE distill_epoch (distiller.cpp:60-89) in one device round trip
+        (poslo_gpu_distill_step): returns (verdict, [valid (s, r), umbrella (s, r)])
+        with (sig.s_hat, pk.r_hats[epoch]) folded into both aggregates when valid."""
+        pb = PackedBatch(pk.suite.suite, pk.suite.n2, {epoch: list(msgs)}, sig.ds)
+        cb = pb.cstruct()
+        acc_s = acc[0][0] + acc[1][0]
+        acc_r = acc[0][1] + acc[1][1]
+        v = ctypes.c_uint8(0)
+        out_s = ctypes.create_string_buffer(64)
+        out_r = ctypes.create_string_buffer(64)
+        self._call(self._lib.poslo_gpu_distill_step, ctypes.byref(cb), _buf(pk.y), _buf(sig.s_hat),
+                   _buf(pk.r_hats[epoch]), _buf(acc_s), _buf(acc_r), ctypes.byref(v), out_s, out_r)
+        rs, rr = out_s.raw, out_r.raw
+        return bool(v.value), [(rs[:32], rr[:32]), (rs[32:], rr[32:])]
 
     def segfold(self, scalars: Sequence[bytes], points: Sequence[bytes], mask: Optional[Sequence[bool]],
                 seg: Sequence[int]):

@@ -1865,43 +1865,29 @@ int poslo_gpu_distill_step(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     CU(cudaMemsetAsync(d_flags, 0, 16, s));
     int rc = ensure_tables(ctx, y, d_flags, err);
     if (rc) return rc;
-    // items [valid acc, item, umbrella acc, item], mask [1, v, 1, v]
-    uint8_t items[256];
+    // scalars [valid acc, s_hat, umbrella acc], points [valid acc, R-hat, umbrella acc]
+    uint8_t items[192];
     std::memcpy(items, acc_s, 32);
     std::memcpy(items + 32, s_hat, 32);
     std::memcpy(items + 64, acc_s + 32, 32);
-    std::memcpy(items + 96, s_hat, 32);
-    std::memcpy(items + 128, acc_r, 32);
-    std::memcpy(items + 160, r_hat, 32);
-    std::memcpy(items + 192, acc_r + 32, 32);
-    std::memcpy(items + 224, r_hat, 32);
+    std::memcpy(items + 96, acc_r, 32);
+    std::memcpy(items + 128, r_hat, 32);
+    std::memcpy(items + 160, acc_r + 32, 32);
     uint8_t* d_items;
     UPLOAD(b_s, items, sizeof items, d_items);
-    const uint32_t* d_sc = reinterpret_cast<const uint32_t*>(d_items);
-    const uint8_t* d_pt = d_items + 128;
     Prepared P;
     rc = run_hash(ctx, b, P, err);
     if (rc) return rc;
-    uint8_t *d_verdict, *d_mask;
+    uint8_t *d_verdict, *d_out_r;
+    uint32_t* d_out_s;
     ENSURE(b_verdict, 1, d_verdict);
-    ENSURE(b_mask, 4, d_mask);
-    launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, 1, P.d_etilde, d_sc + 8,
-                            d_pt + 32, nullptr, d_verdict, s);
-    CU(cudaMemsetAsync(d_mask, 1, 4, s));
-    CU(cudaMemcpyAsync(d_mask + 1, d_verdict, 1, cudaMemcpyDeviceToDevice, s));
-    CU(cudaMemcpyAsync(d_mask + 3, d_verdict, 1, cudaMemcpyDeviceToDevice, s));
-    static const uint64_t seg64[3] = {0, 2, 4};
-    static const uint32_t seg32[3] = {0, 2, 4};
-    uint64_t* d_seg;
-    uint32_t *d_seg32, *d_out_s;
-    uint8_t* d_out_r;
-    UPLOAD(b_seg, seg64, sizeof seg64, d_seg);
-    UPLOAD(b_seg32, seg32, sizeof seg32, d_seg32);
     ENSURE(b_out_s, 16, d_out_s);
     ENSURE(b_out_r, 64, d_out_r);
-    launch_segsum_mod_l(d_sc, d_seg, 2, d_mask, d_out_s, s, /*skip_val=*/0);
-    launch_segfold_points(d_pt, d_seg32, 2, d_mask, d_out_r, d_flags + 1, s);
-    ctx->launches += 3;
+    // check + both folds in one CTA: the decodes run beside the comb, the
+    // verdict is a projective comparison, the two new aggregates encode at once
+    launch_distill_step(ctx->d_tabY, ctx->d_tabB, P.d_etilde, reinterpret_cast<const uint32_t*>(d_items),
+                        d_items + 96, d_verdict, d_out_s, d_out_r, d_flags + 1, s);
+    ctx->launches += 1;
     PinnedStage* st = ctx->stage;
     CU(cudaMemcpyAsync(&st->err_key, ctx->b_err.p, 8, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(&st->verdict, d_verdict, 1, cudaMemcpyDeviceToHost, s));

@@ -6,6 +6,7 @@
 #define POSLO_FE_CALL 1  // out-of-line field multiplication in the group kernels (i-cache)
 #include "poslo_internal.h"
 #include "ristretto.cuh"
+#include "scalar.cuh"
 
 namespace poslo_gpu {
 
@@ -579,7 +580,97 @@ __global__ void __launch_bounds__(128) k_segfold_points(const uint8_t* __restric
     }
 }
 
+// One distill_epoch step (poslo_gpu_distill_step) in one CTA of 160 threads:
+// warps 0-3 evaluate e Y + s B on the radix-16 combs (thread t < 64 window t
+// of e on Y's table, 64 + t window t of s on alpha's) while warp 4 decodes R-hat
+// and the two running aggregates' points in parallel; the verdict is the
+// projective ristretto equality of e Y + s B and R-hat (no encode on the
+// check's path), and on a valid verdict R-hat is added to both aggregates and
+// the two sums encoded by two threads at once (Scalar::add / group_combine,
+// distiller.cpp:45-53). in: s_items = [acc_s0, s_hat, acc_s1] (8 limbs each),
+// pts = [acc_r0, r_hat, acc_r1] encodings. out: verdict, out_s (2 x 8 limbs),
+// out_r (2 x 32 B); *bad on an undecodable point.
+__global__ void __launch_bounds__(160) k_distill_step(const gcached* __restrict__ tabY,
+                                                      const gcached* __restrict__ tabB,
+                                                      const uint32_t* __restrict__ e, const uint32_t* __restrict__ s_items,
+                                                      const uint8_t* __restrict__ pts, uint8_t* __restrict__ verdict,
+                                                      uint32_t* __restrict__ out_s, uint8_t* __restrict__ out_r,
+                                                      int* __restrict__ bad) {
+    __shared__ int8_t dig[128];
+    __shared__ gpt sh[128];
+    __shared__ gpt dec[3];
+    __shared__ int dec_ok[3];
+    __shared__ int s_verdict;
+    const int t = threadIdx.x;
+    if (t < 2) {
+        uint32_t v[8];
+        const uint32_t* src = t == 0 ? e : s_items + 8;
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = src[k];
+        int8_t d[64];
+        sc_signed_radix16(v, d);
+        for (int k = 0; k < 64; k++) dig[64 * t + k] = d[k];
+    } else if (t >= 128 && t < 131) {  // warp 4: the three decodes, concurrently with the comb
+        uint8_t b[32];
+        load32(pts + 32 * (t - 128), b);
+        gpt P;
+        const bool ok = rist_decode(b, P);
+        dec[t - 128] = ok ? P : pt_identity();
+        dec_ok[t - 128] = ok;
+    }
+    __syncthreads();
+    if (t < 128) {
+        const int dgt = dig[t];
+        gpt acc = pt_identity();
+        if (dgt) acc = pt_add_cached(acc, table_pick(t < 64 ? tabY : tabB, t & 63, dgt));
+        sh[t] = acc;
+    }
+    __syncthreads();
+    for (int w = 64; w >= 1; w >>= 1) {
+        if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
+        __syncthreads();
+    }
+    if (t == 0) {
+        // an R-hat that does not decode never equals a canonical encoding (false,
+        // as the encoding comparison); undecodable aggregates are a format error
+        if (!dec_ok[0] || !dec_ok[2]) atomicOr(bad, 1);
+        s_verdict = dec_ok[0] && dec_ok[1] && dec_ok[2] && rist_equal(sh[0], dec[1]);
+        *verdict = (uint8_t)s_verdict;
+    }
+    __syncthreads();
+    const bool v = s_verdict != 0;
+    if (t < 2) {  // the two aggregates: point add + encode, one thread each
+        const int a = 2 * t;  // item 0 = valid aggregate, item 2 = umbrella aggregate
+        uint8_t o[32];
+        if (v) {
+            rist_encode(pt_add(dec[a], dec[1]), o);
+        } else {
+            load32(pts + 32 * a, o);
+        }
+#pragma unroll
+        for (int k = 0; k < 32; k++) out_r[32 * t + k] = o[k];
+    } else if (t == 32 || t == 33) {  // scalars
+        const int i = t - 32;
+        uint32_t a[8], b[8], r[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            a[k] = s_items[16 * i + k];
+            b[k] = v ? s_items[8 + k] : 0u;
+        }
+        sc_add(a, b, r);
+#pragma unroll
+        for (int k = 0; k < 8; k++) out_s[8 * i + k] = r[k];
+    }
+}
+
 }  // namespace
+
+void launch_distill_step(const void* d_tabY, const void* d_tabB, const uint32_t* d_e, const uint32_t* d_s_items,
+                         const uint8_t* d_pts, uint8_t* d_verdict, uint32_t* d_out_s, uint8_t* d_out_r, int* d_bad,
+                         cudaStream_t s) {
+    k_distill_step<<<1, 160, 0, s>>>(static_cast<const gcached*>(d_tabY), static_cast<const gcached*>(d_tabB), d_e,
+                                     d_s_items, d_pts, d_verdict, d_out_s, d_out_r, d_bad);
+}
 
 void launch_decode_points(const uint8_t* d_enc, uint32_t n, void* d_pts, uint8_t* d_ok, cudaStream_t s) {
     if (!n) return;

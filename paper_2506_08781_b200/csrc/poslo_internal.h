@@ -131,6 +131,11 @@ constexpr size_t kCombTableBytes = 512 * kCachedBytes;      // radix 16: 64 x 8 
 constexpr size_t kComb256TableBytes = 4096 * kCachedBytes;  // radix 256: 32 x 128 points
 constexpr size_t kComb16TableBytes = (size_t)16 * 32768 * kCachedBytes;  // radix 2^16: 16 x 32768 points (60 MiB)
 constexpr uint32_t kCtaCheckMax = 1024;          // larger batches use one thread per check (radix-256 combs)
+// One coarse distill step on the radix-16 combs (k_distill_step): s_items =
+// [acc_s0, s_hat, acc_s1], pts = [acc_r0, r_hat, acc_r1] (encodings).
+void launch_distill_step(const void* d_tabY, const void* d_tabB, const uint32_t* d_e, const uint32_t* d_s_items,
+                         const uint8_t* d_pts, uint8_t* d_verdict, uint32_t* d_out_s, uint8_t* d_out_r, int* d_bad,
+                         cudaStream_t s);
 // pk[i] = 16^i P, i < 64 (P decoded from d_enc, or the generator); then the
 // comb table of radix kind 0 = 16, 1 = 256, 2 = 2^16 from those powers.
 void launch_table_powers(const uint8_t* d_enc, void* d_pk, int* d_bad, cudaStream_t s);

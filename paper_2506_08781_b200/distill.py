@@ -142,6 +142,34 @@ class ColdCryptoData:
             else:
                 self.umb_acc, self.umb_nonempty = acc, nonempty
 
+    def distill_epoch_step(self, pk: api.PoslocPublicKey, msgs: Sequence[bytes], sig: api.EpochSignature):
+        """distill_epoch (distiller.cpp:60-89) through the single-epoch device
+        step (poslo_gpu_distill_step), the route of the C++ drop-in
+        (host/distiller_gpu.cpp): same state and errors as distill_epoch."""
+        if self.scheme != COARSE:
+            raise StateError("coarse distillation on a fine-grained stream")
+        if self.next_epoch >= self.suite.n1:
+            raise StateError("stream already complete")
+        i = self.next_epoch
+        if i not in pk.r_hats:
+            raise StateError(f"epoch {i} already distilled (commitment gone)")
+        if len(msgs) != self.suite.n2:
+            raise StateError("every batch must hold exactly n2 entries")
+        ok, (valid, umb) = self.v.distill_step(pk, i, msgs, sig, [self.valid_, self.umb_acc])
+        if ok:
+            self.valid_, self.umb_acc = valid, umb
+            self.has_valid = True
+            self.umb_nonempty = True
+        else:
+            self.invalid.append((i, sig.s_hat, pk.r_hats[i]))
+        del pk.r_hats[i]
+        self.ds = sig.ds
+        self.next_epoch += 1
+        w = self.umbrella_width()
+        if self.next_epoch % w == 0:
+            self.umbrellas.append(((self.next_epoch - 1) // w, *self.umb_acc))
+            self.umb_acc, self.umb_nonempty = (ZERO, IDENTITY), False
+
     # -- fine-grained distillation (distiller.cpp:91-129)
     def distill_epoch_fine(self, pk, msgs: Sequence[bytes], sigs):
         self.distill_epochs_fine(pk, [msgs], [sigs])

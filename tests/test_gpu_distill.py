@@ -20,14 +20,19 @@ def _objs(name):
 
 
 @pytest.mark.parametrize("name", STREAMS)
-@pytest.mark.parametrize("chunk", [0, 1, 3])
+@pytest.mark.parametrize("chunk", [0, 1, 3, -1])
 def test_distill_ccd_bytes_match_reference(verifier, name, chunk):
+    """chunk -1: epoch by epoch through poslo_gpu_distill_step (the C++
+    drop-in's route: check and both aggregate folds in one device call)."""
     from paper_2506_08781_b200.distill import ColdCryptoData
     st, suite, pk, sigs = _objs(name)
     ccd = ColdCryptoData(ord("C"), suite, verifier)
     msgs = [st.batches[i] for i in range(st.n1)]
-    step = chunk or st.n1
-    for k in range(0, st.n1, step):
+    if chunk < 0:
+        for i in range(st.n1):
+            ccd.distill_epoch_step(pk, msgs[i], sigs[i])
+    step = chunk if chunk > 0 else st.n1
+    for k in range(0, st.n1 if chunk >= 0 else 0, step):
         ccd.distill_epochs(pk, msgs[k:k + step], sigs[k:k + step])
     ccd.finalize()
     assert [i for i, _, _ in ccd.invalid] == st.d["invalid_epochs"]
