@@ -956,15 +956,30 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
     return POSLO_OK;
 }
 
-// The batched checks on the widest tables ensure_tables built: with decoded
-// R-hat (d_pts, d_ok), 8 lanes per check (radix 256 or 2^16); without, one
-// thread per check on the radix-2^16 combs comparing encodings (d_r).
+// POSLO_CHECK16=split: radix-2^16 checks against decoded R-hat as 8 lanes per
+// check (k_check_split16) instead of a thread per check (A/B knob).
+static bool check16_split() {
+    const char* e = std::getenv("POSLO_CHECK16");
+    return e && std::strcmp(e, "split") == 0;
+}
+
+static bool epoch_decode16() {
+    const char* e = std::getenv("POSLO_EPOCH_DECODE");
+    return !(e && std::strcmp(e, "0") == 0);
+}
+
+// The batched checks on the widest tables ensure_tables built: radix 2^16, a
+// thread per check, comparing ristretto classes against R-hat decoded ahead
+// (d_pts, d_ok) or, without it, encodings (d_r); radix 256, 8 lanes per check
+// against decoded R-hat.
 void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
                    const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st) {
     if (xwide && !d_pts)
         launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, nullptr, d_verdict, st);
-    else if (xwide)
+    else if (xwide && check16_split())
         launch_check_split16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
+    else if (xwide)
+        launch_check_thread16d(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
     else
         launch_check_split(ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
 }
@@ -1591,10 +1606,13 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         if (rc) return rc;
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
-        if (n < comb16_min()) {  // radix 256: 8-lane checks against R-hat decoded here
+        // R-hat decoded on the side stream while the log is hashed: the checks
+        // then compare ristretto classes (POSLO_EPOCH_DECODE=0: radix-2^16
+        // checks encode instead, A/B knob)
+        if (n < comb16_min() || epoch_decode16()) {
             rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
             if (rc) return rc;
-        }  // radix 2^16: thread per check, encode compare (cheaper than decode + 8 lanes)
+        }
     }
     Prepared P;
     uint8_t* d_vpipe = nullptr;
@@ -1749,10 +1767,8 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
     }
-    // R-hat decoded once, on the side stream during hashing, for the fold (and
-    // the 8-lane radix-256 checks); radix-2^16 batches check thread per check
-    // (encode compare), cheaper than 8 lanes on the decoded point
-    const bool xw = split && n >= comb16_min();
+    // R-hat decoded once, on the side stream during hashing, for the fold and
+    // the checks (ristretto class compare: no encoding per check)
     if (split) {
         rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
         if (rc) return rc;
@@ -1767,9 +1783,8 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
             CU(cudaEventRecord(ctx->ev_side[0], hs));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
-                          d_r + 32 * (size_t)e0,
-                          !xw ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
-                          !xw ? d_ok + e0 : nullptr, d_verdict + e0, ctx->side);
+                          d_r + 32 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
+                          d_ok + e0, d_verdict + e0, ctx->side);
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1788,7 +1803,7 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
         CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
     } else if (split) {
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, xw ? nullptr : d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
         if (rc) return rc;
     } else {
         launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s,

@@ -285,6 +285,33 @@ __global__ void __launch_bounds__(128) k_check_thread16(const gcached* __restric
     }
 }
 
+// k_check_thread16 against R-hat decoded ahead (k_decode_pts, side stream):
+// the ristretto class compare (RFC 9496 4.3.3, 4 multiplications) replaces
+// the encoding's inverse square root, about half of a thread-per-check
+// check. A failed decode can never equal a canonical encoding: verdict 0.
+#ifndef POSLO_CHECK16D_MINB
+#define POSLO_CHECK16D_MINB 1
+#endif
+__global__ void __launch_bounds__(128, POSLO_CHECK16D_MINB) k_check_thread16d(const gcached* __restrict__ tabY,
+                                                         const gcached* __restrict__ tabB, uint32_t n,
+                                                         const uint32_t* __restrict__ e,
+                                                         const uint32_t* __restrict__ s,
+                                                         const gpt* __restrict__ R,
+                                                         const uint8_t* __restrict__ rok,
+                                                         uint8_t* __restrict__ verdict) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t v[8];
+    gpt acc = pt_identity();
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = e[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabY, v);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = s[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabB, v);
+    verdict[i] = (rok[i] && rist_equal(acc, R[i])) ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict__ tabY,
                                                       const gcached* __restrict__ tabB, uint32_t n,
                                                       const uint32_t* __restrict__ e,
@@ -694,6 +721,15 @@ void launch_check_thread16(const void* d_tabY16, const void* d_tabB16, uint32_t 
     k_check_thread16<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
                                                      static_cast<const gcached*>(d_tabB16), n, d_e, d_s, d_r, d_enc,
                                                      d_verdict);
+}
+
+void launch_check_thread16d(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                            const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                            cudaStream_t s) {
+    if (!n) return;
+    k_check_thread16d<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
+                                                      static_cast<const gcached*>(d_tabB16), n, d_e, d_s,
+                                                      static_cast<const gpt*>(d_pts), d_ok, d_verdict);
 }
 
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,

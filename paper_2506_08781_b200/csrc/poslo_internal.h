@@ -177,6 +177,9 @@ void launch_build_table65536(const uint8_t* d_enc, void* d_pk_scratch, void* d_t
 void launch_check_thread16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
                            const uint32_t* d_s, const uint8_t* d_r, uint8_t* d_enc, uint8_t* d_verdict,
                            cudaStream_t s);
+void launch_check_thread16d(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
+                            const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
+                            cudaStream_t s);
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
                           const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
                           cudaStream_t s);

@@ -468,16 +468,23 @@ def test_chunked_varlen_host_path_matches_device_resident(verifier):
     assert a == h
 
 
-@pytest.mark.parametrize("comb16", [False, True])
+@pytest.mark.parametrize("comb16", [False, "thread", "encode", "split"])
 @pytest.mark.parametrize("resident", [0, 1])
 def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
     """> 1024 per-epoch checks take the split path (R-hat decoded on a side
-    stream, 8 lanes per check; device-resident batches also pipeline the
-    checks behind the hashing): signatures from the reference derivation
-    (signer.py) verify, and exactly the tampered epochs fail — on the
-    radix-256 combs and (comb16, POSLO_COMB16_MIN = 1) on the radix-2^16
-    combs large batches take by default."""
+    stream; device-resident batches also pipeline the checks behind the
+    hashing): signatures from the reference derivation (signer.py) verify, and
+    exactly the tampered epochs fail — on the radix-256 combs (8 lanes per
+    check) and (POSLO_COMB16_MIN = 1) on the radix-2^16 combs large batches
+    take by default, in each check form: a thread per check against decoded
+    R-hat (default), encoding compare (POSLO_EPOCH_DECODE=0), 8 lanes per
+    check (POSLO_CHECK16=split). Device-resident batches also run
+    distill_coarse (whose checks always use the decoded R-hat)."""
     monkeypatch.setenv("POSLO_COMB16_MIN", "1" if comb16 else "4294967295")
+    if comb16 == "encode":
+        monkeypatch.setenv("POSLO_EPOCH_DECODE", "0")
+    if comb16 == "split":
+        monkeypatch.setenv("POSLO_CHECK16", "split")
     import ctypes
 
     import torch
@@ -518,6 +525,13 @@ def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
         verifier._call(verifier._lib.poslo_gpu_epoch_verify, ctypes.byref(b), pk.y, ctypes.c_void_p(s_dev.data_ptr()),
                        ctypes.c_void_p(r_dev.data_ptr()), verd, None)
         got = [bool(x) for x in verd.raw]
+        seg = np.array([0, 1000, n1], dtype=np.uint32)
+        dverd = ctypes.create_string_buffer(n1)
+        so, ro = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+        verifier._call(verifier._lib.poslo_gpu_distill_coarse, ctypes.byref(b), pk.y,
+                       ctypes.c_void_p(s_dev.data_ptr()), ctypes.c_void_p(r_dev.data_ptr()),
+                       ctypes.c_void_p(seg.ctypes.data), 2, dverd, so, ro)
+        assert dverd.raw == verd.raw
     assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
 
 
