@@ -350,7 +350,10 @@ __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict_
 // over 8 lanes (8 radix-256 windows each, 4 of e and 4 of s) and a 3-level
 // shuffle tree, plus a 4-multiplication compare: no inverse square root on
 // the critical path and 8x the threads of the thread-per-check kernel.
-__global__ void __launch_bounds__(128) k_decode_pts(const uint8_t* __restrict__ enc, uint32_t n,
+#ifndef POSLO_DECODE_MINB
+#define POSLO_DECODE_MINB 1
+#endif
+__global__ void __launch_bounds__(128, POSLO_DECODE_MINB) k_decode_pts(const uint8_t* __restrict__ enc, uint32_t n,
                                                     gpt* __restrict__ out, uint8_t* __restrict__ ok) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
