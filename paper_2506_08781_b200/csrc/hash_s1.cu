@@ -4,6 +4,26 @@
 #include "entry_hash.cuh"
 #include "tile_common.cuh"
 
+// Pipe assignment of the lean kernel's SHA rounds (sha256.cuh SHA_RND_SEL).
+// 5: every addition on the FMA pipe, h + W + K included, so the ALU pipe
+// carries only the rotations and LOP3s (12.05 -> 11.52 ms per 2^26 entries
+// vs 2, which keeps h + W + K as one IADD3 on the ALU pipe). This needs the
+// multiplier `one` in a uniform register (IMAD R, R, UR, R): no FMA-pipe add
+// may take an immediate or uniform addend (sha256_rounds_head's CM masks),
+// or ptxas holds `one` in a vector register for the whole kernel and every
+// IMAD reads three vector registers (slower than 2, profiles/r02_ab_var.txt).
+#ifndef POSLO_S1_FMA
+#define POSLO_S1_FMA 5
+#endif
+#ifndef POSLO_S1_LOOP_FMA
+#define POSLO_S1_LOOP_FMA POSLO_S1_FMA  // ... of the rolled rounds 32-63
+#endif
+#ifndef POSLO_S1_OTSB_FMA
+#define POSLO_S1_OTSB_FMA POSLO_S1_FMA  // ... of onetime_seed rounds 16-31
+#endif
+#ifndef POSLO_S1_ENTB_FMA
+#define POSLO_S1_ENTB_FMA POSLO_S1_FMA  // ... of the entry hashes' rounds 16-31
+#endif
 #ifndef POSLO_ENTRY_SPEC
 #define POSLO_ENTRY_SPEC 1  // entry-hash head specialisation (W13 = W14 = 0): 12.13 vs 12.16 ms
 #endif
@@ -165,19 +185,19 @@ __global__ void __launch_bounds__(T, MINB) k_hash_s1_l32r(const uint4* __restric
                 // 16-round loop (rounds 32-63, or 16-63 for the entry hashes) shared
                 int blk0 = 16;
                 if (c == 0) {
-                    ots_head_rounds<FMA>(st, W, j, s_ots[le], pk);
+                    ots_head_rounds<FMA, POSLO_S1_OTSB_FMA>(st, W, j, s_ots[le], pk);
                     blk0 = 32;
                 } else {
 #if POSLO_ENTRY_SPEC
                     // W13 = W14 = 0, W15 = 384 / 392: sigma terms of W13..W15 fold
-                    entry_head_rounds<FMA>(st, W, c == 1 ? sha_s1(384u) : sha_s1(392u),
+                    entry_head_rounds<FMA, POSLO_S1_ENTB_FMA>(st, W, c == 1 ? sha_s1(384u) : sha_s1(392u),
                                            c == 1 ? sha_s0(384u) : sha_s0(392u), pk);
                     blk0 = 32;
 #else
                     sha256_rounds_head<FMA>(st, W, 0, pk);
 #endif
                 }
-                sha256_rounds_loop<FMA>(st, W, blk0, pk);
+                sha256_rounds_loop<POSLO_S1_LOOP_FMA>(st, W, blk0, pk);
                 (void)r0;
 #else
                 sha256_rounds_compact<FMA>(st, W, r0, pk);
@@ -264,9 +284,6 @@ static void launch_tiled(uint32_t n_tiles, const uint4* pay, const TileMap& tm, 
 #endif
 #ifndef POSLO_S1_MINB
 #define POSLO_S1_MINB 4  // __launch_bounds__ min CTAs/SM of the lean kernel (48 regs: 5 fit anyway)
-#endif
-#ifndef POSLO_S1_FMA
-#define POSLO_S1_FMA 2  // pipe assignment of the lean kernel's SHA rounds (sha256.cuh SHA_RND_SEL)
 #endif
 
 void launch_hash_s1_l32(const EntryLayout& lay, const TileMap& tm, const uint4* d_x0,

@@ -529,35 +529,43 @@ PHD uint32_t sha_sched_p(uint32_t w16, uint32_t w15, uint32_t w7, uint32_t w2, c
     } while (0)
 
 // Rounds r0..15 (r0 = 0, or 4 resuming after a hoisted round 3) over W[0..15].
-// st is a..h in the usual order on entry and exit.
-template <int FMA = 0>
+// st is a..h in the usual order on entry and exit. CM: rounds whose W is a
+// compile-time constant; with FMA == 5 they keep the SHA_RND_F form, where
+// h + (W + K) folds to one VIADD with an immediate (the FMA == 5 form would
+// be an IMAD with an immediate addend, whose multiplier `one` ptxas must
+// then hold in a vector register for the whole kernel: R-R-R IMADs).
+template <int FMA = 0, uint32_t CM = 0>
 PHD void sha256_rounds_head(uint32_t st[8], const uint32_t W[16], int r0, const PipeK& pk) {
     const uint32_t one = pk.one;
     (void)one;
-#define RND SHA_RND_SEL
+#define RNDC(i, ...)                                                    \
+    do {                                                                \
+        if (FMA == 5 && ((CM >> (i)) & 1u)) SHA_RND_F(__VA_ARGS__);     \
+        else SHA_RND_SEL(__VA_ARGS__);                                  \
+    } while (0)
     uint32_t a, b, c, d, e, f, g, h;
     if (r0 == 0) {
         a = st[0]; b = st[1]; c = st[2]; d = st[3]; e = st[4]; f = st[5]; g = st[6]; h = st[7];
-        RND(a, b, c, d, e, f, g, h, W[0], sha_k(0));
-        RND(h, a, b, c, d, e, f, g, W[1], sha_k(1));
-        RND(g, h, a, b, c, d, e, f, W[2], sha_k(2));
-        RND(f, g, h, a, b, c, d, e, W[3], sha_k(3));
+        RNDC(0, a, b, c, d, e, f, g, h, W[0], sha_k(0));
+        RNDC(1, h, a, b, c, d, e, f, g, W[1], sha_k(1));
+        RNDC(2, g, h, a, b, c, d, e, f, W[2], sha_k(2));
+        RNDC(3, f, g, h, a, b, c, d, e, W[3], sha_k(3));
     } else {  // resume after round 3: the names are rotated by four
         e = st[0]; f = st[1]; g = st[2]; h = st[3]; a = st[4]; b = st[5]; c = st[6]; d = st[7];
     }
-    RND(e, f, g, h, a, b, c, d, W[4], sha_k(4));
-    RND(d, e, f, g, h, a, b, c, W[5], sha_k(5));
-    RND(c, d, e, f, g, h, a, b, W[6], sha_k(6));
-    RND(b, c, d, e, f, g, h, a, W[7], sha_k(7));
-    RND(a, b, c, d, e, f, g, h, W[8], sha_k(8));
-    RND(h, a, b, c, d, e, f, g, W[9], sha_k(9));
-    RND(g, h, a, b, c, d, e, f, W[10], sha_k(10));
-    RND(f, g, h, a, b, c, d, e, W[11], sha_k(11));
-    RND(e, f, g, h, a, b, c, d, W[12], sha_k(12));
-    RND(d, e, f, g, h, a, b, c, W[13], sha_k(13));
-    RND(c, d, e, f, g, h, a, b, W[14], sha_k(14));
-    RND(b, c, d, e, f, g, h, a, W[15], sha_k(15));
-#undef RND
+    RNDC(4, e, f, g, h, a, b, c, d, W[4], sha_k(4));
+    RNDC(5, d, e, f, g, h, a, b, c, W[5], sha_k(5));
+    RNDC(6, c, d, e, f, g, h, a, b, W[6], sha_k(6));
+    RNDC(7, b, c, d, e, f, g, h, a, W[7], sha_k(7));
+    RNDC(8, a, b, c, d, e, f, g, h, W[8], sha_k(8));
+    RNDC(9, h, a, b, c, d, e, f, g, W[9], sha_k(9));
+    RNDC(10, g, h, a, b, c, d, e, f, W[10], sha_k(10));
+    RNDC(11, f, g, h, a, b, c, d, e, W[11], sha_k(11));
+    RNDC(12, e, f, g, h, a, b, c, d, W[12], sha_k(12));
+    RNDC(13, d, e, f, g, h, a, b, c, W[13], sha_k(13));
+    RNDC(14, c, d, e, f, g, h, a, b, W[14], sha_k(14));
+    RNDC(15, b, c, d, e, f, g, h, a, W[15], sha_k(15));
+#undef RNDC
     st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
 }
 
@@ -598,11 +606,12 @@ PHD void sha256_rounds_compact(uint32_t st[8], uint32_t W[16], int r0, const Pip
 // W15, so sigma1(W14), sigma0(W13), sigma0(W14) vanish and sigma1(W15),
 // sigma0(W15) are constants (s1w15, s0w15) in W16..W31. Runs rounds 0..31
 // and leaves W = W16..W31 for sha256_rounds_loop(.., 32, ..).
-template <int FMA = 2>
+template <int FMA_H = 2, int FMA_B = FMA_H>  // FMA_B: pipe assignment of rounds 16..31
 PHD void entry_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t s1w15, uint32_t s0w15, const PipeK& pk) {
+    constexpr int FMA = FMA_H;
     const uint32_t one = pk.one;
     (void)one;
-    sha256_rounds_head<FMA>(st, W, 0, pk);
+    sha256_rounds_head<FMA, (1u << 13) | (1u << 14) | (1u << 15)>(st, W, 0, pk);  // W13 = W14 = 0, W15 uniform
     const uint32_t w0 = W[0], w1 = W[1], w2 = W[2], w3 = W[3], w4 = W[4], w5 = W[5], w6 = W[6], w7 = W[7];
     const uint32_t w8 = W[8], w9 = W[9], w10 = W[10], w11 = W[11], w12 = W[12], w15 = W[15];
     W[0] = fadd(sha_s0(w1), fadd(w9, w0, one), one);                                   // W16
@@ -622,7 +631,10 @@ PHD void entry_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t s1w15, uint3
     W[14] = fadd(sha_s1(W[12]), fadd(W[7], s0w15, one), one);                        // W30 (W14 = 0)
     W[15] = fadd(sha_s1(W[13]), fadd(sha_s0(W[0]), fadd(W[8], w15, one), one), one); // W31
     uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
-    SHA_16_ROUNDS(sha_k, 16);
+    {
+        constexpr int FMA = FMA_B;  // rounds 16..31
+        SHA_16_ROUNDS(sha_k, 16);
+    }
     st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
 }
 
@@ -652,13 +664,14 @@ PHD OtsEpoch ots_epoch_consts(const uint32_t x0w[4]) {
     return E;
 }
 
-template <int FMA = 2>
+template <int FMA_H = 2, int FMA_B = FMA_H>  // FMA_B: pipe assignment of rounds 16..31
 PHD void ots_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t j, const OtsEpoch& E, const PipeK& pk) {
+    constexpr int FMA = FMA_H;
     const uint32_t one = pk.one;
     (void)one;
     // rounds 4..15: W4 = j, the rest compile-time constants
     const uint32_t Wm[16] = {0, 0, 0, 0, j, 0x80000000u, 0, 0, 0, 0, 0, 0, 0, 0, 0, 160u};
-    sha256_rounds_head<FMA>(st, Wm, 4, pk);
+    sha256_rounds_head<FMA, 0xffe0u>(st, Wm, 4, pk);  // W5..W15 constant
     // schedule words 16..31
     W[0] = E.w16;
     W[1] = E.w17;
@@ -677,7 +690,10 @@ PHD void ots_head_rounds(uint32_t st[8], uint32_t W[16], uint32_t j, const OtsEp
     W[14] = fadd(sha_s1(W[12]), W[7] + sha_s0(160u), one);
     W[15] = fadd(sha_s1(W[13]), fadd(W[8], E.c31, one), one);
     uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
-    SHA_16_ROUNDS(sha_k, 16);
+    {
+        constexpr int FMA = FMA_B;  // rounds 16..31
+        SHA_16_ROUNDS(sha_k, 16);
+    }
     st[0] = a; st[1] = b; st[2] = c; st[3] = d; st[4] = e; st[5] = f; st[6] = g; st[7] = h;
 }
 
