@@ -3,7 +3,9 @@
 // the R-hat fold of paver (batch_verify.cpp:75-81, group_combine
 // group.cpp:169-178) and point validation (GroupElement::from_bytes,
 // group.cpp:107-114). One thread per check; folds are block trees.
+#ifndef POSLO_FE_INLINE
 #define POSLO_FE_CALL 1  // out-of-line field multiplication in the group kernels (i-cache)
+#endif
 #include "poslo_internal.h"
 #include "ristretto.cuh"
 #include "scalar.cuh"
