@@ -92,11 +92,12 @@ __global__ void __launch_bounds__(128) k_fold_stage2(const gpt* __restrict__ par
     gpt acc = pt_identity();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) acc = pt_add(acc, partial[i]);
     block_reduce_pt(acc, sh);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the encode by the whole warp 0
         uint8_t b[32];
-        rist_encode(acc, b);
+        rist_encode_w(acc, b);
+        if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < 32; k++) out[k] = b[k];
+            for (int k = 0; k < 32; k++) out[k] = b[k];
     }
 }
 
@@ -238,9 +239,10 @@ __global__ void __launch_bounds__(128) k_check_cta(const gcached* __restrict__ t
         if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
         __syncthreads();
     }
-    if (t == 0) {
+    if (t < 32) {  // the encode by the whole warp 0, lane 0 writes
         uint8_t out[32];
-        rist_encode(sh[0], out);
+        rist_encode_w(sh[0], out);
+        if (t != 0) return;
         if (enc)
 #pragma unroll
             for (int k = 0; k < 32; k++) enc[(size_t)i * 32 + k] = out[k];
@@ -505,11 +507,12 @@ __global__ void __launch_bounds__(128) k_segfold_gpt(const gpt* __restrict__ pts
     for (uint32_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
         if (!mask || mask[k]) acc = pt_add(acc, pts[k]);
     block_reduce_pt(acc, sh);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the encode by the whole warp 0
         uint8_t o[32];
-        rist_encode(acc, o);
+        rist_encode_w(acc, o);
+        if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
+            for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
     }
 }
 
@@ -524,6 +527,7 @@ struct CheckPre {
 static_assert(sizeof(CheckPre) <= 256, "b_pre holds one CheckPre");
 
 __device__ __forceinline__ void named_sync64() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+__device__ __forceinline__ void named_sync128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // 64 threads each take one signed radix-16 window of the scalar from the
 // table, then a 6-level shared-memory tree (named barrier over warps 0-1).
@@ -560,12 +564,15 @@ __global__ void __launch_bounds__(96) k_check_pre(const gcached* __restrict__ ta
     if (threadIdx.x < 64) {
         gpt S = comb_tree64(tabB, s, dig, sh);
         (void)S;
-    } else if (threadIdx.x == 64) {  // warp 2 decodes R concurrently
+    } else {  // warp 2 decodes R concurrently (the whole warp: rist_decode_w)
         uint8_t b[32];
         load32(r_enc, b);
         gpt P;
-        rok = rist_decode(b, P) ? 1 : 0;
-        R = P;
+        const bool ok = rist_decode_w(b, P);
+        if (threadIdx.x == 64) {
+            rok = ok ? 1 : 0;
+            R = P;
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -604,25 +611,27 @@ __global__ void __launch_bounds__(128) k_segfold_points(const uint8_t* __restric
         acc = pt_add(acc, P);
     }
     block_reduce_pt(acc, sh);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the encode by the whole warp 0
         uint8_t o[32];
-        rist_encode(acc, o);
+        rist_encode_w(acc, o);
+        if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
+            for (int k = 0; k < 32; k++) out[(size_t)g * 32 + k] = o[k];
     }
 }
 
-// One distill_epoch step (poslo_gpu_distill_step) in one CTA of 160 threads:
+// One distill_epoch step (poslo_gpu_distill_step) in one CTA of 224 threads:
 // warps 0-3 evaluate e Y + s B on the radix-16 combs (thread t < 64 window t
-// of e on Y's table, 64 + t window t of s on alpha's) while warp 4 decodes R-hat
-// and the two running aggregates' points in parallel; the verdict is the
+// of e on Y's table, 64 + t window t of s on alpha's) while warps 4-6 decode
+// R-hat and the two running aggregates' points (a warp-cooperative inverse
+// square root each); the verdict is the
 // projective ristretto equality of e Y + s B and R-hat (no encode on the
 // check's path), and on a valid verdict R-hat is added to both aggregates and
-// the two sums encoded by two threads at once (Scalar::add / group_combine,
+// the two sums encoded by two warps at once (Scalar::add / group_combine,
 // distiller.cpp:45-53). in: s_items = [acc_s0, s_hat, acc_s1] (8 limbs each),
 // pts = [acc_r0, r_hat, acc_r1] encodings. out: verdict, out_s (2 x 8 limbs),
 // out_r (2 x 32 B); *bad on an undecodable point.
-__global__ void __launch_bounds__(160) k_distill_step(const gcached* __restrict__ tabY,
+__global__ void __launch_bounds__(224) k_distill_step(const gcached* __restrict__ tabY,
                                                       const gcached* __restrict__ tabB,
                                                       const uint32_t* __restrict__ e, const uint32_t* __restrict__ s_items,
                                                       const uint8_t* __restrict__ pts, uint8_t* __restrict__ verdict,
@@ -634,34 +643,38 @@ __global__ void __launch_bounds__(160) k_distill_step(const gcached* __restrict_
     __shared__ int dec_ok[3];
     __shared__ int s_verdict;
     const int t = threadIdx.x;
-    if (t < 2) {
-        uint32_t v[8];
-        const uint32_t* src = t == 0 ? e : s_items + 8;
-#pragma unroll
-        for (int k = 0; k < 8; k++) v[k] = src[k];
-        int8_t d[64];
-        sc_signed_radix16(v, d);
-        for (int k = 0; k < 64; k++) dig[64 * t + k] = d[k];
-    } else if (t >= 128 && t < 131) {  // warp 4: the three decodes, concurrently with the comb
+    if (t >= 128) {  // warps 4-6: the three decodes (a warp each), concurrently with the comb
+        const int q = (t - 128) >> 5;
         uint8_t b[32];
-        load32(pts + 32 * (t - 128), b);
+        load32(pts + 32 * q, b);
         gpt P;
-        const bool ok = rist_decode(b, P);
-        dec[t - 128] = ok ? P : pt_identity();
-        dec_ok[t - 128] = ok;
-    }
-    __syncthreads();
-    if (t < 128) {
+        const bool ok = rist_decode_w(b, P);
+        if ((t & 31) == 0) {
+            dec[q] = ok ? P : pt_identity();
+            dec_ok[q] = ok;
+        }
+    } else {  // warps 0-3: comb and tree, synchronised among themselves only (barrier 1)
+        if (t < 2) {
+            uint32_t v[8];
+            const uint32_t* src = t == 0 ? e : s_items + 8;
+#pragma unroll
+            for (int k = 0; k < 8; k++) v[k] = src[k];
+            int8_t d[64];
+            sc_signed_radix16(v, d);
+            for (int k = 0; k < 64; k++) dig[64 * t + k] = d[k];
+        }
+        named_sync128();
         const int dgt = dig[t];
         gpt acc = pt_identity();
         if (dgt) acc = pt_add_cached(acc, table_pick(t < 64 ? tabY : tabB, t & 63, dgt));
         sh[t] = acc;
+        named_sync128();
+        for (int w = 64; w >= 1; w >>= 1) {
+            if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
+            named_sync128();
+        }
     }
-    __syncthreads();
-    for (int w = 64; w >= 1; w >>= 1) {
-        if (t < w) sh[t] = pt_add(sh[t], sh[t + w]);
-        __syncthreads();
-    }
+    __syncthreads();  // the decodes
     if (t == 0) {
         // an R-hat that does not decode never equals a canonical encoding (false,
         // as the encoding comparison); undecodable aggregates are a format error
@@ -671,18 +684,20 @@ __global__ void __launch_bounds__(160) k_distill_step(const gcached* __restrict_
     }
     __syncthreads();
     const bool v = s_verdict != 0;
-    if (t < 2) {  // the two aggregates: point add + encode, one thread each
-        const int a = 2 * t;  // item 0 = valid aggregate, item 2 = umbrella aggregate
+    if (t < 64) {  // the two aggregates: point add + encode, a warp each
+        const int w = t >> 5;
+        const int a = 2 * w;  // item 0 = valid aggregate, item 2 = umbrella aggregate
         uint8_t o[32];
         if (v) {
-            rist_encode(pt_add(dec[a], dec[1]), o);
+            rist_encode_w(pt_add(dec[a], dec[1]), o);
         } else {
             load32(pts + 32 * a, o);
         }
+        if ((t & 31) == 0)
 #pragma unroll
-        for (int k = 0; k < 32; k++) out_r[32 * t + k] = o[k];
-    } else if (t == 32 || t == 33) {  // scalars
-        const int i = t - 32;
+            for (int k = 0; k < 32; k++) out_r[32 * w + k] = o[k];
+    } else if (t == 64 || t == 65) {  // scalars
+        const int i = t - 64;
         uint32_t a[8], b[8], r[8];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
@@ -700,7 +715,7 @@ __global__ void __launch_bounds__(160) k_distill_step(const gcached* __restrict_
 void launch_distill_step(const void* d_tabY, const void* d_tabB, const uint32_t* d_e, const uint32_t* d_s_items,
                          const uint8_t* d_pts, uint8_t* d_verdict, uint32_t* d_out_s, uint8_t* d_out_r, int* d_bad,
                          cudaStream_t s) {
-    k_distill_step<<<1, 160, 0, s>>>(static_cast<const gcached*>(d_tabY), static_cast<const gcached*>(d_tabB), d_e,
+    k_distill_step<<<1, 224, 0, s>>>(static_cast<const gcached*>(d_tabY), static_cast<const gcached*>(d_tabB), d_e,
                                      d_s_items, d_pts, d_verdict, d_out_s, d_out_r, d_bad);
 }
 

@@ -229,12 +229,102 @@ PHD fe fe_pow22523(const fe& z) {
     return fe_mul(fe_sqn(z250, 2), z);           // 2^252 - 3
 }
 
+#ifdef __CUDACC__
+// ---- warp-cooperative exponentiation (latency paths) ----------------------
+// One product on one thread is a serial 10-limb carry chain (~700 cycles);
+// the inverse square root behind every encode / decode is 252 squarings and
+// 11 products of them. Where ONE encode or decode sits on a critical path
+// (a single check, a distill step, a fold's result) the whole warp runs it:
+// the element is spread over lanes 0..9 (lane k holds limb k), lane k forms
+// column k of a product from 10 broadcast limbs of a and 10 rotated limbs of
+// b (20 shuffles, 10 IMAD.WIDE), and the carries run as parallel passes
+// (shuffle up; lane 0 takes 19 x lane 9's carry). Lanes 10..31 mirror lane 0.
+// The result is carried (limb < 2^w + 38), as fe_carry64's.
+// One parallel carry pass over 32-bit limbs (limb k keeps its low w bits and
+// takes lane k-1's carry; lane 0 takes 19 x lane 9's).
+__device__ __forceinline__ uint32_t fw_carry32(uint32_t h, int k) {
+    const int w = (k & 1) ? 25 : 26;
+    const uint32_t c = h >> w;
+    const uint32_t cin = __shfl_sync(0xffffffffu, c, k == 0 ? 9 : k - 1);
+    return (h & ((1u << w) - 1)) + (k == 0 ? 19u * cin : cin);
+}
+
+// Column sums (< 2^61) -> limbs < 2^w + 2^20 in two parallel passes: enough
+// for the next product's bounds (and for fe_sub's bias); fw_out adds a third.
+__device__ __forceinline__ uint32_t fw_carry(uint64_t h, int k) {
+    const int w = (k & 1) ? 25 : 26;
+    const uint64_t c = h >> w;  // < 2^36
+    const uint64_t cin = __shfl_sync(0xffffffffu, c, k == 0 ? 9 : k - 1);
+    h = (h & ((1ull << w) - 1)) + (k == 0 ? 19 * cin : cin);  // < 2^41
+    const uint32_t c2 = (uint32_t)(h >> w);                      // < 2^16
+    const uint32_t cin2 = __shfl_sync(0xffffffffu, c2, k == 0 ? 9 : k - 1);
+    return (uint32_t)(h & ((1ull << w) - 1)) + (k == 0 ? 19u * cin2 : cin2);
+}
+
+__device__ __forceinline__ uint32_t fw_mul(uint32_t a, uint32_t b, int k) {
+    uint64_t h = 0;
+#pragma unroll
+    for (int i = 0; i < 10; i++) {
+        const uint32_t ai = __shfl_sync(0xffffffffu, a, i);
+        const int j = k >= i ? k - i : k - i + 10;  // column k = i + j (mod 10)
+        const uint32_t bj = __shfl_sync(0xffffffffu, b, j);
+        // x19 for the wrapped terms (2^255 == 19), x2 when both limb offsets round down
+        const uint32_t f = (k >= i ? 1u : 19u) << (i & j & 1);
+        h += (uint64_t)ai * (bj * f);
+    }
+    return fw_carry(h, k);
+}
+
+__device__ __noinline__ uint32_t fw_sqn(uint32_t a, int n, int k) {
+#pragma unroll 1
+    for (int i = 0; i < n; i++) a = fw_mul(a, a, k);
+    return a;
+}
+
+// fe_pow22523 by the whole (converged) warp; z and the result are the same
+// value in every lane.
+__device__ __noinline__ fe fe_pow22523_w(const fe& zf) {
+    const int lane = threadIdx.x & 31, k = lane < 10 ? lane : 0;
+    uint32_t z = zf.v[0];
+#pragma unroll
+    for (int i = 1; i < 10; i++)
+        if (k == i) z = zf.v[i];
+    const uint32_t z2 = fw_mul(z, z, k);
+    const uint32_t z3 = fw_mul(z2, z, k);                         // 2^2 - 1
+    const uint32_t z15 = fw_mul(fw_sqn(z3, 2, k), z3, k);         // 2^4 - 1
+    const uint32_t z31 = fw_mul(fw_sqn(z15, 1, k), z, k);         // 2^5 - 1
+    const uint32_t z10 = fw_mul(fw_sqn(z31, 5, k), z31, k);       // 2^10 - 1
+    const uint32_t z20 = fw_mul(fw_sqn(z10, 10, k), z10, k);      // 2^20 - 1
+    const uint32_t z40 = fw_mul(fw_sqn(z20, 20, k), z20, k);      // 2^40 - 1
+    const uint32_t z50 = fw_mul(fw_sqn(z40, 10, k), z10, k);      // 2^50 - 1
+    const uint32_t z100 = fw_mul(fw_sqn(z50, 50, k), z50, k);     // 2^100 - 1
+    const uint32_t z200 = fw_mul(fw_sqn(z100, 100, k), z100, k);  // 2^200 - 1
+    const uint32_t z250 = fw_mul(fw_sqn(z200, 50, k), z50, k);    // 2^250 - 1
+    const uint32_t r = fw_carry32(fw_mul(fw_sqn(z250, 2, k), z, k), k);  // 2^252 - 3, limbs < 2^w + 38
+    fe out;
+#pragma unroll
+    for (int i = 0; i < 10; i++) out.v[i] = __shfl_sync(0xffffffffu, r, i);
+    return out;
+}
+#endif
+
+// W = true: the exponentiation by the whole warp (every lane of a converged
+// warp calls with the same operands; device code only).
+template <bool W>
+PHD fe fe_pow22523_sel(const fe& z) {
+#ifdef __CUDA_ARCH__
+    if constexpr (W) return fe_pow22523_w(z);
+#endif
+    return fe_pow22523(z);
+}
+
 // SQRT_RATIO_M1(u, v): returns was_square, r = non-negative root.
+template <bool W = false>
 PHD bool fe_sqrt_ratio_m1(const fe& u, const fe& v, fe& r) {
     const fe sqrtm1 = FE_CONST(FE_SQRTM1_LIMBS);
     fe v3 = fe_mul(fe_sq(v), v);
     fe v7 = fe_mul(fe_sq(v3), v);
-    r = fe_mul(fe_mul(u, v3), fe_pow22523(fe_mul(u, v7)));
+    r = fe_mul(fe_mul(u, v3), fe_pow22523_sel<W>(fe_mul(u, v7)));
     fe check = fe_mul(v, fe_sq(r));
     fe nu = fe_neg(u);
     bool correct = fe_eq(check, u);
@@ -340,7 +430,10 @@ PHD gpt pt_neg(const gpt& p) {
 
 // Ristretto decode with full validation (RFC 9496 §4.3.1); false = invalid
 // encoding, exactly the set crypto_core_ristretto255_is_valid_point rejects.
-PHD bool rist_decode(const uint8_t b[32], gpt& out) {
+// W = true: the inverse square root by the whole warp (every lane calls with
+// the same bytes; rist_decode_w).
+template <bool W>
+PHD bool rist_decode_t(const uint8_t b[32], gpt& out) {
     fe s = fe_from_bytes_le(b);
     // canonical: s < p and bit 255 clear (re-encoding reproduces b), non-negative
     uint8_t rb[32];
@@ -356,7 +449,7 @@ PHD bool rist_decode(const uint8_t b[32], gpt& out) {
     fe u2sq = fe_sq(u2);
     fe v = fe_sub(fe_neg(fe_mul(d, fe_sq(u1))), u2sq);
     fe inv;
-    bool was_square = fe_sqrt_ratio_m1(fe_one(), fe_mul(v, u2sq), inv);
+    bool was_square = fe_sqrt_ratio_m1<W>(fe_one(), fe_mul(v, u2sq), inv);
     fe den_x = fe_mul(inv, u2);
     fe den_y = fe_mul(fe_mul(inv, den_x), v);
     fe x = fe_abs(fe_mul(fe_add(s, s), den_x));
@@ -370,14 +463,17 @@ PHD bool rist_decode(const uint8_t b[32], gpt& out) {
     return true;
 }
 
+PHD bool rist_decode(const uint8_t b[32], gpt& out) { return rist_decode_t<false>(b, out); }
+
 // Ristretto encode (RFC 9496 §4.3.2) -> 32 canonical bytes.
-PHD void rist_encode(const gpt& p, uint8_t out[32]) {
+template <bool W>
+PHD void rist_encode_t(const gpt& p, uint8_t out[32]) {
     const fe sqrtm1 = FE_CONST(FE_SQRTM1_LIMBS);
     const fe isqrt_amd = FE_CONST(FE_INVSQRT_A_MINUS_D_LIMBS);
     fe u1 = fe_mul(fe_add(p.Z, p.Y), fe_sub(p.Z, p.Y));
     fe u2 = fe_mul(p.X, p.Y);
     fe inv;
-    fe_sqrt_ratio_m1(fe_one(), fe_mul(u1, fe_sq(u2)), inv);
+    fe_sqrt_ratio_m1<W>(fe_one(), fe_mul(u1, fe_sq(u2)), inv);
     fe den1 = fe_mul(inv, u1);
     fe den2 = fe_mul(inv, u2);
     fe z_inv = fe_mul(fe_mul(den1, den2), p.T);
@@ -392,6 +488,13 @@ PHD void rist_encode(const gpt& p, uint8_t out[32]) {
     fe s = fe_abs(fe_mul(den_inv, fe_sub(p.Z, y)));
     fe_to_bytes_le(s, out);
 }
+
+PHD void rist_encode(const gpt& p, uint8_t out[32]) { rist_encode_t<false>(p, out); }
+#ifdef __CUDACC__
+// by the whole converged warp, same operands in every lane
+__device__ __forceinline__ bool rist_decode_w(const uint8_t b[32], gpt& out) { return rist_decode_t<true>(b, out); }
+__device__ __forceinline__ void rist_encode_w(const gpt& p, uint8_t out[32]) { rist_encode_t<true>(p, out); }
+#endif
 
 // Scalar bit i of a canonical 32-byte little-endian scalar held as 8 limbs.
 PHD int sc_bit(const uint32_t s[8], int i) { return (s[i >> 5] >> (i & 31)) & 1; }
