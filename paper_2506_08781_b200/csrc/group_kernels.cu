@@ -117,22 +117,22 @@ __global__ void k_validate(const uint8_t* __restrict__ pts, uint32_t n, uint8_t*
 // W = 4: 64 powers 16^k P; W = 8: 32 powers 256^k P.
 template <int W>
 __global__ void k_table_pow(const uint8_t* __restrict__ enc, gpt* __restrict__ pk, int* bad) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // one warp: the decode and the 252-doubling chain warp-cooperatively
+    // (rist_decode_w, fw3_pow16_chain: three field products per round)
+    static_assert(W == 4, "the warp chain stores 16^k P");
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
     gpt P;
     if (enc) {
         uint8_t b[32];
         load32(enc, b);
-        if (!rist_decode(b, P)) {
-            atomicOr(bad, 1);
+        if (!rist_decode_w(b, P)) {
+            if (threadIdx.x == 0) atomicOr(bad, 1);
             P = pt_identity();
         }
     } else {
         P = pt_base();
     }
-    for (int k = 0; k < 256 / W; k++) {
-        pk[k] = P;
-        for (int i = 0; i < W; i++) P = pt_dbl(P);
-    }
+    fw3_pow16_chain(P, pk, 256 / W);
 }
 
 // Radix-256 fill: thread t = 128 k + i writes (i + 1) 256^k P, by

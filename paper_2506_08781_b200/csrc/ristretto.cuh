@@ -242,37 +242,40 @@ PHD fe fe_pow22523(const fe& z) {
 // The result is carried (limb < 2^w + 38), as fe_carry64's.
 // One parallel carry pass over 32-bit limbs (limb k keeps its low w bits and
 // takes lane k-1's carry; lane 0 takes 19 x lane 9's).
-__device__ __forceinline__ uint32_t fw_carry32(uint32_t h, int k) {
+__device__ __forceinline__ uint32_t fw_carry32(uint32_t h, int k, int base = 0) {
     const int w = (k & 1) ? 25 : 26;
     const uint32_t c = h >> w;
-    const uint32_t cin = __shfl_sync(0xffffffffu, c, k == 0 ? 9 : k - 1);
+    const uint32_t cin = __shfl_sync(0xffffffffu, c, base + (k == 0 ? 9 : k - 1));
     return (h & ((1u << w) - 1)) + (k == 0 ? 19u * cin : cin);
 }
 
 // Column sums (< 2^61) -> limbs < 2^w + 2^20 in two parallel passes: enough
 // for the next product's bounds (and for fe_sub's bias); fw_out adds a third.
-__device__ __forceinline__ uint32_t fw_carry(uint64_t h, int k) {
+__device__ __forceinline__ uint32_t fw_carry(uint64_t h, int k, int base = 0) {
     const int w = (k & 1) ? 25 : 26;
+    const int src = base + (k == 0 ? 9 : k - 1);
     const uint64_t c = h >> w;  // < 2^36
-    const uint64_t cin = __shfl_sync(0xffffffffu, c, k == 0 ? 9 : k - 1);
+    const uint64_t cin = __shfl_sync(0xffffffffu, c, src);
     h = (h & ((1ull << w) - 1)) + (k == 0 ? 19 * cin : cin);  // < 2^41
     const uint32_t c2 = (uint32_t)(h >> w);                      // < 2^16
-    const uint32_t cin2 = __shfl_sync(0xffffffffu, c2, k == 0 ? 9 : k - 1);
+    const uint32_t cin2 = __shfl_sync(0xffffffffu, c2, src);
     return (uint32_t)(h & ((1ull << w) - 1)) + (k == 0 ? 19u * cin2 : cin2);
 }
 
-__device__ __forceinline__ uint32_t fw_mul(uint32_t a, uint32_t b, int k) {
+// base: the group's first lane (0, or 10 / 20 when a warp holds three
+// elements, fw3_*), k: this lane's limb index within its group.
+__device__ __forceinline__ uint32_t fw_mul(uint32_t a, uint32_t b, int k, int base = 0) {
     uint64_t h = 0;
 #pragma unroll
     for (int i = 0; i < 10; i++) {
-        const uint32_t ai = __shfl_sync(0xffffffffu, a, i);
+        const uint32_t ai = __shfl_sync(0xffffffffu, a, base + i);
         const int j = k >= i ? k - i : k - i + 10;  // column k = i + j (mod 10)
-        const uint32_t bj = __shfl_sync(0xffffffffu, b, j);
+        const uint32_t bj = __shfl_sync(0xffffffffu, b, base + j);
         // x19 for the wrapped terms (2^255 == 19), x2 when both limb offsets round down
         const uint32_t f = (k >= i ? 1u : 19u) << (i & j & 1);
         h += (uint64_t)ai * (bj * f);
     }
-    return fw_carry(h, k);
+    return fw_carry(h, k, base);
 }
 
 __device__ __noinline__ uint32_t fw_sqn(uint32_t a, int n, int k) {
@@ -305,6 +308,87 @@ __device__ __noinline__ fe fe_pow22523_w(const fe& zf) {
 #pragma unroll
     for (int i = 0; i < 10; i++) out.v[i] = __shfl_sync(0xffffffffu, r, i);
     return out;
+}
+
+// ---- warp-cooperative doubling chain (comb-table builds) -------------------
+// Three elements per warp: group g = lane / 10 (lanes 30, 31 mirror group
+// 2's limb 0) holds limb k = lane % 10 of its element, so one round of
+// fw_mul multiplies three independent pairs. A doubling (dbl-2008-hwcd with
+// 2XY for (X + Y)^2 - X^2 - Y^2) is three rounds: {X^2, Y^2, XY}, {Z^2},
+// {EF, GH, FG} (+ {EH} for T when the point is stored), the coordinates
+// replicated in every group between rounds by one shuffle each.
+struct Fw3Lane {
+    int g, k, base;
+};
+__device__ __forceinline__ Fw3Lane fw3_lane() {
+    const int lane = threadIdx.x & 31;
+    Fw3Lane L;
+    L.g = lane < 30 ? lane / 10 : 2;
+    L.k = lane < 30 ? lane % 10 : 0;
+    L.base = 10 * L.g;
+    return L;
+}
+// limb k of a replicated fe
+__device__ __forceinline__ uint32_t fw_pick(const fe& a, int k) {
+    uint32_t x = a.v[0];
+#pragma unroll
+    for (int i = 1; i < 10; i++)
+        if (k == i) x = a.v[i];
+    return x;
+}
+// 2p - b + a per limb (b carried: limb < 2^w + 2^20), then one carry pass
+__device__ __forceinline__ uint32_t fw_sub(uint32_t a, uint32_t b, const Fw3Lane& L) {
+    const uint32_t bias = L.k == 0 ? 0x7ffffdau : ((L.k & 1) ? 0x3fffffeu : 0x7fffffeu);
+    return fw_carry32(a + bias - b, L.k, L.base);
+}
+__device__ __forceinline__ uint32_t fw_add(uint32_t a, uint32_t b, const Fw3Lane& L) {
+    return fw_carry32(a + b, L.k, L.base);
+}
+// the value group `from` holds, in every group (limb for limb)
+__device__ __forceinline__ uint32_t fw_bcast(uint32_t x, int from, const Fw3Lane& L) {
+    return __shfl_sync(0xffffffffu, x, 10 * from + L.k);
+}
+
+// Store pk[k] = 16^k P for k < n (n = 256 / 4 = 64 here): the power chain of
+// the comb tables, P given replicated in every lane; T is formed only for
+// the stored points. Every lane of the warp calls.
+__device__ __noinline__ void fw3_pow16_chain(const gpt& P, gpt* out, int n) {
+    const Fw3Lane L = fw3_lane();
+    uint32_t X = fw_pick(P.X, L.k), Y = fw_pick(P.Y, L.k), Z = fw_pick(P.Z, L.k), T = fw_pick(P.T, L.k);
+#pragma unroll 1
+    for (int q = 0; q < n; q++) {
+        {  // group 0 stores the point, a limb per lane (T: from the last doubling)
+            const uint32_t xs = fw_carry32(X, L.k, L.base), ys = fw_carry32(Y, L.k, L.base);
+            const uint32_t zs = fw_carry32(Z, L.k, L.base), ts = fw_carry32(T, L.k, L.base);
+            if ((threadIdx.x & 31) < 10) {
+                out[q].X.v[L.k] = xs;
+                out[q].Y.v[L.k] = ys;
+                out[q].Z.v[L.k] = zs;
+                out[q].T.v[L.k] = ts;
+            }
+        }
+        if (q + 1 == n) break;
+#pragma unroll 1
+        for (int d = 0; d < 4; d++) {
+            // round 1: A = X^2 (group 0), B = Y^2 (1), XY (2)
+            const uint32_t u = L.g == 1 ? Y : X, v = L.g == 0 ? X : Y;
+            const uint32_t r1 = fw_mul(u, v, L.k, L.base);
+            const uint32_t A = fw_bcast(r1, 0, L), B = fw_bcast(r1, 1, L), XY = fw_bcast(r1, 2, L);
+            // round 2: Z^2 (every group)
+            const uint32_t Z2 = fw_mul(Z, Z, L.k, L.base);
+            const uint32_t E = fw_add(XY, XY, L);
+            const uint32_t G = fw_sub(B, A, L);
+            const uint32_t F = fw_sub(G, fw_add(Z2, Z2, L), L);
+            const uint32_t H = fw_sub(0u, fw_add(A, B, L), L);
+            // round 3: X3 = EF (0), Y3 = GH (1), Z3 = FG (2); T3 = EH on the last doubling
+            const uint32_t p = L.g == 1 ? G : (L.g == 0 ? E : F), r = L.g == 1 ? H : (L.g == 0 ? F : G);
+            const uint32_t r3 = fw_mul(p, r, L.k, L.base);
+            X = fw_bcast(r3, 0, L);
+            Y = fw_bcast(r3, 1, L);
+            Z = fw_bcast(r3, 2, L);
+            if (d == 3) T = fw_mul(E, H, L.k, L.base);
+        }
+    }
 }
 #endif
 
