@@ -29,6 +29,35 @@ def test_agg_ekeys_matches_reference(verifier, name):
     assert e_hat == st.e_hat
 
 
+def test_warp_decode_and_table_chain_on_kat_points(verifier, kat):
+    """The warp-cooperative paths (ristretto.cuh fw_*) on every KAT encoding,
+    14 valid and 34 invalid (RFC 9496 negative vectors among them):
+    commit_check with the point as Y builds Y's comb tables (decode by a whole
+    warp, then the 252-doubling chain three products per round) and must
+    equal the oracle, or raise FormatError for an invalid Y; as the paver's
+    R-hat aggregate (decoded by a warp in k_check_pre) only the correct
+    aggregate verifies, and an invalid encoding is a plain reject."""
+    import random
+    api = A()
+    from oracle import ristretto as R
+    rng = random.Random(255)
+    e = rng.randrange(R.L).to_bytes(32, "little")
+    s = rng.randrange(R.L).to_bytes(32, "little")
+    pts = [(bytes.fromhex(h), bool(v)) for h, v in kat["point_valid"]]
+    assert sum(v for _, v in pts) == 14 and len(pts) == 48
+    for y, valid in pts:
+        if valid:
+            assert verifier.commit_check(y, e, s) == R.commit_check(y, e, s)
+        else:
+            with pytest.raises(api.FormatError):
+                verifier.commit_check(y, e, s)
+    st = Stream(load_golden("stream_s1_clean_big.json"))
+    suite, pk, ds = st.api_objects()
+    assert verifier.paver(pk, st.batches, st.s_hat, st.r_hat_agg, ds, 1) is True
+    for r, _ in pts:
+        assert verifier.paver(pk, st.batches, st.s_hat, r, ds, 1) == (r == st.r_hat_agg)
+
+
 @pytest.mark.parametrize("name", STREAMS)
 def test_paver_matches_reference(verifier, name):
     st = Stream(load_golden(name + ".json"))
