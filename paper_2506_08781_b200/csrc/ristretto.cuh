@@ -265,7 +265,7 @@ __device__ __forceinline__ uint32_t fw_carry(uint64_t h, int k, int base = 0) {
 // base: the group's first lane (0, or 10 / 20 when a warp holds three
 // elements, fw3_*), k: this lane's limb index within its group.
 __device__ __forceinline__ uint32_t fw_mul(uint32_t a, uint32_t b, int k, int base = 0) {
-    uint64_t h = 0;
+    uint64_t h0 = 0, h1 = 0;  // two accumulation chains (even / odd i): half the dependent IMAD.WIDEs
 #pragma unroll
     for (int i = 0; i < 10; i++) {
         const uint32_t ai = __shfl_sync(0xffffffffu, a, base + i);
@@ -273,9 +273,10 @@ __device__ __forceinline__ uint32_t fw_mul(uint32_t a, uint32_t b, int k, int ba
         const uint32_t bj = __shfl_sync(0xffffffffu, b, base + j);
         // x19 for the wrapped terms (2^255 == 19), x2 when both limb offsets round down
         const uint32_t f = (k >= i ? 1u : 19u) << (i & j & 1);
-        h += (uint64_t)ai * (bj * f);
+        if (i & 1) h1 += (uint64_t)ai * (bj * f);
+        else h0 += (uint64_t)ai * (bj * f);
     }
-    return fw_carry(h, k, base);
+    return fw_carry(h0 + h1, k, base);
 }
 
 __device__ __noinline__ uint32_t fw_sqn(uint32_t a, int n, int k) {
