@@ -19,6 +19,7 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/poslo_gpu.h"
@@ -82,8 +83,14 @@ int ok(poslo_error* err) {
     } while (0)
 
 template <class T>
+constexpr size_t elem_bytes() {  // void buffers are counted in bytes
+    if constexpr (std::is_void<T>::value) return 1;
+    else return sizeof(T);
+}
+
+template <class T>
 int ensure(DevBuf& b, size_t count, T** out, poslo_error* err) {
-    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    size_t bytes = std::max<size_t>(count * elem_bytes<T>(), 16);
     if (b.cap < bytes) {
         size_t want = std::max(bytes, b.cap * 3 / 2);
         if (b.p) cudaFree(b.p);
@@ -1372,7 +1379,7 @@ int poslo_gpu_combine_check_prepare(poslo_gpu_ctx* ctx, const uint8_t y[32], con
     // own buffers: the side-stream kernel may run after later calls reuse the shared ones
     uint32_t* d_s;
     uint8_t* d_rhat;
-    void* d_pre;
+    uint8_t* d_pre;  // a CheckPre record (group_kernels.cu), 256 bytes reserved
     UPLOAD(b_ppre_s, s_hat, 32, d_s);
     UPLOAD(b_ppre_r, r_hat, 32, d_rhat);
     ENSURE(b_ppre, 256, d_pre);
@@ -1420,7 +1427,7 @@ int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t*
     }
     uint32_t *d_sum, *d_scr;
     uint8_t* d_verdict;
-    void* d_pre;
+    uint8_t* d_pre;
     ENSURE(b_sum, 8, d_sum);
     ENSURE(b_scratch, 17 * 1024, d_scr);
     ENSURE(b_pre, 256, d_pre);
@@ -1433,7 +1440,7 @@ int poslo_gpu_combine_check(poslo_gpu_ctx* ctx, uint32_t n_parts, const uint8_t*
     ctx->pre_valid = false;
     if (prepared) {  // queued by combine_check_prepare on the side stream
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_pre, 0));
-        d_pre = ctx->b_ppre.p;
+        d_pre = static_cast<uint8_t*>(ctx->b_ppre.p);
     } else {
         uint32_t* d_s;
         uint8_t* d_rhat;
@@ -1489,7 +1496,7 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
     int rc = ensure_tables(ctx, y, d_flags, err);  // syncs only when Y changed
     if (rc) return rc;
     uint32_t *d_sum, *d_scr, *d_s;
-    void* d_pre;
+    uint8_t* d_pre;
     uint8_t* d_verdict;
     UPLOAD(b_s, s_hat, 32, d_s);
     ENSURE(b_pre, 256, d_pre);

@@ -35,7 +35,6 @@ constexpr int kVarBuckets = 32;   // block-count buckets (clamped)
 // same-index LDS of a warp over 8 banks (a stride of 32 would put all 32
 // lanes on one bank)
 constexpr int kSlotWords = 36;
-constexpr uint32_t kNoEntry = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t nblocks(uint64_t msg_len) { return (uint32_t)((msg_len + 9 + 63) / 64); }
 
@@ -128,15 +127,6 @@ __device__ __forceinline__ void load_block(uint32_t word_addr, uint32_t sel, uin
 #undef POSLO_LDS_W
 #pragma unroll
     for (int k = 0; k < 16; k++) W[k] = __byte_perm(w[k], w[k + 1], sel);
-}
-
-__device__ __forceinline__ void compress_into(uint32_t H[8], uint32_t W[16], const PipeK& pk) {
-    uint32_t st[8];
-#pragma unroll
-    for (int i = 0; i < 8; i++) st[i] = H[i];
-    sha256_rounds_compact<POSLO_VAR_FMA>(st, W, 0, pk);
-#pragma unroll
-    for (int i = 0; i < 8; i++) H[i] += st[i];
 }
 
 PD void smem_acc9_add8v(uint32_t* s, int stride, const uint32_t v[8]) {
