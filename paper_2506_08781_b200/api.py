@@ -546,6 +546,9 @@ class Verifier:
         seeds and hashes only those. want: the modes to evaluate. Returns dict with
         keys V (list, only when valid given), U, I."""
         eps = range(epochs_distilled) if hashed is None else hashed
+        for i in eps:  # a missing epoch is the reference's FormatError, not a KeyError
+            if i not in all_msgs:
+                raise FormatError(f"messages for epoch {i} missing")
         batches = {i: all_msgs[i] for i in eps}
         pb = PackedBatch(suite.suite, suite.n2, batches, ds)
         cb = pb.cstruct()
