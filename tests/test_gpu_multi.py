@@ -145,6 +145,44 @@ def test_multi_context_byte_identical_at_scale(signed, multi):
         assert vd.value == 0
 
 
+def test_determinism_gate_1_2_4_8_members(signed):
+    """SURVEY §8e's gate at G = 1, 2, 4 and 8 (members sharing the one GPU):
+    every e~, e-hat, the per-epoch verdict bitmap and the distillation pieces
+    (umbrellas of 96 epochs, not aligned with any shard cut) are byte-identical
+    to one device, and the coarse paver decision agrees."""
+    v, sl = signed
+    lib = v._lib
+    pay, n1 = sl.host, sl.n1
+    cuts = np.array(list(range(0, n1, 96)) + [n1], dtype=np.uint32)
+    ng = len(cuts) - 1
+    S = v.scalar_sum([sl.s_hats[32 * i:32 * i + 32] for i in range(n1)])
+    R = v.group_fold([sl.r_hats[32 * i:32 * i + 32] for i in range(n1)])
+
+    def outputs(ctx):
+        et, eh = ctypes.create_string_buffer(32 * n1), ctypes.create_string_buffer(32)
+        ctx._call(lib.poslo_gpu_agg_ekeys, ctypes.byref(_host_batch(sl, pay)), et, eh)
+        vb = ctypes.create_string_buffer(n1)
+        ctx._call(lib.poslo_gpu_epoch_verify, ctypes.byref(_host_batch(sl, pay)), sl.Y, sl.s_hats, sl.r_hats,
+                  vb, None)
+        db = ctypes.create_string_buffer(n1)
+        o = [ctypes.create_string_buffer(32 * ng) for _ in range(3)]
+        ctx._call(lib.poslo_gpu_distill_coarse_ex, ctypes.byref(_host_batch(sl, pay)), sl.Y, sl.s_hats,
+                  sl.r_hats, ctypes.c_void_p(cuts.ctypes.data), ng, db, *o)
+        vd = ctypes.c_uint8(7)
+        ctx._call(lib.poslo_gpu_paver, ctypes.byref(_host_batch(sl, pay)), sl.Y, S, R, None, ctypes.byref(vd))
+        return et.raw, eh.raw, vb.raw, db.raw, o[0].raw, o[1].raw, o[2].raw, vd.value
+
+    ref = outputs(v)
+    assert [i for i in range(n1) if not ref[2][i]] == sl.bad_epochs() and ref[7] == 0
+    for g in (2, 4, 8):
+        m = _api().Verifier(devices=[0] * g)
+        try:
+            assert m.members() == g
+            assert outputs(m) == ref, f"{g} members"
+        finally:
+            m.close()
+
+
 def test_multi_context_errors_are_the_lowest_epoch(multi, verifier):
     """SeedNotDisclosed in the second and third member's ranges: the lowest
     undisclosed epoch is reported, as by one device (workers = 1 order)."""

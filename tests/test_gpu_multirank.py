@@ -1,7 +1,7 @@
 """Multi-rank determinism gate on the DEVICE ("outputs must be
 byte-identical at G = 1, 2, 4, 8"): the same multi_gpu.py code runs at world
-size 1 and 2 (gloo, both ranks on cuda:0 — the box has one GPU; NCCL needs one
-GPU per rank), each rank verifying its epoch shard with the device Verifier,
+size 1, 2 and 4 (gloo, all ranks on cuda:0 — the box has one GPU; NCCL needs
+one GPU per rank), each rank verifying its epoch shard with the device Verifier,
 and every gathered output must equal the world-1 output byte for byte:
 
   config 2 shape (coarse PAVer, n2 = 256): every e~, the folded e-hat, the verdict;
@@ -113,15 +113,16 @@ def _run(world):
     return res
 
 
-def test_world1_vs_world2_byte_identical_on_device():
+@pytest.mark.parametrize("world", [2, 4])
+def test_world1_vs_world_n_byte_identical_on_device(world):
     g1 = _run(1)[0]
-    g2s = _run(2)
+    g2s = _run(world)
     g2 = g2s[0]
     # world 1 equals the direct single-context calls
     assert g1["c2_e_tilde"] == g1["direct_c2"][0] and g1["c2_e_hat"] == g1["direct_c2"][1]
     assert g1["c2_verdict"] is True and g1["direct_c2_verdict"] is True
     assert g1["c3_verdicts"] == g1["direct_c3"]
-    # the determinism gate: G = 2 gathered outputs == G = 1, on every rank
+    # the determinism gate: G = world gathered outputs == G = 1, on every rank
     for r, g in g2s.items():
         assert g["c2_verdict"] == g1["c2_verdict"]
         assert g["c2_e_tilde"] == g1["c2_e_tilde"]
