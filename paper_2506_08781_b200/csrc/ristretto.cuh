@@ -231,7 +231,7 @@ PHD fe fe_pow22523(const fe& z) {
 
 #ifdef __CUDACC__
 // ---- warp-cooperative exponentiation (latency paths) ----------------------
-// One product on one thread is a serial 10-limb carry chain (~700 cycles);
+// One product on one thread is a serial 10-limb carry chain (~900 cycles);
 // the inverse square root behind every encode / decode is 252 squarings and
 // 11 products of them. Where ONE encode or decode sits on a critical path
 // (a single check, a distill step, a fold's result) the whole warp runs it:
@@ -239,7 +239,8 @@ PHD fe fe_pow22523(const fe& z) {
 // column k of a product from 10 broadcast limbs of a and 10 rotated limbs of
 // b (20 shuffles, 10 IMAD.WIDE), and the carries run as parallel passes
 // (shuffle up; lane 0 takes 19 x lane 9's carry). Lanes 10..31 mirror lane 0.
-// The result is carried (limb < 2^w + 38), as fe_carry64's.
+// Results leaving the warp form are carried (limb < 2^w + 38), as fe_carry64's.
+
 // One parallel carry pass over 32-bit limbs (limb k keeps its low w bits and
 // takes lane k-1's carry; lane 0 takes 19 x lane 9's).
 __device__ __forceinline__ uint32_t fw_carry32(uint32_t h, int k, int base = 0) {
@@ -250,7 +251,8 @@ __device__ __forceinline__ uint32_t fw_carry32(uint32_t h, int k, int base = 0) 
 }
 
 // Column sums (< 2^61) -> limbs < 2^w + 2^20 in two parallel passes: enough
-// for the next product's bounds (and for fe_sub's bias); fw_out adds a third.
+// for the next product's bounds (and for fe_sub's bias); a result leaving the
+// warp form takes a third (fw_carry32).
 __device__ __forceinline__ uint32_t fw_carry(uint64_t h, int k, int base = 0) {
     const int w = (k & 1) ? 25 : 26;
     const int src = base + (k == 0 ? 9 : k - 1);
