@@ -531,16 +531,21 @@ def main():
     ms_per_step = ms / a.steps
     value = world * n / (ms_per_step * 1e-3)
     prof_path = os.environ.get("POSLO_PROFILE_STEP")
-    if prof_path and rank == 0:  # diagnostics only, after (never inside) the timed region
+    if prof_path:  # diagnostics only, after (never inside) the timed region; every rank
+        # runs the step (it holds collectives), rank 0 records it
+        from contextlib import nullcontext
+
         from torch.profiler import ProfilerActivity, profile
-        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+        with (profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) if rank == 0
+              else nullcontext()) as prof:
             t0 = time.perf_counter()
             step(bdev)
             torch.cuda.synchronize()
             host_ms = (time.perf_counter() - t0) * 1e3
-        prof.export_chrome_trace(prof_path)
-        print(f"profiled step: {host_ms:.2f} ms wall", file=sys.stderr)
-        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40), file=sys.stderr)
+        if rank == 0:
+            prof.export_chrome_trace(prof_path)
+            print(f"profiled step: {host_ms:.2f} ms wall", file=sys.stderr)
+            print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40), file=sys.stderr)
 
     # ---- e2e: same metric through the C-ABI with the log in pinned HOST memory
     v.enable_timing(False)
