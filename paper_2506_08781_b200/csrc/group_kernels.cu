@@ -112,9 +112,9 @@ __global__ void k_validate(const uint8_t* __restrict__ pts, uint32_t n, uint8_t*
 
 // ---- comb tables ------------------------------------------------------------
 // Builds the fixed-base table of P (decoded from `enc`, or the ristretto255
-// generator when enc == nullptr). Stage A (one thread): P_k = 16^k P. Stage B
-// (one thread per entry): (i+1) P_k in cached form.
-// W = 4: 64 powers 16^k P; W = 8: 32 powers 256^k P.
+// generator when enc == nullptr). Stage A (one warp, warp-cooperative field
+// products): the 64 powers P_k = 16^k P. Stage B (one thread per entry): the
+// multiples of P_k (radix 16 / 256 / 2^16 fills) in cached form.
 template <int W>
 __global__ void k_table_pow(const uint8_t* __restrict__ enc, gpt* __restrict__ pk, int* bad) {
     // one warp: the decode and the 252-doubling chain warp-cooperatively
