@@ -198,6 +198,11 @@ struct Prepared {
     // e~ are final on stream st, so the caller can start its per-epoch
     // checks for that piece while the next one hashes.
     std::function<int(uint32_t, uint32_t, cudaStream_t)> on_piece;
+    // Runs right after the seed kernel is queued, before any hashing: a side-
+    // stream job queued here (the R-hat decode) starts behind the seeds and
+    // runs beside the hashing instead of delaying the seeds and the first
+    // hash CTAs.
+    std::function<int()> on_seeded;
 };
 
 // Entries per tile of the generic / variable-length kernels (<= 1024, the
@@ -524,6 +529,10 @@ int run_hash(poslo_gpu_ctx* ctx, const poslo_batch* b, Prepared& P, poslo_error*
                            ctx->d_t0, s);
     }
     ctx->launches += n_ep ? 1 : 0;
+    if (P.on_seeded) {
+        rc = P.on_seeded();
+        if (rc) return rc;
+    }
     mark(ctx, kEvHash);
 
     // tiles
@@ -968,6 +977,13 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
 static bool check16_split() {
     const char* e = std::getenv("POSLO_CHECK16");
     return e && std::strcmp(e, "split") == 0;
+}
+
+// POSLO_DECODE_EARLY=1: queue the R-hat decode before the seeds (A/B knob;
+// default: behind the seed kernel, beside the hashing)
+static bool decode_early() {
+    const char* e = std::getenv("POSLO_DECODE_EARLY");
+    return e && std::strcmp(e, "1") == 0;
 }
 
 static bool epoch_decode16() {
@@ -1605,6 +1621,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     void* d_pts = nullptr;
     uint8_t* d_ok = nullptr;
     int rc;
+    bool want_decode = false;
     if (split) {  // tables and R-hat decoding ahead of (and overlapping) the hashing
         int* d_flags;
         ENSURE(b_flags, 4, d_flags);
@@ -1616,12 +1633,15 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         // R-hat decoded on the side stream while the log is hashed: the checks
         // then compare ristretto classes (POSLO_EPOCH_DECODE=0: radix-2^16
         // checks encode instead, A/B knob)
-        if (n < comb16_min() || epoch_decode16()) {
+        want_decode = n < comb16_min() || epoch_decode16();
+        if (want_decode && decode_early()) {
             rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
             if (rc) return rc;
+            want_decode = false;
         }
     }
     Prepared P;
+    if (want_decode) P.on_seeded = [&]() { return start_decode(ctx, n, d_r, &d_pts, &d_ok, err); };
     uint8_t* d_vpipe = nullptr;
     bool piped = false;
     if (split && b->device_resident) {  // checks of piece q overlap the hashing of piece q + 1
@@ -1776,11 +1796,12 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
     }
     // R-hat decoded once, on the side stream during hashing, for the fold and
     // the checks (ristretto class compare: no encoding per check)
-    if (split) {
+    if (split && decode_early()) {
         rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
         if (rc) return rc;
     }
     Prepared P;
+    if (split && !decode_early()) P.on_seeded = [&]() { return start_decode(ctx, n, d_r, &d_pts, &d_ok, err); };
     // per-epoch verdicts stay on the device as the fold mask
     uint8_t* d_verdict;
     ENSURE(b_verdict, std::max<uint32_t>(n, 1), d_verdict);
