@@ -34,7 +34,8 @@ extern "C" {  // defined with the batched-check entry points below
 static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
                         poslo_error* err);
 static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
-                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err);
+                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err,
+                        uint8_t* d_scr16e = nullptr);
 }
 
 namespace {
@@ -972,11 +973,23 @@ int ensure_tables(poslo_gpu_ctx* ctx, const uint8_t y[32], int* d_flags, poslo_e
     return POSLO_OK;
 }
 
-// POSLO_CHECK16=split: radix-2^16 checks against decoded R-hat as 8 lanes per
-// check (k_check_split16) instead of a thread per check (A/B knob).
-static bool check16_split() {
+// Form of the radix-2^16 batched checks (POSLO_CHECK16, A/B knob):
+//   sqrt    no square root per check: combs -> one batched inversion per 32
+//           checks -> encode(P) == R-hat by squares (launch_check16e); the
+//           default for per-epoch verdicts
+//   decode  a thread per check against R-hat decoded on a side stream while the
+//           log is hashed (k_check_thread16d); distillation always decodes R-hat
+//           (it folds the decoded points) and checks this way
+//   split   8 lanes per check against decoded R-hat (k_check_split16)
+//   encode  a thread per check comparing encodings (k_check_thread16)
+enum class Check16 { Sqrt, Decode, Split, Encode };
+static Check16 check16_mode() {
     const char* e = std::getenv("POSLO_CHECK16");
-    return e && std::strcmp(e, "split") == 0;
+    if (!e) return Check16::Sqrt;
+    if (!std::strcmp(e, "decode")) return Check16::Decode;
+    if (!std::strcmp(e, "split")) return Check16::Split;
+    if (!std::strcmp(e, "encode")) return Check16::Encode;
+    return Check16::Sqrt;
 }
 
 // POSLO_DECODE_EARLY=1: queue the R-hat decode before the seeds (A/B knob;
@@ -986,20 +999,18 @@ static bool decode_early() {
     return e && std::strcmp(e, "1") == 0;
 }
 
-static bool epoch_decode16() {
-    const char* e = std::getenv("POSLO_EPOCH_DECODE");
-    return !(e && std::strcmp(e, "0") == 0);
-}
-
 // The batched checks on the widest tables ensure_tables built: radix 2^16, a
 // thread per check, comparing ristretto classes against R-hat decoded ahead
 // (d_pts, d_ok) or, without it, encodings (d_r); radix 256, 8 lanes per check
 // against decoded R-hat.
 void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
-                   const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st) {
-    if (xwide && !d_pts)
+                   const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st,
+                   uint8_t* d_scr16e = nullptr) {
+    if (xwide && !d_pts && d_scr16e)  // no square root per check (launch_check16e)
+        launch_check16e(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, d_scr16e, d_verdict, st);
+    else if (xwide && !d_pts)
         launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, nullptr, d_verdict, st);
-    else if (xwide && check16_split())
+    else if (xwide && check16_mode() == Check16::Split)
         launch_check_split16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
     else if (xwide)
         launch_check_thread16d(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_pts, d_ok, d_verdict, st);
@@ -1180,7 +1191,7 @@ void poslo_gpu_destroy(poslo_gpu_ctx* ctx) {
                       &ctx->b_seg32, &ctx->b_out_s, &ctx->b_out_r, &ctx->b_dpts, &ctx->b_dok,
                       &ctx->b_scan_exit, &ctx->b_scan_cnt, &ctx->b_scan_start, &ctx->b_scan_base,
                       &ctx->b_scan_off, &ctx->b_scan_state, &ctx->b_seg_e, &ctx->b_out_e, &ctx->b_ppre_s, &ctx->b_ppre_r,
-                      &ctx->b_ppre};
+                      &ctx->b_ppre, &ctx->b_scr16e};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->d_t0) cudaFree(ctx->d_t0);
@@ -1574,9 +1585,10 @@ static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void
 }
 
 static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
-                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err) {
+                        const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err,
+                        uint8_t* d_scr16e) {
     if (d_pts) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode
-    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_r, d_pts, d_ok, d_verdict, ctx->stream);
+    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_r, d_pts, d_ok, d_verdict, ctx->stream, d_scr16e);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     return POSLO_OK;
@@ -1622,6 +1634,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     uint8_t* d_ok = nullptr;
     int rc;
     bool want_decode = false;
+    uint8_t* d_scr16e = nullptr;  // scratch of the square-root-free checks (Check16::Sqrt)
     if (split) {  // tables and R-hat decoding ahead of (and overlapping) the hashing
         int* d_flags;
         ENSURE(b_flags, 4, d_flags);
@@ -1630,10 +1643,12 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         if (rc) return rc;
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
-        // R-hat decoded on the side stream while the log is hashed: the checks
-        // then compare ristretto classes (POSLO_EPOCH_DECODE=0: radix-2^16
-        // checks encode instead, A/B knob)
-        want_decode = n < comb16_min() || epoch_decode16();
+        // radix 256 (n < comb16_min) and the decode / split forms check against
+        // R-hat decoded while the log is hashed; the default radix-2^16 form
+        // needs no decode (launch_check16e)
+        const Check16 mode = check16_mode();
+        want_decode = n < comb16_min() || mode == Check16::Decode || mode == Check16::Split;
+        if (n >= comb16_min() && mode == Check16::Sqrt) ENSURE(b_scr16e, (size_t)n * kCheck16eScratch, d_scr16e);
         if (want_decode && decode_early()) {
             rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
             if (rc) return rc;
@@ -1652,7 +1667,8 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
                           d_r + 32 * (size_t)e0,
                           d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
-                          d_ok ? d_ok + e0 : nullptr, d_vpipe + e0, ctx->side);
+                          d_ok ? d_ok + e0 : nullptr, d_vpipe + e0, ctx->side,
+                          d_scr16e ? d_scr16e + kCheck16eScratch * (size_t)e0 : nullptr);
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1682,7 +1698,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     } else if (split) {
         uint8_t* d_verdict;
         ENSURE(b_verdict, n, d_verdict);
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err, d_scr16e);
         if (rc) return rc;
         CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));

@@ -48,7 +48,7 @@ struct poslo_gpu_ctx {
     uint32_t* d_t0 = nullptr;
     DevBuf b_epochs, b_x0, b_partial, b_etilde, b_sum, b_scratch, b_tiles, b_starts, b_tbegin,
         b_err, b_flags, b_payload, b_offsets, b_e, b_s, b_r, b_enc, b_verdict, b_mask, b_seg,
-        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state, b_seg_e, b_out_e, b_ppre_s, b_ppre_r, b_ppre;
+        b_y, b_pts, b_foldscratch, b_rhat, b_pre, b_starts_ds, b_seg32, b_out_s, b_out_r, b_dpts, b_dok, b_scan_exit, b_scan_cnt, b_scan_start, b_scan_base, b_scan_off, b_scan_state, b_seg_e, b_out_e, b_ppre_s, b_ppre_r, b_ppre, b_scr16e;
     // fixed-base comb tables: generator (built once) and the last Y seen
     void* d_tabB = nullptr;
     void* d_tabY = nullptr;

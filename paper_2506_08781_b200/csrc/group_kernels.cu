@@ -316,6 +316,66 @@ __global__ void __launch_bounds__(128, POSLO_CHECK16D_MINB) k_check_thread16d(co
     verdict[i] = (rok[i] && rist_equal(acc, R[i])) ? 1 : 0;
 }
 
+// ---- radix-2^16 checks with no square root per check ----------------------
+// (rist_encoding_matches): stage 1 the combs -> P and u2 = XY, stage 2 one
+// batched inversion of u2 per chunk of kInvChunk checks (Montgomery's trick:
+// 3 products per element + one inversion per chunk), stage 3 the verdict
+// encode(P) == R-hat from P, 1 / u2 and R-hat's bytes (~15 products). Against
+// decoding R-hat (an inverse square root, ~265 products) + the class compare.
+constexpr uint32_t kInvChunk = 32;
+
+__global__ void __launch_bounds__(128) k_check16e_comb(const gcached* __restrict__ tabY,
+                                                       const gcached* __restrict__ tabB, uint32_t n,
+                                                       const uint32_t* __restrict__ e,
+                                                       const uint32_t* __restrict__ s, gpt* __restrict__ P,
+                                                       fe* __restrict__ u2) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t v[8];
+    gpt acc = pt_identity();
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = e[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabY, v);
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = s[(size_t)i * 8 + k];
+    acc = comb65536_mul_add(acc, tabB, v);
+    P[i] = acc;
+    const fe t = fe_mul(acc.X, acc.Y);
+    u2[i] = fe_is_zero(t) ? fe_one() : t;  // the identity class (u2 = 0) is decided without 1 / u2
+}
+
+// a[lo, hi) <- 1 / a[lo, hi) for the chunk of thread t; pre[] holds the prefix products
+__global__ void __launch_bounds__(64) k_batch_invert(fe* __restrict__ a, fe* __restrict__ pre, uint32_t n) {
+    const uint32_t lo = (blockIdx.x * blockDim.x + threadIdx.x) * kInvChunk;
+    if (lo >= n) return;
+    const uint32_t hi = min(n, lo + kInvChunk);
+    fe acc = a[lo];
+    pre[lo] = acc;
+#pragma unroll 1
+    for (uint32_t i = lo + 1; i < hi; i++) {
+        acc = fe_mul(acc, a[i]);
+        pre[i] = acc;
+    }
+    fe inv = fe_invert(acc);
+#pragma unroll 1
+    for (uint32_t i = hi - 1; i > lo; i--) {
+        const fe ai = a[i];
+        a[i] = fe_mul(inv, pre[i - 1]);
+        inv = fe_mul(inv, ai);
+    }
+    a[lo] = inv;
+}
+
+__global__ void __launch_bounds__(128) k_check16e_verify(const gpt* __restrict__ P, const fe* __restrict__ inv_u2,
+                                                         uint32_t n, const uint8_t* __restrict__ r,
+                                                         uint8_t* __restrict__ verdict) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t b[32];
+    load32(r + (size_t)i * 32, b);
+    verdict[i] = rist_encoding_matches(P[i], inv_u2[i], b) ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(128) k_check_thread(const gcached* __restrict__ tabY,
                                                       const gcached* __restrict__ tabB, uint32_t n,
                                                       const uint32_t* __restrict__ e,
@@ -750,6 +810,19 @@ void launch_check_thread16d(const void* d_tabY16, const void* d_tabB16, uint32_t
     k_check_thread16d<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
                                                       static_cast<const gcached*>(d_tabB16), n, d_e, d_s,
                                                       static_cast<const gpt*>(d_pts), d_ok, d_verdict);
+}
+
+void launch_check16e(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
+                     const uint8_t* d_r, uint8_t* d_scratch, uint8_t* d_verdict, cudaStream_t s) {
+    if (!n) return;
+    gpt* P = reinterpret_cast<gpt*>(d_scratch);
+    fe* u2 = reinterpret_cast<fe*>(d_scratch + (size_t)n * sizeof(gpt));
+    fe* pre = u2 + n;
+    k_check16e_comb<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
+                                                    static_cast<const gcached*>(d_tabB16), n, d_e, d_s, P, u2);
+    const uint32_t chunks = (n + kInvChunk - 1) / kInvChunk;
+    k_batch_invert<<<(chunks + 63) / 64, 64, 0, s>>>(u2, pre, n);
+    k_check16e_verify<<<(n + 127) / 128, 128, 0, s>>>(P, u2, n, d_r, d_verdict);
 }
 
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,

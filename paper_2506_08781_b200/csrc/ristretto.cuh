@@ -738,6 +738,39 @@ PHD gpt comb65536_mul_add(gpt acc, const gcached* tab, const uint32_t s[8]) {
     return acc;
 }
 
+// encode(P) == r without a square root. In RFC 9496 §4.3.2 every branch of
+// the encoding depends on z_inv = den1 den2 T = T / u2 (u1 = Z^2 - Y^2,
+// u2 = XY, invsqrt^2 = 1 / (u1 u2^2): the sign of invsqrt cancels), and the
+// output is s = |invsqrt K| with K = (rotate ? u1 INVSQRT_A_MINUS_D : u2)(Z - y).
+// For a valid point W = u1 u2^2 is a square, so with r's s canonical and
+// non-negative: encode(P) == r  <=>  s^2 W == K^2 (the square map is
+// injective on non-negative elements). u2 == 0 is the identity class, which
+// encodes to 0. inv_u2 = 1 / u2 comes from a batched inversion
+// (k_batch_invert); checked against the encoding on random points, torsion
+// representatives and rescaled coordinates (tests/test_gpu_parity.py).
+PHD bool rist_encoding_matches(const gpt& p, const fe& inv_u2, const uint8_t r[32]) {
+    const fe s = fe_from_bytes_le(r);
+    uint8_t rb[32];
+    fe_to_bytes_le(s, rb);
+    uint32_t diff = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) diff |= rb[i] ^ r[i];
+    if (diff || (r[0] & 1)) return false;  // encodings are canonical and non-negative
+    const fe u2 = fe_mul(p.X, p.Y);
+    if (fe_is_zero(u2)) return fe_is_zero(s);
+    const fe u1 = fe_mul(fe_add(p.Z, p.Y), fe_sub(p.Z, p.Y));
+    const fe z_inv = fe_mul(p.T, inv_u2);
+    const bool rotate = fe_is_neg(fe_mul(p.T, z_inv));
+    const fe sqrtm1 = FE_CONST(FE_SQRTM1_LIMBS);
+    const fe x = rotate ? fe_mul(p.Y, sqrtm1) : p.X;
+    fe y = rotate ? fe_mul(p.X, sqrtm1) : p.Y;
+    if (fe_is_neg(fe_mul(x, z_inv))) y = fe_neg(y);
+    const fe k = rotate ? fe_mul(u1, FE_CONST(FE_INVSQRT_A_MINUS_D_LIMBS)) : u2;
+    const fe K = fe_mul(k, fe_sub(p.Z, y));
+    const fe W = fe_mul(u1, fe_sq(u2));
+    return fe_eq(fe_mul(fe_sq(s), W), fe_sq(K));
+}
+
 // Ristretto equality of classes (RFC 9496 §4.3.3): X1*Y2 == Y1*X2 or
 // Y1*Y2 == X1*X2. Equal classes <=> equal canonical encodings, so comparing
 // against a decoded R replaces encoding P (the reference's byte compare).

@@ -497,7 +497,7 @@ def test_chunked_varlen_host_path_matches_device_resident(verifier):
     assert a == h
 
 
-@pytest.mark.parametrize("comb16", [False, "thread", "encode", "split"])
+@pytest.mark.parametrize("comb16", [False, "sqrt", "decode", "encode", "split"])
 @pytest.mark.parametrize("resident", [0, 1])
 def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
     """> 1024 per-epoch checks take the split path (R-hat decoded on a side
@@ -505,15 +505,13 @@ def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
     hashing): signatures from the reference derivation (signer.py) verify, and
     exactly the tampered epochs fail — on the radix-256 combs (8 lanes per
     check) and (POSLO_COMB16_MIN = 1) on the radix-2^16 combs large batches
-    take by default, in each check form: a thread per check against decoded
-    R-hat (default), encoding compare (POSLO_EPOCH_DECODE=0), 8 lanes per
-    check (POSLO_CHECK16=split). Device-resident batches also run
+    take by default, in each check form (POSLO_CHECK16): no square root per
+    check (sqrt, the default), a thread per check against decoded R-hat
+    (decode), encoding compare (encode), 8 lanes per check (split). Device-resident batches also run
     distill_coarse (whose checks always use the decoded R-hat)."""
     monkeypatch.setenv("POSLO_COMB16_MIN", "1" if comb16 else "4294967295")
-    if comb16 == "encode":
-        monkeypatch.setenv("POSLO_EPOCH_DECODE", "0")
-    if comb16 == "split":
-        monkeypatch.setenv("POSLO_CHECK16", "split")
+    if comb16:
+        monkeypatch.setenv("POSLO_CHECK16", comb16)
     import ctypes
 
     import torch
@@ -561,6 +559,49 @@ def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
                        ctypes.c_void_p(s_dev.data_ptr()), ctypes.c_void_p(r_dev.data_ptr()),
                        ctypes.c_void_p(seg.ctypes.data), 2, dverd, so, ro)
         assert dverd.raw == verd.raw
+    assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
+
+
+@pytest.mark.parametrize("mode", ["sqrt", "decode", "encode", "split"])
+def test_epoch_checks_on_adversarial_r_hats(verifier, mode, monkeypatch):
+    """Per-epoch verdicts when R-hat_i is not the signer's commitment: the
+    identity encoding, s = p (non-canonical), an odd (negative) s, bit 255
+    set, and valid encodings of other points (including -R and R + one
+    generator). Every form of the radix-2^16 check must reject exactly those
+    epochs, as the reference's byte compare encode(e Y + s B) == R does."""
+    monkeypatch.setenv("POSLO_COMB16_MIN", "1")
+    monkeypatch.setenv("POSLO_CHECK16", mode)
+    from paper_2506_08781_b200 import signer
+    from oracle import ristretto as R
+    api = A()
+    n1, n2 = 2048, 2
+    suite = api.SuiteConfig(1, n1, n2, 8)
+    rng = random.Random(43)
+    sk = signer.PoslocSecretKey(suite, rng.randrange(1, O.L).to_bytes(32, "little"),
+                                bytes(rng.getrandbits(8) for _ in range(16)),
+                                bytes(rng.getrandbits(8) for _ in range(16)))
+    batches = {i: [bytes(rng.getrandbits(8) for _ in range(32)) for _ in range(n2)] for i in range(n1)}
+    pk = signer.kg_public_key(sk, verifier)
+    s_hats = signer.sign_epochs(sk, batches, verifier)
+    gen = R.encode(R.BASE)
+    def neg(enc):
+        x, y, z, t = R.decode(enc)
+        return R.encode(((-x) % R.P, y, z, (-t) % R.P))
+    bad = {
+        3: bytes(32),                                              # identity
+        100: R.P.to_bytes(32, "little"),                           # s = p: non-canonical
+        101: (R.P + 2).to_bytes(32, "little"),                     # s = p + 2: non-canonical
+        777: (int.from_bytes(pk.r_hats[777], "little") | 1).to_bytes(32, "little"),  # odd s
+        900: (int.from_bytes(pk.r_hats[900], "little") | (1 << 255)).to_bytes(32, "little"),  # bit 255
+        1500: neg(pk.r_hats[1500]),                                # -R
+        2047: R.group_combine(pk.r_hats[2047], gen),               # R + B
+    }
+    r_hats = dict(pk.r_hats)
+    for i, r in bad.items():
+        assert r != pk.r_hats[i]
+        r_hats[i] = r
+    pk2 = api.PoslocPublicKey(pk.suite, pk.y, r_hats)
+    got = verifier.epoch_verify(pk2, batches, s_hats, sk.root_stack())
     assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
 
 
