@@ -33,9 +33,22 @@ using namespace poslo_gpu;
 extern "C" {  // defined with the batched-check entry points below
 static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
                         poslo_error* err);
+// Scratch of the square-root-free radix-2^16 checks (launch_check16e): the
+// points P = e Y + s B of every check, 1 / u2 and the inversion's prefixes.
+struct Scr16e {
+    uint8_t* P = nullptr;
+    uint8_t* u2 = nullptr;
+    uint8_t* pre = nullptr;
+    explicit operator bool() const { return P != nullptr; }
+    Scr16e at(uint32_t e0) const {  // the checks of epochs e0 ..
+        if (!P) return Scr16e{};
+        return Scr16e{P + kGptBytes * (size_t)e0, u2 + kFeBytes * (size_t)e0, pre + kFeBytes * (size_t)e0};
+    }
+};
 static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
                         const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err,
-                        uint8_t* d_scr16e = nullptr);
+                        const Scr16e& scr = Scr16e{});
+static int ensure_scr16e(poslo_gpu_ctx* ctx, uint32_t n, Scr16e& out, poslo_error* err);
 }
 
 namespace {
@@ -1005,9 +1018,9 @@ static bool decode_early() {
 // against decoded R-hat.
 void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
                    const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st,
-                   uint8_t* d_scr16e = nullptr) {
-    if (xwide && !d_pts && d_scr16e)  // no square root per check (launch_check16e)
-        launch_check16e(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, d_scr16e, d_verdict, st);
+                   const Scr16e& scr = Scr16e{}) {
+    if (xwide && !d_pts && scr)  // no square root per check (launch_check16e)
+        launch_check16e(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, scr.P, scr.u2, scr.pre, d_verdict, st);
     else if (xwide && !d_pts)
         launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, nullptr, d_verdict, st);
     else if (xwide && check16_mode() == Check16::Split)
@@ -1572,6 +1585,15 @@ int poslo_gpu_paver(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8_t y[32
 // R-hat decoding for batched checks: queued on the side stream behind
 // everything already on the main stream (their upload), so it overlaps the
 // hashing that follows; split_checks waits for it.
+static int ensure_scr16e(poslo_gpu_ctx* ctx, uint32_t n, Scr16e& out, poslo_error* err) {
+    uint8_t* base;
+    ENSURE(b_scr16e, (size_t)std::max<uint32_t>(n, 1) * kCheck16eScratch, base);
+    out.P = base;
+    out.u2 = base + kGptBytes * (size_t)n;
+    out.pre = out.u2 + kFeBytes * (size_t)n;
+    return POSLO_OK;
+}
+
 static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void** d_pts, uint8_t** d_ok,
                         poslo_error* err) {
     ENSURE(b_dpts, (size_t)std::max<uint32_t>(n, 1) * kPointBytes, *d_pts);
@@ -1586,9 +1608,9 @@ static int start_decode(poslo_gpu_ctx* ctx, uint32_t n, const uint8_t* d_r, void
 
 static int split_checks(poslo_gpu_ctx* ctx, uint32_t n, const uint32_t* d_e, const uint32_t* d_s, const uint8_t* d_r,
                         const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, poslo_error* err,
-                        uint8_t* d_scr16e) {
+                        const Scr16e& scr) {
     if (d_pts) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode
-    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_r, d_pts, d_ok, d_verdict, ctx->stream, d_scr16e);
+    launch_checks(ctx, n >= comb16_min(), n, d_e, d_s, d_r, d_pts, d_ok, d_verdict, ctx->stream, scr);
     ctx->launches += n ? 1 : 0;
     CU(cudaGetLastError());
     return POSLO_OK;
@@ -1634,7 +1656,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     uint8_t* d_ok = nullptr;
     int rc;
     bool want_decode = false;
-    uint8_t* d_scr16e = nullptr;  // scratch of the square-root-free checks (Check16::Sqrt)
+    Scr16e scr;  // the square-root-free checks (Check16::Sqrt)
     if (split) {  // tables and R-hat decoding ahead of (and overlapping) the hashing
         int* d_flags;
         ENSURE(b_flags, 4, d_flags);
@@ -1648,7 +1670,10 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
         // needs no decode (launch_check16e)
         const Check16 mode = check16_mode();
         want_decode = n < comb16_min() || mode == Check16::Decode || mode == Check16::Split;
-        if (n >= comb16_min() && mode == Check16::Sqrt) ENSURE(b_scr16e, (size_t)n * kCheck16eScratch, d_scr16e);
+        if (n >= comb16_min() && mode == Check16::Sqrt) {
+            rc = ensure_scr16e(ctx, n, scr, err);
+            if (rc) return rc;
+        }
         if (want_decode && decode_early()) {
             rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
             if (rc) return rc;
@@ -1667,8 +1692,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
                           d_r + 32 * (size_t)e0,
                           d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
-                          d_ok ? d_ok + e0 : nullptr, d_vpipe + e0, ctx->side,
-                          d_scr16e ? d_scr16e + kCheck16eScratch * (size_t)e0 : nullptr);
+                          d_ok ? d_ok + e0 : nullptr, d_vpipe + e0, ctx->side, scr.at(e0));
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1698,7 +1722,7 @@ int poslo_gpu_epoch_verify(poslo_gpu_ctx* ctx, const poslo_batch* b, const uint8
     } else if (split) {
         uint8_t* d_verdict;
         ENSURE(b_verdict, n, d_verdict);
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err, d_scr16e);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err, scr);
         if (rc) return rc;
         CU(cudaMemcpyAsync(verdicts, d_verdict, n, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
@@ -1810,14 +1834,24 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
         rc = sig_arrays(ctx, b, s_hats, r_hats, &d_s, &d_r, err);
         if (rc) return rc;
     }
-    // R-hat decoded once, on the side stream during hashing, for the fold and
-    // the checks (ristretto class compare: no encoding per check)
-    if (split && decode_early()) {
+    // Radix-2^16 checks with no square root per check keep the points
+    // P_i = e_i Y + s_i B, and for a valid epoch P_i IS R-hat_i as a ristretto
+    // element (encode(P_i) == R-hat_i), so the umbrella folds add the P_i of
+    // the valid epochs: R-hat is never decoded. The other forms decode R-hat
+    // once, on the side stream during hashing, for the fold and the checks.
+    const bool sqrt16 = split && n >= comb16_min() && check16_mode() == Check16::Sqrt;
+    Scr16e scr;
+    if (sqrt16) {
+        rc = ensure_scr16e(ctx, n, scr, err);
+        if (rc) return rc;
+    }
+    if (split && !sqrt16 && decode_early()) {
         rc = start_decode(ctx, n, d_r, &d_pts, &d_ok, err);
         if (rc) return rc;
     }
     Prepared P;
-    if (split && !decode_early()) P.on_seeded = [&]() { return start_decode(ctx, n, d_r, &d_pts, &d_ok, err); };
+    if (split && !sqrt16 && !decode_early())
+        P.on_seeded = [&]() { return start_decode(ctx, n, d_r, &d_pts, &d_ok, err); };
     // per-epoch verdicts stay on the device as the fold mask
     uint8_t* d_verdict;
     ENSURE(b_verdict, std::max<uint32_t>(n, 1), d_verdict);
@@ -1827,8 +1861,9 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
             CU(cudaEventRecord(ctx->ev_side[0], hs));
             CU(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
             launch_checks(ctx, n >= comb16_min(), e1 - e0, P.d_etilde + 8 * (size_t)e0, d_s + 8 * (size_t)e0,
-                          d_r + 32 * (size_t)e0, static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0,
-                          d_ok + e0, d_verdict + e0, ctx->side);
+                          d_r + 32 * (size_t)e0,
+                          d_pts ? static_cast<const uint8_t*>(d_pts) + kPointBytes * (size_t)e0 : nullptr,
+                          d_ok ? d_ok + e0 : nullptr, d_verdict + e0, ctx->side, scr.at(e0));
             ctx->launches += 1;
             piped = true;
             return POSLO_OK;
@@ -1847,7 +1882,7 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
         CU(cudaEventRecord(ctx->ev_side[1], ctx->side));
         CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));
     } else if (split) {
-        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err);
+        rc = split_checks(ctx, n, P.d_etilde, d_s, d_r, d_pts, d_ok, d_verdict, err, scr);
         if (rc) return rc;
     } else {
         launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, P.d_etilde, d_s,
@@ -1868,7 +1903,7 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
         ctx->launches += 1;
         CU(cudaMemcpyAsync(seg_e, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    if (split) {  // scalars as before; points from the decoded R-hats (no second decode)
+    if (split) {  // scalars as before; points from the checks' P_i or the decoded R-hats (no second decode)
         rc = segfold_dev(ctx, n, d_s, nullptr, d_verdict, seg, n_seg, seg_s, nullptr, err);
         if (rc) return rc;
         if (n_seg) {
@@ -1879,8 +1914,9 @@ int poslo_gpu_distill_coarse_ex(poslo_gpu_ctx* ctx, const poslo_batch* b, const 
             uint8_t* d_out;
             UPLOAD(b_seg32, seg, (size_t)(n_seg + 1) * 4, d_seg);
             ENSURE(b_out_r, (size_t)n_seg * 32, d_out);
-            CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode (side stream)
-            launch_segfold_decoded(d_pts, d_seg, n_seg, d_verdict, d_out, ctx->stream);
+            CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_side[1], 0));  // the R-hat decode / piped checks
+            launch_segfold_decoded(sqrt16 ? static_cast<const void*>(scr.P) : d_pts, d_seg, n_seg, d_verdict, d_out,
+                                   ctx->stream);
             ctx->launches += 1;
             CU(cudaMemcpyAsync(seg_r, d_out, (size_t)n_seg * 32, cudaMemcpyDeviceToHost, ctx->stream));
         }

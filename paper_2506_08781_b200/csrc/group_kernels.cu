@@ -813,11 +813,11 @@ void launch_check_thread16d(const void* d_tabY16, const void* d_tabB16, uint32_t
 }
 
 void launch_check16e(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
-                     const uint8_t* d_r, uint8_t* d_scratch, uint8_t* d_verdict, cudaStream_t s) {
+                     const uint8_t* d_r, void* d_P, void* d_u2, void* d_pre, uint8_t* d_verdict, cudaStream_t s) {
     if (!n) return;
-    gpt* P = reinterpret_cast<gpt*>(d_scratch);
-    fe* u2 = reinterpret_cast<fe*>(d_scratch + (size_t)n * sizeof(gpt));
-    fe* pre = u2 + n;
+    gpt* P = static_cast<gpt*>(d_P);
+    fe* u2 = static_cast<fe*>(d_u2);
+    fe* pre = static_cast<fe*>(d_pre);
     k_check16e_comb<<<(n + 127) / 128, 128, 0, s>>>(static_cast<const gcached*>(d_tabY16),
                                                     static_cast<const gcached*>(d_tabB16), n, d_e, d_s, P, u2);
     const uint32_t chunks = (n + kInvChunk - 1) / kInvChunk;

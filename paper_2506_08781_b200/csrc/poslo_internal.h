@@ -181,10 +181,12 @@ void launch_check_thread16d(const void* d_tabY16, const void* d_tabB16, uint32_t
                             const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
                             cudaStream_t s);
 // radix-2^16 checks without a square root per check (encode(P) == R-hat by
-// squares, one batched inversion per 32 checks); d_scratch >= n * kCheck16eScratch
+// squares, one batched inversion per 32 checks): d_P n x kGptBytes (the points
+// e Y + s B, kept: distillation folds them in place of the decoded R-hat),
+// d_u2 and d_pre n x kFeBytes scratch
 constexpr size_t kCheck16eScratch = kGptBytes + 2 * kFeBytes;
 void launch_check16e(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
-                     const uint8_t* d_r, uint8_t* d_scratch, uint8_t* d_verdict, cudaStream_t s);
+                     const uint8_t* d_r, void* d_P, void* d_u2, void* d_pre, uint8_t* d_verdict, cudaStream_t s);
 void launch_check_split16(const void* d_tabY16, const void* d_tabB16, uint32_t n, const uint32_t* d_e,
                           const uint32_t* d_s, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict,
                           cudaStream_t s);

@@ -559,6 +559,12 @@ def test_batched_epoch_checks_large(verifier, resident, comb16, monkeypatch):
                        ctypes.c_void_p(s_dev.data_ptr()), ctypes.c_void_p(r_dev.data_ptr()),
                        ctypes.c_void_p(seg.ctypes.data), 2, dverd, so, ro)
         assert dverd.raw == verd.raw
+        # umbrella folds of the valid epochs (the sqrt form folds its computed
+        # points e Y + s B instead of decoding R-hat: the same group elements)
+        for g in range(2):
+            ok = [i for i in range(seg[g], seg[g + 1]) if verd.raw[i]]
+            assert so.raw[32 * g:32 * g + 32] == verifier.scalar_sum([s_hats[i] for i in ok])
+            assert ro.raw[32 * g:32 * g + 32] == verifier.group_fold([pk.r_hats[i] for i in ok])
     assert [i for i, ok in enumerate(got) if not ok] == sorted(bad)
 
 
