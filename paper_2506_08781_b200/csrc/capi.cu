@@ -1045,9 +1045,16 @@ int group_check_dev(poslo_gpu_ctx* ctx, const uint8_t y[32], uint32_t n, const u
     if (rc) return rc;
     if (h_verdict) ENSURE(b_verdict, n, d_verdict);
     if (h_enc) ENSURE(b_enc, (size_t)n * 32, d_enc);
-    if (xwide)
+    if (xwide && !d_enc && d_r && d_verdict && check16_mode() == Check16::Sqrt) {
+        // verdicts only: no square root per check (launch_check16e)
+        Scr16e scr;
+        rc = ensure_scr16e(ctx, n, scr, err);
+        if (rc) return rc;
+        launch_check16e(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, scr.P, scr.u2, scr.pre, d_verdict,
+                        ctx->stream);
+    } else if (xwide) {
         launch_check_thread16(ctx->d_tabY16, ctx->d_tabB16, n, d_e, d_s, d_r, d_enc, d_verdict, ctx->stream);
-    else
+    } else
         launch_group_check_comb(ctx->d_tabY, ctx->d_tabB, ctx->d_tabY256, ctx->d_tabB256, n, d_e, d_s, d_r, d_enc,
                                 d_verdict, ctx->stream);
     ctx->launches += n ? 1 : 0;
