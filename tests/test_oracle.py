@@ -110,3 +110,55 @@ def test_group_check_oracle_vs_reference(name):
     assert r_fold == st.r_hat_agg
     ok = R.commit_check(st.pk.y, st.e_hat, st.s_hat) == r_fold
     assert ok == bool(st.d["paver"]) == bool(st.d["aver"])
+
+
+def _encoding_matches_by_squares(pt, r: bytes) -> bool:
+    """The device's square-root-free check (ristretto.cuh rist_encoding_matches):
+    every branch of RFC 9496 §4.3.2 depends only on z_inv = T / u2, and
+    s = |invsqrt K| with invsqrt^2 = 1 / (u1 u2^2), so for a canonical
+    non-negative s: encode(P) == r  <=>  s^2 u1 u2^2 == K^2."""
+    P = R.P
+    s = int.from_bytes(r, "little")
+    if s >= P or s & 1:
+        return False
+    x0, y0, z0, t0 = pt
+    u1 = (z0 + y0) * (z0 - y0) % P
+    u2 = x0 * y0 % P
+    if u2 == 0:
+        return s == 0
+    z_inv = t0 * pow(u2, P - 2, P) % P
+    rotate = R._is_neg(t0 * z_inv)
+    x, y = (y0 * R.SQRT_M1 % P, x0 * R.SQRT_M1 % P) if rotate else (x0, y0)
+    k = u1 * R.INVSQRT_A_MINUS_D % P if rotate else u2
+    if R._is_neg(x * z_inv):
+        y = (-y) % P
+    K = k * (z0 - y) % P
+    return s * s % P * (u1 * u2 % P * u2) % P == K * K % P
+
+
+def test_square_root_free_encoding_check_matches_encode():
+    """The identity behind the square-root-free checks, on the oracle: for
+    random multiples of the generator, their 4-torsion representatives and
+    projective rescalings, the check accepts the point's encoding and rejects
+    neighbours, other points, non-canonical and negative encodings."""
+    import random
+    rng = random.Random(2025)
+    P = R.P
+    torsion = [(0, 1, 1, 0), (0, P - 1, 1, 0), (R.SQRT_M1, 0, 1, 0), (P - R.SQRT_M1, 0, 1, 0)]
+    for t in torsion:  # the identity class encodes to 0
+        assert R.encode(t) == bytes(32) and _encoding_matches_by_squares(t, bytes(32))
+    for it in range(150):
+        pt = R.scalarmult(rng.randrange(1, R.L), R.BASE)
+        if it % 3 == 1:
+            pt = R.add(pt, torsion[rng.randrange(4)])
+        if it % 4 == 2:
+            z = rng.randrange(1, P)
+            pt = tuple(c * z % P for c in pt)
+        e = R.encode(pt)
+        assert _encoding_matches_by_squares(pt, e)
+        s = int.from_bytes(e, "little")
+        for wrong in (bytes(32), (s ^ 2).to_bytes(32, "little"), ((P - s) % P).to_bytes(32, "little"),
+                      (s + P).to_bytes(32, "little") if s + P < 2**256 else bytes(32),
+                      R.encode(R.add(pt, R.BASE))):
+            if wrong != e:
+                assert not _encoding_matches_by_squares(pt, wrong)
