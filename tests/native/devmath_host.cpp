@@ -262,6 +262,20 @@ int dm_check_split(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32]
     return rist_equal(E, T) ? 1 : 0;
 }
 
+// the square-root-free verdict of the per-epoch checks (rist_encoding_matches)
+// on P = e Y + s B, with 1 / u2 from fe_invert (the device batches it)
+int dm_check_sqrtfree(const uint8_t y[32], const uint8_t e[32], const uint8_t s[32], const uint8_t r[32]) {
+    gpt Y;
+    if (!rist_decode(y, Y)) return -1;
+    uint32_t ee[8], ss[8];
+    words_le(e, ee, 8);
+    words_le(s, ss, 8);
+    const gpt P = double_scalarmult(Y, ee, ss);
+    const fe u2 = fe_mul(P.X, P.Y);
+    const fe inv = fe_is_zero(u2) ? fe_one() : fe_invert(u2);
+    return rist_encoding_matches(P, inv, r) ? 1 : 0;
+}
+
 int dm_fold(uint32_t n, const uint8_t* pts, uint8_t out[32]) {
     gpt acc = pt_identity();
     for (uint32_t i = 0; i < n; i++) {

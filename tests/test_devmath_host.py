@@ -143,6 +143,30 @@ def test_group_ops(dm, kat):
         assert o.raw.hex() == c
 
 
+def test_square_root_free_check_host(dm, kat):
+    """ristretto.cuh rist_encoding_matches (the device's per-epoch verdict with
+    no square root) compiled for the CPU: accepts exactly the reference's
+    commit_check encoding, incl. e = s = 0 (the identity), and rejects other
+    points' encodings, negated / non-canonical / bit-255 variants."""
+    rows = kat["commit_check"]
+    P = 2**255 - 19
+    for i, (Y, e, s, Pk) in enumerate(rows):
+        Yb, eb, sb, Pb = (bytes.fromhex(x) for x in (Y, e, s, Pk))
+        assert dm.dm_check_sqrtfree(Yb, eb, sb, Pb) == 1
+        v = int.from_bytes(Pb, "little")
+        wrongs = [bytes.fromhex(rows[(i + 1) % len(rows)][3]), ((P - v) % P).to_bytes(32, "little"),
+                  (v | (1 << 255)).to_bytes(32, "little"), (v ^ 4).to_bytes(32, "little")]
+        if v + P < 2**256:
+            wrongs.append((v + P).to_bytes(32, "little"))
+        for w in wrongs:
+            if w != Pb:
+                assert dm.dm_check_sqrtfree(Yb, eb, sb, w) == 0
+    Y0 = bytes.fromhex(rows[0][0])
+    assert dm.dm_check_sqrtfree(Y0, bytes(32), bytes(32), bytes(32)) == 1  # identity encodes to 0
+    assert dm.dm_check_sqrtfree(Y0, bytes(32), bytes(32), bytes.fromhex(rows[0][3])) == int(
+        bytes.fromhex(rows[0][3]) == bytes(32))
+
+
 def test_signer_math_matches_reference_keys(dm):
     """kg / sig_epoch on the device math: R-hat_i =
     alpha^(sum_j nonce_to_scalar(r, i, j)) equals the reference's public key,
