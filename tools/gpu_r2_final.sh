@@ -21,7 +21,7 @@ $T 900 python bench.py --varlen --mode epoch --n2 1024 --log2n 22 --steps 5 --wa
 $T 900 python bench.py --mode tamper --n2 1024 --log2n 30 --tamper 1024 --steps 3 --warmup 3 --e2e-steps 0 > $O/bench_c5.json 2> $O/bench_c5.err
 $T 600 python bench.py --suite 2 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/bench_s2.json 2> $O/bench_s2.err
 $T 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --no-dropin > /dev/null 2>&1
-for spec in "k_hash_s1_l32r:--steps 3 --warmup 3" "k_hash_s1_var:--varlen --mode epoch --n2 1024 --log2n 25 --steps 1 --warmup 3" "k_check_thread16d:--mode epoch --n2 1024 --log2n 28 --steps 1 --warmup 3" "k_decode_pts:--mode epoch --n2 1024 --log2n 28 --steps 1 --warmup 3"; do
+for spec in "k_hash_s1_l32r:--steps 3 --warmup 3" "k_hash_s1_var:--varlen --mode epoch --n2 1024 --log2n 25 --steps 1 --warmup 3" "k_check16e_comb:--mode epoch --n2 1024 --log2n 28 --steps 1 --warmup 3" "k_batch_invert:--mode epoch --n2 1024 --log2n 28 --steps 1 --warmup 3"; do
   k=${spec%%:*}; args=${spec#*:}
   POSLO_PIPE_PIECES=1 $T 1200 ncu --set full --clock-control none --import-source on -f -k regex:$k -c 1 -o /tmp/$k python bench.py $args --no-cpu-baseline --e2e-steps 0 --no-dropin > /dev/null 2>&1
   ncu -i /tmp/$k.ncu-rep --page raw --csv > $O/ncu_${k}_raw.csv 2>&1
