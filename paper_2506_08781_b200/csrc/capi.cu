@@ -1012,9 +1012,11 @@ static bool decode_early() {
     return e && std::strcmp(e, "1") == 0;
 }
 
-// The batched checks on the widest tables ensure_tables built: radix 2^16, a
-// thread per check, comparing ristretto classes against R-hat decoded ahead
-// (d_pts, d_ok) or, without it, encodings (d_r); radix 256, 8 lanes per check
+// The batched checks on the widest tables ensure_tables built. Radix 2^16, a
+// thread per check: with scratch (scr) and no decoded R-hat, no square root
+// per check (launch_check16e, the points kept in scr.P); with R-hat decoded
+// ahead (d_pts, d_ok), the class compare (or 8 lanes per check, POSLO_CHECK16=
+// split); with neither, encodings compared (d_r). Radix 256: 8 lanes per check
 // against decoded R-hat.
 void launch_checks(poslo_gpu_ctx* ctx, bool xwide, uint32_t n, const uint32_t* d_e, const uint32_t* d_s,
                    const uint8_t* d_r, const void* d_pts, const uint8_t* d_ok, uint8_t* d_verdict, cudaStream_t st,
