@@ -145,11 +145,17 @@ def test_multi_context_byte_identical_at_scale(signed, multi):
         assert vd.value == 0
 
 
-def test_determinism_gate_1_2_4_8_members(signed):
+@pytest.mark.parametrize("comb16", [False, True])
+def test_determinism_gate_1_2_4_8_members(signed, comb16, monkeypatch):
     """SURVEY §8e's gate at G = 1, 2, 4 and 8 (members sharing the one GPU):
     every e~, e-hat, the per-epoch verdict bitmap and the distillation pieces
     (umbrellas of 96 epochs, not aligned with any shard cut) are byte-identical
-    to one device, and the coarse paver decision agrees."""
+    to one device, and the coarse paver decision agrees — on the radix-256
+    checks against decoded R-hat and (comb16: POSLO_COMB16_MIN = 1) on the
+    radix-2^16 checks with no square root, whose umbrella folds add the
+    checks' own points."""
+    if comb16:
+        monkeypatch.setenv("POSLO_COMB16_MIN", "1")
     v, sl = signed
     lib = v._lib
     pay, n1 = sl.host, sl.n1
